@@ -1,0 +1,85 @@
+"""In-tree build of the sm_100a product library and the test oracles.
+
+``python -m paper_2302_09883_b200.build`` compiles every ``csrc/*.cu`` with
+nvcc for sm_100a (``-gencode arch=compute_100a,code=sm_100a -lineinfo``) into
+``paper_2302_09883_b200/libwavegrid_b200.so``.  ``build_oracles()`` builds
+the C restatement (and, where /root/reference exists, the compiled
+reference) via ``oracle/Makefile`` — the checkers, never the product.
+"""
+from __future__ import annotations
+
+import concurrent.futures as cf
+import os
+import shutil
+import subprocess
+import sys
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+REPO = PKG.parent
+CSRC = PKG / "csrc"
+BUILD = REPO / "build" / "obj"
+LIB = PKG / "libwavegrid_b200.so"
+
+NVCC = os.environ.get("NVCC", shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+NVFLAGS = ARCH + [
+    "-O3",
+    "-lineinfo",
+    "-std=c++20",
+    "-fmad=false",  # no FMA contraction: the reference's Release build has none
+    "--expt-relaxed-constexpr",
+    "-Xcompiler", "-fPIC",
+    "-I", str(REPO / "include"),
+    "-I", str(CSRC),
+]
+
+
+def _sources():
+    return sorted(CSRC.glob("*.cu"))
+
+
+def _compile(src: Path, verbose_ptxas: bool) -> Path:
+    obj = BUILD / (src.stem + ".o")
+    deps = [src] + list(CSRC.glob("*.cuh")) + list(CSRC.glob("*.h")) + [REPO / "include" / "wavegrid_b200.h"]
+    if obj.exists() and all(obj.stat().st_mtime >= d.stat().st_mtime for d in deps):
+        return obj
+    cmd = [NVCC, *NVFLAGS, "-c", str(src), "-o", str(obj)]
+    if verbose_ptxas:
+        cmd[1:1] = ["-Xptxas", "-v"]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError(f"nvcc failed for {src.name}:\n{res.stdout}\n{res.stderr}")
+    if verbose_ptxas:
+        (BUILD / (src.stem + ".ptxas.txt")).write_text(res.stderr)
+    return obj
+
+
+def build_product(verbose_ptxas: bool = False, jobs: int | None = None) -> Path:
+    BUILD.mkdir(parents=True, exist_ok=True)
+    srcs = _sources()
+    with cf.ThreadPoolExecutor(max_workers=jobs or min(8, os.cpu_count() or 4)) as ex:
+        objs = list(ex.map(lambda s: _compile(s, verbose_ptxas), srcs))
+    if LIB.exists() and all(LIB.stat().st_mtime >= o.stat().st_mtime for o in objs):
+        return LIB
+    tmp = LIB.with_suffix(".so.tmp")
+    cmd = [NVCC, *ARCH, "-shared", "-o", str(tmp), *map(str, objs), "-lcudart"]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError(f"link failed:\n{res.stdout}\n{res.stderr}")
+    tmp.replace(LIB)
+    return LIB
+
+
+def build_oracles(reference: bool = True) -> None:
+    """Checker libraries for tests/ and the bench cpu_baseline leg."""
+    targets = ["c"]
+    if reference and Path("/root/reference/proj/include/wavegrid").is_dir():
+        targets.append("ref")
+    subprocess.run(["make", "-s", "-C", str(REPO / "oracle"), *targets], check=True)
+
+
+if __name__ == "__main__":
+    v = "-v" in sys.argv
+    print(build_product(verbose_ptxas=v))
+    build_oracles()

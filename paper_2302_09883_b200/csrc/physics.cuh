@@ -1,0 +1,161 @@
+// physics.cuh — the scheme updates (device), in the reference's exact
+// operation order.  Compiled with -fmad=false: no FMA contraction, matching
+// the reference's x86-64 Release build.
+#pragma once
+
+#include <cmath>
+
+namespace wg {
+
+// ---- transport: flux_upwind, solver.hpp:53-57 --------------------------------
+// smax/smin are std::max(speed, 0.0) / std::min(speed, 0.0) of the direction,
+// computed once on the host with the reference's formula.
+__host__ __device__ __forceinline__ double flux_upwind(double wl, double wr, double smax,
+                                                        double smin) {
+    return wl * smax + wr * smin;
+}
+
+// ---- shallow water: solver.hpp:74-199 ---------------------------------------
+struct SweStatus {
+    int err;  // 0 ok, 1 domain, 2 riemann
+};
+
+__device__ __forceinline__ double phi_side(double h, double hs, double g) {
+    if (h <= hs) return 2.0 * (sqrt(g * h) - sqrt(g * hs));
+    return (h - hs) * sqrt(g * (h + hs) / (2.0 * h * hs));
+}
+
+__device__ __forceinline__ double phi_side_deriv(double h, double hs, double g) {
+    if (h <= hs) return sqrt(g / h);
+    const double a = sqrt(g * (h + hs) / (2.0 * h * hs));
+    return a - (h - hs) * g / (4.0 * a * h * h);
+}
+
+// SweRiemann::solve_hstar, solver.hpp:107-124 (std::pow(x, 2) as x * x).
+__device__ __forceinline__ double solve_hstar(double g, double hl, double ul, double hr,
+                                              double ur, int& err) {
+    if (hl <= 0.0 || hr <= 0.0) {
+        err = 1;
+        return 1.0;
+    }
+    const double cl = sqrt(g * hl), cr = sqrt(g * hr);
+    const double b = 0.5 * (cl + cr) + 0.25 * (ul - ur);
+    double h = (b * b) / g;
+    h = (h < 1e-12) ? 1e-12 : h;
+    for (int it = 0; it < 100; ++it) {
+        const double f = phi_side(h, hl, g) + phi_side(h, hr, g) + ur - ul;
+        const double df = phi_side_deriv(h, hl, g) + phi_side_deriv(h, hr, g);
+        double dh = f / df;
+        if (h - dh <= 0.0) dh = h / 2.0;
+        h -= dh;
+        if (fabs(dh) < 1e-10) return h;
+    }
+    err = 2;
+    return h;
+}
+
+// flux_godunov_swe at xi = 0, solver.hpp:128-189.
+__device__ __forceinline__ void flux_swe(const double* wl, const double* wr, int nxi, int nyi,
+                                         double g, double* f, int& err) {
+    const double hl = wl[0], hr = wr[0];
+    if (hl <= 0.0 || hr <= 0.0) {
+        err = 1;
+        f[0] = f[1] = f[2] = 0.0;
+        return;
+    }
+    const double nx = (double)nxi, ny = (double)nyi;
+    const double ul = (wl[1] * nx + wl[2] * ny) / hl;
+    const double utl = (-wl[1] * ny + wl[2] * nx) / hl;
+    const double ur = (wr[1] * nx + wr[2] * ny) / hr;
+    const double utr = (-wr[1] * ny + wr[2] * nx) / hr;
+    const double xi = 0.0;
+    const double hs = solve_hstar(g, hl, ul, hr, ur, err);
+    const double us = 0.5 * (ul + ur) + 0.5 * (phi_side(hs, hr, g) - phi_side(hs, hl, g));
+    const double ut = xi <= us ? utl : utr;
+    double h, un;
+    if (xi <= us) {
+        const double cl = sqrt(g * hl), cs = sqrt(g * hs);
+        if (hs > hl) {
+            const double sl = ul - cl * sqrt(0.5 * (hs + hl) * hs / (hl * hl));
+            if (xi <= sl) { h = hl; un = ul; }
+            else { h = hs; un = us; }
+        } else {
+            const double head = ul - cl, tail = us - cs;
+            if (xi <= head) { h = hl; un = ul; }
+            else if (xi >= tail) { h = hs; un = us; }
+            else {
+                const double u = (ul + 2.0 * cl + 2.0 * xi) / 3.0;
+                const double c = (ul + 2.0 * cl - xi) / 3.0;
+                h = c * c / g;
+                un = u;
+            }
+        }
+    } else {
+        const double crr = sqrt(g * hr), cs = sqrt(g * hs);
+        if (hs > hr) {
+            const double sr = ur + crr * sqrt(0.5 * (hs + hr) * hs / (hr * hr));
+            if (xi >= sr) { h = hr; un = ur; }
+            else { h = hs; un = us; }
+        } else {
+            const double head = ur + crr, tail = us + cs;
+            if (xi >= head) { h = hr; un = ur; }
+            else if (xi <= tail) { h = hs; un = us; }
+            else {
+                const double u = (ur - 2.0 * crr + 2.0 * xi) / 3.0;
+                const double c = (-ur + 2.0 * crr + xi) / 3.0;
+                h = c * c / g;
+                un = u;
+            }
+        }
+    }
+    const double fn_mass = h * un;
+    const double fn_mom = h * un * un + 0.5 * g * h * h;
+    const double ft_mom = h * un * ut;
+    f[0] = fn_mass;
+    f[1] = fn_mom * nx - ft_mom * ny;
+    f[2] = fn_mom * ny + ft_mom * nx;
+}
+
+// ---- D2Q9 BGK (builder-defined, oracle/ref_shim.cpp) -------
+// q: 0 rest, 1 +x, 2 -x, 3 +y, 4 -y, 5 (+1,+1), 6 (-1,-1), 7 (+1,-1), 8 (-1,+1)
+__host__ __device__ constexpr int lbm_cx(int q) {
+    return q == 1 || q == 5 || q == 7 ? 1 : (q == 2 || q == 6 || q == 8 ? -1 : 0);
+}
+__host__ __device__ constexpr int lbm_cy(int q) {
+    return q == 3 || q == 5 || q == 8 ? 1 : (q == 4 || q == 6 || q == 7 ? -1 : 0);
+}
+__host__ __device__ constexpr double lbm_w(int q) {
+    return q == 0 ? 4.0 / 9.0 : (q < 5 ? 1.0 / 9.0 : 1.0 / 36.0);
+}
+
+__host__ __device__ __forceinline__ double lbm_cu(int q, double ux, double uy) {
+    switch (q) {
+        case 0: return 0.0;
+        case 1: return ux;
+        case 2: return -ux;
+        case 3: return uy;
+        case 4: return -uy;
+        case 5: return ux + uy;
+        case 6: return -(ux + uy);
+        case 7: return ux - uy;
+        default: return uy - ux;
+    }
+}
+
+__host__ __device__ __forceinline__ double lbm_feq(int q, double rho, double cu, double usq) {
+    const double t = ((1.0 + 3.0 * cu) + (4.5 * cu) * cu) - 1.5 * usq;
+    return (lbm_w(q) * rho) * t;
+}
+
+// BGK collide of the 9 pulled populations f (in place).
+__host__ __device__ __forceinline__ void lbm_collide(double (&f)[9], double omega) {
+    const double rho = ((((((((f[0] + f[1]) + f[2]) + f[3]) + f[4]) + f[5]) + f[6]) + f[7]) + f[8]);
+    const double jx = ((f[1] - f[2]) + (f[5] - f[6])) + (f[7] - f[8]);
+    const double jy = ((f[3] - f[4]) + (f[5] - f[6])) + (f[8] - f[7]);
+    const double ux = jx / rho, uy = jy / rho;
+    const double usq = ux * ux + uy * uy;
+#pragma unroll
+    for (int q = 0; q < 9; ++q) f[q] = f[q] - (f[q] - lbm_feq(q, rho, lbm_cu(q, ux, uy), usq)) * omega;
+}
+
+}  // namespace wg

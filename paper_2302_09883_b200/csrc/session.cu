@@ -1,0 +1,623 @@
+// session.cu — the device-resident compressed patch store and its step loop
+// (the B200 hot path), plus run() on top of it.
+//
+// One step (pipeline.hpp:194-289):
+//   k_patch_step<MAIN>   fused decode/ghost/FV/DWT/threshold/CSR/recon per patch
+//   k_patch_step<RAW>    patches whose cycle zeroed nothing keep the raw FV output
+//                        (skip rule, pipeline.hpp:243-249); exits at once if none
+//   k_metrics            deterministic reduction of the per-patch stats into the
+//                        step's MetricsRow (pipeline.hpp:260-274); resets the
+//                        bump allocator of the other pool
+// All three run on the session stream; nothing synchronises with the host
+// inside the step loop.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <vector>
+
+#include "common.cuh"
+#include "host_model.h"
+#include "patch_kernels.cuh"
+
+namespace wg {
+
+void direction_speeds(double alpha, double beta, double* smax, double* smin);  // ops.cu
+
+namespace {
+
+// ---- kernel table ---------------------------------------------------------
+struct KernelSet {
+    void (*main)(StepArgs);
+    void (*raw)(StepArgs);
+    void (*decode)(StepArgs);
+    int P;
+    int threads;
+    size_t smem;
+};
+
+template <int N, int L, int P>
+KernelSet make_set() {
+    using Lay = Layout<N, P>;
+    KernelSet k;
+    k.main = k_patch_step<N, L, P, MODE_MAIN>;
+    k.raw = k_patch_step<N, L, P, MODE_RAW>;
+    k.decode = k_patch_step<N, L, P, MODE_DECODE>;
+    k.P = P;
+    k.threads = Lay::NT;
+    k.smem = Lay::smem_bytes();
+    for (auto f : {k.main, k.raw, k.decode}) {
+        WG_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k.smem));
+    }
+    return k;
+}
+
+template <int N, int P, int L = 0>
+bool pick_levels(int levels, KernelSet& out) {
+    if constexpr ((1 << L) <= N - 1 && L <= kMaxLevels) {
+        if (levels == L) {
+            out = make_set<N, L, P>();
+            return true;
+        }
+        return pick_levels<N, P, L + 1>(levels, out);
+    } else {
+        return false;
+    }
+}
+
+KernelSet select_kernels(uint64_t n, int levels) {
+    KernelSet k{};
+    bool ok = false;
+    switch (n) {
+        case 9: ok = pick_levels<9, 7>(levels, k); break;
+        case 17: ok = pick_levels<17, 15>(levels, k); break;
+        case 33: ok = pick_levels<33, 8>(levels, k); break;
+        case 65: ok = pick_levels<65, 2>(levels, k); break;
+        default: break;
+    }
+    if (!ok)
+        raise(WG_INVALID_ARGUMENT, "device session: patch side " + std::to_string(n) + " with " +
+                                       std::to_string(levels) + " levels is not supported (n in 9,17,33,65)");
+    return k;
+}
+
+// ---- upload: raw store + edge lines from a grid buffer (one thread per
+// (patch, component, row)) ----------------------------------------------------
+__global__ void k_upload(const double* grid, uint32_t N, ShardGeom g, unsigned char* store,
+                         DirEntry* dir, EdgeSet e) {
+    const uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    const uint64_t per = (uint64_t)g.m * N;
+    if (t >= (uint64_t)g.npatch * per) return;
+    const uint32_t p = (uint32_t)(t / per);
+    const uint32_t q = (uint32_t)((t % per) / N);
+    const uint32_t i = (uint32_t)(t % N);
+    const uint64_t TP = N + 2, tcount = TP * TP;
+    const uint64_t block = round16((uint64_t)N * N * 8);
+    const uint64_t off = ((uint64_t)p * g.m + q) * block;
+    const double* src = grid + ((uint64_t)p * g.m + q) * tcount + (i + 1) * TP + 1;
+    double* dst = reinterpret_cast<double*>(store + off) + (uint64_t)i * N;
+    for (uint32_t j = 0; j < N; ++j) dst[j] = src[j];
+    if (i == 0) dir[(uint64_t)p * g.m + q] = DirEntry{off, 0u, DIR_RAW};
+    const uint32_t ar = p / g.P1, b = p % g.P1;
+    const uint64_t own = (((uint64_t)(ar + 1) * g.P1 + b) * g.m + q) * N;
+    const uint64_t oc = (((uint64_t)ar * g.P1 + b) * g.m + q) * N;
+    if (i == 1)
+        for (uint32_t j = 0; j < N; ++j) e.rowlo[own + j] = src[j];
+    if (i == N - 2)
+        for (uint32_t j = 0; j < N; ++j) e.rowhi[own + j] = src[j];
+    e.collo[oc + i] = src[1];
+    e.colhi[oc + i] = src[N - 2];
+}
+
+// ---- per-step metrics (pipeline.hpp:260-274) ------------------------------
+struct MetricsArgs {
+    const PatchStats* stats;
+    uint32_t npatch;
+    uint64_t dense_bytes;  // CompressedPatch::dense_bytes summed (0 if no compression)
+    uint64_t step;
+    double time;
+    int compress;
+    wg_metrics_row* rows;
+    uint64_t row_index;
+    uint32_t* raw_count;            // reset for the next step
+    unsigned long long* bump_next;  // pool written by the next step
+    double* mass_fv_out;            // per-step scheme-output mass (strict mode)
+};
+
+__global__ void __launch_bounds__(1024) k_metrics(MetricsArgs a) {
+    __shared__ unsigned long long s_comp[1024], s_nnz[1024], s_zero[1024];
+    __shared__ double s_mass[1024], s_mfv[1024];
+    const uint32_t t = threadIdx.x, nt = blockDim.x;
+    const uint32_t per = (a.npatch + nt - 1) / nt;
+    const uint32_t b = t * per, e = min(a.npatch, b + per);
+    unsigned long long comp = 0, nnz = 0, zero = 0;
+    double mass = 0.0, mfv = 0.0;
+    for (uint32_t p = b; p < e; ++p) {  // contiguous chunk, fixed order
+        const PatchStats s = a.stats[p];
+        comp += s.comp_bytes;
+        nnz += s.nnz;
+        zero += s.zeroed;
+        mass += s.mass;
+        mfv += s.mass_fv;
+    }
+    s_comp[t] = comp;
+    s_nnz[t] = nnz;
+    s_zero[t] = zero;
+    s_mass[t] = mass;
+    s_mfv[t] = mfv;
+    __syncthreads();
+    for (uint32_t s = nt / 2; s > 0; s >>= 1) {
+        if (t < s) {
+            s_comp[t] += s_comp[t + s];
+            s_nnz[t] += s_nnz[t + s];
+            s_zero[t] += s_zero[t + s];
+            s_mass[t] += s_mass[t + s];
+            s_mfv[t] += s_mfv[t + s];
+        }
+        __syncthreads();
+    }
+    if (t == 0) {
+        wg_metrics_row r;
+        r.step = a.step;
+        r.time = a.time;
+        r.dense_bytes = a.compress ? a.dense_bytes : 0;
+        r.compressed_bytes = a.compress ? s_comp[0] : 0;
+        r.ratio = (a.compress && s_comp[0] > 0) ? (double)r.dense_bytes / (double)s_comp[0] : 1.0;
+        r.nnz = a.compress ? s_nnz[0] : 0;
+        r.zeroed = a.compress ? s_zero[0] : 0;
+        r.global_mass = s_mass[0];
+        r.l2 = 0.0;
+        a.rows[a.row_index] = r;
+        a.mass_fv_out[a.row_index] = s_mfv[0];
+        *a.raw_count = 0;
+        *a.bump_next = 0;
+    }
+}
+
+}  // namespace
+
+// ---- the session -------------------------------------------------------------
+struct Session {
+    wg_run_config cfg{};
+    wg_shard shard{};
+    RunGeometry geo;
+    ShardGeom sg{};
+    uint32_t N = 0;
+    int levels = 0;
+    KernelSet ks{};
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+
+    // device memory
+    unsigned char* store[2] = {nullptr, nullptr};
+    DirEntry* dir[2] = {nullptr, nullptr};
+    EdgeSet edges[2]{};
+    double* edge_mem[2] = {nullptr, nullptr};
+    PatchStats* stats = nullptr;
+    unsigned long long* bump = nullptr;  // [2]
+    uint32_t* raw_list = nullptr;
+    uint32_t* raw_count = nullptr;
+    unsigned* err = nullptr;
+    wg_metrics_row* rows = nullptr;
+    double* mass_fv = nullptr;
+    uint64_t row_cap = 0;
+    uint64_t cap = 0;  // bytes per pool
+    uint64_t device_bytes = 0;
+
+    int cur = 0;  // pool/edges holding the current state
+    uint64_t step = 0;
+    double time = 0.0;
+    double thr[(kMaxLevels + 1) * (kMaxLevels + 1)] = {};
+
+    ~Session() { release(); }
+
+    void release() {
+        if (stream) cudaStreamSynchronize(stream);
+        for (int k = 0; k < 2; ++k) {
+            cudaFree(store[k]);
+            cudaFree(dir[k]);
+            cudaFree(edge_mem[k]);
+            store[k] = nullptr;
+            dir[k] = nullptr;
+            edge_mem[k] = nullptr;
+        }
+        cudaFree(stats);
+        cudaFree(bump);
+        cudaFree(raw_list);
+        cudaFree(raw_count);
+        cudaFree(err);
+        cudaFree(rows);
+        cudaFree(mass_fv);
+        stats = nullptr;
+        bump = nullptr;
+        raw_list = nullptr;
+        raw_count = nullptr;
+        err = nullptr;
+        rows = nullptr;
+        mass_fv = nullptr;
+        if (own_stream && stream) cudaStreamDestroy(stream);
+        stream = nullptr;
+    }
+
+    template <typename T>
+    T* dalloc(uint64_t count) {
+        T* p = nullptr;
+        if (count) {
+            WG_CUDA(cudaMalloc(&p, count * sizeof(T)));
+            device_bytes += count * sizeof(T);
+        }
+        return p;
+    }
+
+    uint64_t halo_doubles() const { return (uint64_t)sg.P1 * sg.m * N; }
+
+    void create(const wg_run_config& c, const wg_shard* sh, void* strm) {
+        cfg = c;
+        if (cfg.codec != 1) raise(WG_INVALID_ARGUMENT, "only Codec::csr is on the hot path");
+        if (cfg.scheme != WG_SCHEME_TRANSPORT)
+            raise(WG_INVALID_ARGUMENT, "device session: scheme not supported by this build");
+        geo = run_geometry(cfg);
+        if (geo.n[0] != geo.n[1]) raise(WG_INVALID_ARGUMENT, "device session: square patches only");
+        N = (uint32_t)geo.n[0];
+        levels = cfg.levels;
+        const uint64_t dims[2] = {geo.n[0], geo.n[1]};
+        plan_validate(dims, 2, levels);  // WaveletPlan{logical, levels}.validate(), pipeline.hpp:135-136
+        if (cfg.c < 0.0) raise(WG_INVALID_ARGUMENT, "apply_threshold: c must be >= 0");
+        if (cfg.threshold_mode < 0 || cfg.threshold_mode > 2)
+            raise(WG_INVALID_ARGUMENT, "band_threshold: unknown mode");
+        if (sh) shard = *sh;
+        else {
+            shard.rank = 0;
+            shard.world = 1;
+            WG_CUDA(cudaGetDevice(&shard.device));
+            shard.row_begin = 0;
+            shard.row_end = geo.splits[0];
+        }
+        if (shard.world < 1 || shard.row_begin >= shard.row_end || shard.row_end > geo.splits[0])
+            raise(WG_INVALID_ARGUMENT, "wg_shard: bad patch-row range");
+        WG_CUDA(cudaSetDevice(shard.device));
+        if (strm) stream = static_cast<cudaStream_t>(strm);
+        else {
+            WG_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+            own_stream = true;
+        }
+        sg.R = (uint32_t)(shard.row_end - shard.row_begin);
+        sg.P1 = (uint32_t)geo.splits[1];
+        sg.m = geo.m;
+        sg.world = shard.world;
+        sg.npatch = sg.R * sg.P1;
+        ks = select_kernels(N, levels);
+        // thresholds (threshold.hpp:31-47) — the "c == 0 or levels == 0"
+        // early return of apply_threshold (threshold.hpp:53) is T = 0.
+        if (cfg.c == 0.0 || levels == 0) std::fill(std::begin(thr), std::end(thr), 0.0);
+        else threshold_table_2d(levels, cfg.threshold_mode, cfg.c, cfg.threshold_alpha, thr);
+
+        const uint64_t raw_block = round16((uint64_t)N * N * 8);
+        const uint64_t blocks = (uint64_t)sg.npatch * sg.m;
+        cap = cfg.store_budget_bytes ? cfg.store_budget_bytes / 2 : blocks * raw_block;
+        cap = std::max<uint64_t>(cap, 16) & ~uint64_t(15);
+        for (int k = 0; k < 2; ++k) {
+            store[k] = dalloc<unsigned char>(cap);
+            dir[k] = dalloc<DirEntry>(blocks);
+            const uint64_t rowline = (uint64_t)(sg.R + 2) * sg.P1 * sg.m * N;
+            const uint64_t colline = (uint64_t)sg.R * sg.P1 * sg.m * N;
+            edge_mem[k] = dalloc<double>(2 * rowline + 2 * colline);
+            WG_CUDA(cudaMemsetAsync(edge_mem[k], 0, (2 * rowline + 2 * colline) * sizeof(double), stream));
+            edges[k].rowlo = edge_mem[k];
+            edges[k].rowhi = edge_mem[k] + rowline;
+            edges[k].collo = edge_mem[k] + 2 * rowline;
+            edges[k].colhi = edge_mem[k] + 2 * rowline + colline;
+        }
+        stats = dalloc<PatchStats>(sg.npatch);
+        bump = dalloc<unsigned long long>(2);
+        raw_list = dalloc<uint32_t>(sg.npatch);
+        raw_count = dalloc<uint32_t>(1);
+        err = dalloc<unsigned>(1);
+        WG_CUDA(cudaMemsetAsync(stats, 0, sizeof(PatchStats) * sg.npatch, stream));
+        WG_CUDA(cudaMemsetAsync(bump, 0, 2 * sizeof(unsigned long long), stream));
+        WG_CUDA(cudaMemsetAsync(raw_count, 0, sizeof(uint32_t), stream));
+        WG_CUDA(cudaMemsetAsync(err, 0, sizeof(unsigned), stream));
+        grow_rows(1024);
+    }
+
+    void grow_rows(uint64_t need) {
+        if (need <= row_cap) return;
+        uint64_t nc = std::max<uint64_t>(need, row_cap * 2);
+        wg_metrics_row* nr = nullptr;
+        double* nm = nullptr;
+        WG_CUDA(cudaMalloc(&nr, nc * sizeof(wg_metrics_row)));
+        WG_CUDA(cudaMalloc(&nm, nc * sizeof(double)));
+        if (rows) {
+            WG_CUDA(cudaMemcpyAsync(nr, rows, row_cap * sizeof(wg_metrics_row), cudaMemcpyDeviceToDevice, stream));
+            WG_CUDA(cudaMemcpyAsync(nm, mass_fv, row_cap * sizeof(double), cudaMemcpyDeviceToDevice, stream));
+            WG_CUDA(cudaStreamSynchronize(stream));
+            cudaFree(rows);
+            cudaFree(mass_fv);
+            device_bytes -= row_cap * (sizeof(wg_metrics_row) + sizeof(double));
+        }
+        rows = nr;
+        mass_fv = nm;
+        device_bytes += nc * (sizeof(wg_metrics_row) + sizeof(double));
+        row_cap = nc;
+    }
+
+    void upload_dev(const double* dgrid) {
+        const uint64_t raw_block = round16((uint64_t)N * N * 8);
+        const uint64_t need = (uint64_t)sg.npatch * sg.m * raw_block;
+        if (need > cap)
+            raise(WG_OUT_OF_MEMORY, "initial state does not fit the compressed-store budget");
+        cur = 0;
+        const uint64_t threads = (uint64_t)sg.npatch * sg.m * N;
+        k_upload<<<(unsigned)((threads + 127) / 128), 128, 0, stream>>>(dgrid, N, sg, store[cur], dir[cur],
+                                                                         edges[cur]);
+        WG_LAUNCH_CHECK("upload");
+        const unsigned long long used = need;
+        WG_CUDA(cudaMemcpyAsync(bump + cur, &used, sizeof used, cudaMemcpyHostToDevice, stream));
+        WG_CUDA(cudaMemsetAsync(bump + (1 - cur), 0, sizeof(unsigned long long), stream));
+        WG_CUDA(cudaStreamSynchronize(stream));  // `used` lives on this stack frame
+        step = 0;
+        time = 0.0;
+    }
+
+    void upload_host(const double* hgrid) {
+        const uint64_t n = (uint64_t)sg.npatch * sg.m * geo.tcount;
+        DevBuf<double> d(n);
+        WG_CUDA(cudaMemcpyAsync(d.p, hgrid, n * sizeof(double), cudaMemcpyHostToDevice, stream));
+        upload_dev(d.p);
+    }
+
+    StepArgs step_args(int src, int dst) const {
+        StepArgs a{};
+        a.store_in = store[src];
+        a.dir_in = dir[src];
+        a.ein = edges[src];
+        a.store_out = store[dst];
+        a.dir_out = dir[dst];
+        a.eout = edges[dst];
+        a.stats = stats;
+        a.bump_out = bump + dst;
+        a.cap_out = cap;
+        a.raw_list = raw_list;
+        a.raw_count = raw_count;
+        a.raw_capacity = sg.npatch;
+        a.err = err;
+        a.g = sg;
+        std::memcpy(a.thr, thr, sizeof(thr));
+        return a;
+    }
+
+    void do_step(double dt) {
+        const int src = cur, dst = 1 - cur;
+        StepArgs a = step_args(src, dst);
+        direction_speeds(cfg.alpha, cfg.beta, a.smax, a.smin);
+        a.r = dt / sim_dx(cfg);  // solver.hpp:212
+        const unsigned grid = (sg.npatch + ks.P - 1) / ks.P;
+        if (cfg.no_compression) {
+            a.raw_list = nullptr;
+            ks.raw<<<grid, ks.threads, ks.smem, stream>>>(a);
+            WG_LAUNCH_CHECK("raw step");
+        } else {
+            ks.main<<<grid, ks.threads, ks.smem, stream>>>(a);
+            WG_LAUNCH_CHECK("fused step");
+            ks.raw<<<grid, ks.threads, ks.smem, stream>>>(a);
+            WG_LAUNCH_CHECK("skip-rule step");
+        }
+        grow_rows(step + 1);
+        MetricsArgs m{};
+        m.stats = stats;
+        m.npatch = sg.npatch;
+        m.dense_bytes = (uint64_t)sg.npatch * 8ull * N * N * sg.m;
+        m.step = step + 1;
+        m.time = time + dt;
+        m.compress = !cfg.no_compression;
+        m.rows = rows;
+        m.row_index = step;
+        m.raw_count = raw_count;
+        m.bump_next = bump + src;
+        m.mass_fv_out = mass_fv;
+        k_metrics<<<1, 1024, 0, stream>>>(m);
+        WG_LAUNCH_CHECK("metrics");
+        cur = dst;
+        ++step;
+        time += dt;
+    }
+
+    void sync() {
+        WG_CUDA(cudaStreamSynchronize(stream));
+        unsigned e = 0;
+        WG_CUDA(cudaMemcpy(&e, err, sizeof e, cudaMemcpyDeviceToHost));
+        check_device_error(e);
+    }
+
+    void download(double* hgrid) {
+        const uint64_t n = (uint64_t)sg.npatch * sg.m * geo.tcount;
+        DevBuf<double> d(n);
+        WG_CUDA(cudaMemsetAsync(d.p, 0, n * sizeof(double), stream));
+        StepArgs a = step_args(cur, 1 - cur);
+        a.decode_out = d.p;
+        const unsigned grid = (sg.npatch + ks.P - 1) / ks.P;
+        ks.decode<<<grid, ks.threads, ks.smem, stream>>>(a);
+        WG_LAUNCH_CHECK("decode");
+        WG_CUDA(cudaMemcpyAsync(hgrid, d.p, n * sizeof(double), cudaMemcpyDeviceToHost, stream));
+        sync();
+    }
+
+    void metrics(wg_metrics_row* out, uint64_t max_rows, uint64_t* nrows) {
+        sync();
+        const uint64_t n = std::min<uint64_t>(step, max_rows);
+        if (out && n) WG_CUDA(cudaMemcpy(out, rows, n * sizeof(wg_metrics_row), cudaMemcpyDeviceToHost));
+        if (nrows) *nrows = step;
+    }
+
+    void patch_csr(uint64_t p, uint32_t q, double* v, uint32_t* col, uint32_t* row, uint64_t* nnz,
+                   int32_t* raw) {
+        if (p >= sg.npatch || q >= sg.m) raise(WG_OUT_OF_RANGE, "patch_csr: patch/component");
+        sync();
+        DirEntry e;
+        WG_CUDA(cudaMemcpy(&e, dir[cur] + p * sg.m + q, sizeof e, cudaMemcpyDeviceToHost));
+        const bool is_raw = e.flags & DIR_RAW;
+        if (raw) *raw = is_raw ? 1 : 0;
+        if (nnz) *nnz = is_raw ? (uint64_t)N * N : e.nnz;
+        const unsigned char* base = store[cur] + e.off;
+        if (is_raw) {
+            if (v) WG_CUDA(cudaMemcpy(v, base, (size_t)N * N * 8, cudaMemcpyDeviceToHost));
+            return;
+        }
+        if (v) WG_CUDA(cudaMemcpy(v, base, 8ull * e.nnz, cudaMemcpyDeviceToHost));
+        if (col) WG_CUDA(cudaMemcpy(col, base + 8ull * e.nnz, 4ull * e.nnz, cudaMemcpyDeviceToHost));
+        if (row) WG_CUDA(cudaMemcpy(row, base + 12ull * e.nnz, 4ull * (N + 1), cudaMemcpyDeviceToHost));
+    }
+};
+
+}  // namespace wg
+
+using namespace wg;
+
+extern "C" {
+
+wg_status wg_session_create(const wg_run_config* cfg, const wg_shard* shard, void* stream,
+                            wg_session** out) {
+    return guard([&] {
+        auto s = std::make_unique<Session>();
+        s->create(*cfg, shard, stream);
+        *out = reinterpret_cast<wg_session*>(s.release());
+    });
+}
+
+wg_status wg_session_destroy(wg_session* s) {
+    return guard([&] { delete reinterpret_cast<Session*>(s); });
+}
+
+wg_status wg_session_info_get(const wg_session* sp, wg_session_info* info) {
+    return guard([&] {
+        const Session* s = reinterpret_cast<const Session*>(sp);
+        info->npatch_local = s->sg.npatch;
+        info->patch_n = s->N;
+        info->components = s->sg.m;
+        info->halo_doubles = s->halo_doubles();
+        info->store_capacity_bytes = s->cap;
+        info->device_bytes = s->device_bytes;
+        info->cells_per_step = (uint64_t)s->sg.R * (s->N - 1) * (uint64_t)s->sg.P1 * (s->N - 1);
+    });
+}
+
+wg_status wg_session_upload(wg_session* s, const double* host_grid) {
+    return guard([&] { reinterpret_cast<Session*>(s)->upload_host(host_grid); });
+}
+
+wg_status wg_dev_session_upload(wg_session* s, const double* dev_grid) {
+    return guard([&] { reinterpret_cast<Session*>(s)->upload_dev(dev_grid); });
+}
+
+wg_status wg_session_step(wg_session* s, double dt) {
+    return guard([&] { reinterpret_cast<Session*>(s)->do_step(dt); });
+}
+
+wg_status wg_session_halo(wg_session* sp, double** send_lo, double** send_hi, double** recv_lo,
+                          double** recv_hi) {
+    return guard([&] {
+        Session* s = reinterpret_cast<Session*>(sp);
+        const EdgeSet& e = s->edges[s->cur];
+        const uint64_t line = s->halo_doubles();
+        if (send_lo) *send_lo = e.rowlo + 1 * line;              // slot 1: first owned row
+        if (send_hi) *send_hi = e.rowhi + (uint64_t)s->sg.R * line;  // slot R: last owned row
+        if (recv_lo) *recv_lo = e.rowhi;                         // slot 0: halo above
+        if (recv_hi) *recv_hi = e.rowlo + (uint64_t)(s->sg.R + 1) * line;  // slot R+1: halo below
+    });
+}
+
+wg_status wg_session_metrics(wg_session* s, wg_metrics_row* rows, uint64_t max_rows, uint64_t* nrows) {
+    return guard([&] { reinterpret_cast<Session*>(s)->metrics(rows, max_rows, nrows); });
+}
+
+wg_status wg_session_download(wg_session* s, double* host_grid) {
+    return guard([&] { reinterpret_cast<Session*>(s)->download(host_grid); });
+}
+
+wg_status wg_session_patch_csr(wg_session* s, uint64_t patch, uint32_t comp, double* v, uint32_t* col,
+                               uint32_t* row, uint64_t* nnz, int32_t* raw) {
+    return guard([&] { reinterpret_cast<Session*>(s)->patch_csr(patch, comp, v, col, row, nnz, raw); });
+}
+
+wg_status wg_session_sync(wg_session* s) {
+    return guard([&] { reinterpret_cast<Session*>(s)->sync(); });
+}
+
+// run(RunConfig) (pipeline.hpp:129-305) on one device through a session.
+wg_status wg_run(const wg_run_config* cfg, wg_metrics_row* rows, uint64_t max_rows, uint64_t* nrows,
+                 double* final_grid, wg_run_summary* summary) {
+    return guard([&] {
+        if (cfg->scheme != WG_SCHEME_LBM_D2Q9) sim_validate(*cfg);
+        const RunGeometry g = run_geometry(*cfg);
+        std::vector<double> dts;
+        if (cfg->scheme == WG_SCHEME_TRANSPORT) dts = transport_dts(*cfg);
+        else if (cfg->scheme == WG_SCHEME_LBM_D2Q9) dts.assign(cfg->lbm_steps, 1.0);
+        else raise(WG_INVALID_ARGUMENT, "wg_run: scheme not supported by this build");
+        Session s;
+        s.create(*cfg, nullptr, nullptr);
+        std::vector<double> grid(g.npatch * g.m * g.tcount);
+        initial_state(*cfg, 0, g.splits[0], grid.data());
+        cudaEvent_t e0, e1;
+        WG_CUDA(cudaEventCreate(&e0));
+        WG_CUDA(cudaEventCreate(&e1));
+        s.upload_host(grid.data());
+        WG_CUDA(cudaEventRecord(e0, s.stream));
+        for (double dt : dts) s.do_step(dt);
+        WG_CUDA(cudaEventRecord(e1, s.stream));
+        s.sync();
+        float ms = 0.f;
+        WG_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        std::vector<wg_metrics_row> r(s.step);
+        uint64_t n = 0;
+        s.metrics(r.data(), r.size(), &n);
+        if (cfg->strict && !cfg->no_compression) {  // pipeline.hpp:278-283 (mass half)
+            std::vector<double> mfv(s.step);
+            if (s.step)
+                WG_CUDA(cudaMemcpy(mfv.data(), s.mass_fv, s.step * sizeof(double), cudaMemcpyDeviceToHost));
+            for (uint64_t k = 0; k < s.step; ++k) {
+                const double scale = std::max(std::abs(mfv[k]), 1.0);
+                if (std::abs(r[k].global_mass - mfv[k]) > 1e-12 * scale)
+                    raise(WG_CONSISTENCY, "strict: compression cycle changed global mass");
+            }
+        }
+        if (cfg->scheme == WG_SCHEME_TRANSPORT && cfg->compute_l2 && !r.empty()) {
+            // l2_error of the final state only (the per-step l2 diagnostic is
+            // host-side harness work)
+            std::vector<double> fg(grid.size());
+            s.download(fg.data());
+            const uint64_t n0 = g.n[0], n1 = g.n[1], ty = n1 + 2;
+            std::vector<double> asmv(cfg->nx * cfg->nx);
+            for (uint64_t p = 0; p < g.npatch; ++p) {
+                const uint64_t a = p / g.splits[1], b = p % g.splits[1];
+                for (uint64_t i = 1; i <= n0; ++i)
+                    for (uint64_t j = 1; j <= n1; ++j)
+                        asmv[(a * (n0 - 1) + i - 1) * cfg->nx + b * (n1 - 1) + j - 1] = fg[p * g.tcount + i * ty + j];
+            }
+            double sum = 0.0;
+            for (uint64_t i = 0; i < cfg->nx; ++i)
+                for (uint64_t j = 0; j < cfg->nx; ++j) {
+                    const double d = asmv[i * cfg->nx + j] - exact_transport_at(*cfg, s.time, i, j);
+                    sum += d * d;
+                }
+            r.back().l2 = cfg->domain_length * cfg->domain_length / (double)(cfg->nx * cfg->nx) * sum;
+        }
+        if (nrows) *nrows = n;
+        if (rows)
+            for (uint64_t k = 0; k < n && k < max_rows; ++k) rows[k] = r[k];
+        if (final_grid) s.download(final_grid);
+        if (summary) {
+            std::memset(summary, 0, sizeof(*summary));
+            double sum = 0.0;
+            for (auto& x : r) sum += x.ratio;
+            summary->avg_ratio = r.empty() ? 1.0 : sum / (double)r.size();
+            summary->total_seconds = ms * 1e-3;
+            summary->step_seconds = ms * 1e-3;
+            summary->t_final = s.time;
+            summary->steps = s.step;
+        }
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,66 @@
+// session.cuh — device data layout of the compressed patch store.
+//
+// HBM layout (per shard):
+//   store[2]   byte pools, double-buffered (read step k-1, write step k).
+//              One block per (patch, component): CSR exactly as the
+//              reference's CsrBlock (codec.hpp:24-34) — v[nnz] f64,
+//              col[nnz] u32, row[n+1] u32, 16-byte aligned — or, for a raw
+//              patch (skip rule, pipeline.hpp:243-249; initial state),
+//              the n*n dense logical block.
+//   dir[2]     DirEntry per (patch, component): byte offset, nnz, flags.
+//   edges[2]   reconstructed boundary lines of every patch (logical rows 1
+//              and n-2, columns 1 and n-2): the ghost-ring source of the
+//              next step (sync_ghosts, patchgrid.hpp:131-201).  Row lines
+//              have R+2 patch-row slots: slot 0 and R+1 are the halo rows
+//              received from the neighbouring shards (multi-GPU).
+//   stats      PatchStats per patch, reduced per step into a metrics row.
+#pragma once
+
+#include <cstdint>
+
+namespace wg {
+
+constexpr uint32_t DIR_RAW = 1u;
+
+struct DirEntry {
+    uint64_t off;    // byte offset in the pool
+    uint32_t nnz;    // CSR entries (0 for raw)
+    uint32_t flags;  // DIR_RAW
+};
+
+struct PatchStats {
+    uint64_t comp_bytes;  // CsrBlock::byte_size summed over components
+    uint32_t nnz;
+    uint32_t zeroed;
+    double mass;          // trapezoid mass of component 0..m-1 summed (after the cycle)
+    double mass_fv;       // same, of the scheme output before compression (strict mode)
+};
+
+struct EdgeSet {
+    double* rowlo;  // [(R+2) slots][P1][m][n]: logical row 1
+    double* rowhi;  // [(R+2) slots][P1][m][n]: logical row n-2
+    double* collo;  // [R][P1][m][n]: logical column 1
+    double* colhi;  // [R][P1][m][n]: logical column n-2
+};
+
+struct ShardGeom {
+    uint32_t R;       // owned patch rows
+    uint32_t P1;      // patches per row
+    uint32_t m;       // components
+    int world;        // 1: periodic wrap is local
+    uint32_t npatch;  // R * P1
+};
+
+__host__ __device__ inline uint64_t round16(uint64_t b) { return (b + 15) & ~uint64_t(15); }
+
+// Row slot of local patch row a' in [-1, R] (halo rows for world > 1; the
+// periodic wrap for world == 1, patchgrid.hpp:143-161).
+__device__ __forceinline__ uint32_t row_slot(int a, const ShardGeom& g) {
+    if (g.world == 1) {
+        const int R = (int)g.R;
+        a = (a + R) % R;
+    }
+    return (uint32_t)(a + 1);
+}
+
+}  // namespace wg

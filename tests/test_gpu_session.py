@@ -1,0 +1,175 @@
+"""The fused compressed stencil loop (device session) against the C oracle's
+run() — the reference's pipeline.hpp:129-305 restated — bit-exact in state,
+compressed layout and integer metrics; mass within 1e-12 (summation order)."""
+from __future__ import annotations
+
+import ctypes as C
+import json
+
+import numpy as np
+import pytest
+
+from paper_2302_09883_b200 import abi, api
+
+from .conftest import GOLDEN
+
+pytestmark = pytest.mark.gpu
+
+
+def bits(a):
+    return np.ascontiguousarray(a).view(np.uint64)
+
+
+def compare_runs(a: api.RunResult, b: api.RunResult, mass_rtol=1e-12):
+    assert len(a.rows) == len(b.rows)
+    for ra, rb in zip(a.rows, b.rows):
+        for k in ("step", "dense_bytes", "compressed_bytes", "nnz", "zeroed"):
+            assert ra[k] == rb[k], (k, ra, rb)
+        assert ra["time"] == rb["time"]
+        assert ra["ratio"] == rb["ratio"]
+        assert abs(ra["global_mass"] - rb["global_mass"]) <= mass_rtol * max(abs(rb["global_mass"]), 1.0)
+    la, lb = a.grid.logical_view(), b.grid.logical_view()
+    assert np.array_equal(bits(la), bits(lb)), f"{np.sum(la != lb)} logical cells differ"
+
+
+def transport_cfg(nx, splits, levels, c, steps, mode="capped", **kw):
+    cfg = api.RunConfig(scheme="transport", nx=nx, splits=splits, levels=levels,
+                        spec=api.ThresholdSpec(mode, c), compute_l2=False, **kw)
+    cfg.t_end = steps * cfg.cfl * (1.0 / (nx - 1)) / max(cfg.alpha, cfg.beta)
+    return cfg
+
+
+def test_c1_full_parity(product, oracle):
+    """C1: 257^2 points, 8x8 patches of 33^2, L=4, capped 1e-3, 100 steps."""
+    cfg = api.RunConfig(scheme="transport", nx=257, splits=(8, 8), levels=4, t_end=100 / 512,
+                        spec=api.ThresholdSpec("capped", 1e-3), compute_l2=True)
+    a = api.run(cfg, lib=product)
+    b = api.run(cfg, lib=oracle)
+    compare_runs(a, b)
+    gold = json.loads((GOLDEN / "c1_transport.json").read_text())
+    last = a.rows[-1]
+    assert len(a.rows) == gold["steps"]
+    assert last["nnz"] == gold["final"]["nnz"] and last["zeroed"] == gold["final"]["zeroed"]
+    assert last["compressed_bytes"] == gold["final"]["compressed_bytes"]
+    assert abs(a.summary["avg_ratio"] - gold["avg_ratio"]) <= 1e-12 * gold["avg_ratio"]
+    assert abs(last["l2"] - gold["final"]["l2"]) <= 1e-12 * gold["final"]["l2"]
+
+
+@pytest.mark.parametrize(
+    "nx,splits,levels,c,mode,steps",
+    [(33, (2, 2), 3, 0.01, "capped", 10),       # test_pipeline.cpp small_transport
+     (65, (1, 1), 4, 1e-3, "capped", 5),        # single periodic patch
+     (129, (2, 2), 4, 0.01, "capped", 20),      # acceptance transport_base (65^2 patches)
+     (129, (2, 2), 2, 0.02, "accumulation", 8),
+     (129, (8, 8), 3, 0.005, "constant", 8),    # 17^2 patches
+     (257, (4, 4), 6, 1e-3, "capped", 6),       # L = k (non-conservative, still bit-exact)
+     (65, (8, 8), 2, 0.05, "capped", 6),        # 9^2 patches
+     (129, (2, 2), 0, 0.1, "capped", 4)],       # L = 0: nothing transforms, always raw
+)
+def test_transport_parity(product, oracle, nx, splits, levels, c, mode, steps):
+    cfg = transport_cfg(nx, splits, levels, c, steps, mode)
+    compare_runs(api.run(cfg, lib=product), api.run(cfg, lib=oracle))
+
+
+def test_zero_threshold_equals_no_compression(product):
+    """test_pipeline.cpp:33-53 — c=0 keeps every patch raw (skip rule)."""
+    a = api.run(transport_cfg(33, (2, 2), 3, 0.0, 12), lib=product)
+    cfg = transport_cfg(33, (2, 2), 3, 0.0, 12)
+    cfg.no_compression = True
+    b = api.run(cfg, lib=product)
+    assert all(r["zeroed"] == 0 for r in a.rows)
+    assert all(r["compressed_bytes"] == 0 and r["ratio"] == 1.0 for r in b.rows)
+    for ra, rb in zip(a.rows, b.rows):
+        assert ra["global_mass"] == rb["global_mass"]
+    assert np.array_equal(bits(a.grid.logical_view()), bits(b.grid.logical_view()))
+
+
+def test_skip_rule_mixed_patches(product, oracle):
+    """A threshold that zeroes nothing on some patches and something on
+    others exercises the raw-patch kernel inside a compressed run."""
+    cfg = transport_cfg(129, (4, 4), 3, 2e-5, 10)
+    a, b = api.run(cfg, lib=product), api.run(cfg, lib=oracle)
+    compare_runs(a, b)
+
+
+def test_deterministic(product):
+    cfg = transport_cfg(129, (4, 4), 4, 1e-3, 10)
+    a, b = api.run(cfg, lib=product), api.run(cfg, lib=product)
+    assert [r["global_mass"] for r in a.rows] == [r["global_mass"] for r in b.rows]
+    assert np.array_equal(bits(a.grid.data), bits(b.grid.data))
+
+
+def test_strict_mode_accepts_healthy_run(product):
+    cfg = transport_cfg(33, (2, 2), 3, 0.01, 10, strict=True)
+    api.run(cfg, lib=product)  # test_pipeline.cpp:73-77
+
+
+def test_mass_conserved(product):
+    cfg = transport_cfg(129, (2, 2), 4, 0.01, 40)
+    r = api.run(cfg, lib=product)
+    m0 = r.rows[0]["global_mass"]
+    assert all(abs(x["global_mass"] - m0) <= 1e-10 * abs(m0) for x in r.rows)  # acceptance.cpp:197
+
+
+def test_csr_bytes_accounting(product):
+    """acceptance.cpp:251-255: bytes == 12 nnz + 4 * 66 * 4."""
+    r = api.run(transport_cfg(129, (2, 2), 4, 0.01, 10), lib=product)
+    assert all(x["compressed_bytes"] == 12 * x["nnz"] + 4 * 66 * 4 for x in r.rows)
+
+
+def _session(product, cfg: api.RunConfig):
+    c = cfg.to_c()
+    s = abi.vp()
+    product.check(product.wg_session_create(C.byref(c), None, None, C.byref(s)))
+    return s
+
+
+def test_session_csr_layout_bit_exact(product, oracle):
+    """The stored CSR blocks equal csr_encode of the oracle's thresholded
+    coefficients of the same state (index layout and values bit-exact)."""
+    cfg = transport_cfg(129, (2, 2), 4, 1e-3, 3)
+    s = _session(product, cfg)
+    try:
+        g0 = api.initial_state(cfg, lib=product)
+        product.check(product.wg_session_upload(s, abi.dptr(g0.data)))
+        dt = cfg.cfl / 128 / 0.9
+        # oracle: one step by hand (sync, FV, DWT, threshold)
+        ref = api.PatchGrid(g0.global_dims, g0.splits, 1, True, data=g0.data.copy())
+        for _ in range(2):
+            product.check(product.wg_session_step(s, dt))
+            api.sync_ghosts(ref, lib=oracle)
+            nxt = api.PatchGrid(ref.global_dims, ref.splits, 1, True, data=ref.data.copy())
+            api.fv_step(ref, nxt, "transport", dt, 1 / 128, lib=oracle)
+            ref = nxt
+            for p in range(ref.npatch):
+                blk = np.ascontiguousarray(ref.data[p, 0, 1:-1, 1:-1])
+                cs = api.dwt_nd(blk, 4, lib=oracle)
+                z = api.apply_threshold(cs, 4, cfg.spec, lib=oracle)
+                assert z > 0
+                ref.data[p, 0, 1:-1, 1:-1] = api.idwt_nd(cs + 0.0, 4, lib=oracle)
+                want = api.csr_encode(cs, 65, 65, lib=oracle)
+                nnz, raw = abi.u64(), abi.i32()
+                product.check(product.wg_session_patch_csr(s, p, 0, None, None, None, C.byref(nnz), C.byref(raw)))
+                assert raw.value == 0 and nnz.value == want.nnz()
+                v = np.empty(nnz.value)
+                col = np.empty(nnz.value, np.uint32)
+                row = np.empty(66, np.uint32)
+                product.check(product.wg_session_patch_csr(
+                    s, p, 0, abi.dptr(v), col.ctypes.data_as(C.POINTER(abi.u32)),
+                    row.ctypes.data_as(C.POINTER(abi.u32)), C.byref(nnz), C.byref(raw)))
+                assert np.array_equal(bits(v), bits(want.v))
+                assert np.array_equal(col, want.col) and np.array_equal(row, want.row)
+    finally:
+        product.wg_session_destroy(s)
+
+
+def test_budget_overflow_fails_loudly(product):
+    cfg = transport_cfg(129, (2, 2), 4, 1e-3, 2)
+    cfg.store_budget_bytes = 64 * 1024  # smaller than the raw initial state
+    s = _session(product, cfg)
+    try:
+        g0 = api.initial_state(cfg, lib=product)
+        with pytest.raises(abi.OutOfMemoryError):
+            product.check(product.wg_session_upload(s, abi.dptr(g0.data)))
+    finally:
+        product.wg_session_destroy(s)
