@@ -276,6 +276,12 @@ wg_status wg_session_patch_csr(wg_session* s, uint64_t patch, uint32_t comp,
 /* Synchronise the session stream and return the device error word. */
 wg_status wg_session_sync(wg_session* s);
 
+/* Bench instrumentation: when enabled, CUDA events bracket every launch of
+ * the fused step kernel on the session stream; _read returns the summed
+ * device time (ms) and the launch count since the last enable. */
+wg_status wg_session_profile(wg_session* s, int32_t enable);
+wg_status wg_session_profile_read(wg_session* s, double* main_ms, uint64_t* launches);
+
 /* ---- device per-op entry points (async; for benches and torch callers) -- */
 wg_status wg_dev_dwt2d(const double* in, double* out, uint64_t n0, uint64_t n1,
                        int32_t levels, uint64_t batch, void* stream);

@@ -219,6 +219,8 @@ _PROTOS = {
     "wg_session_download": (i32, [vp, dp]),
     "wg_session_patch_csr": (i32, [vp, u64, u32, dp, P(u32), P(u32), P(u64), P(i32)]),
     "wg_session_sync": (i32, [vp]),
+    "wg_session_profile": (i32, [vp, i32]),
+    "wg_session_profile_read": (i32, [vp, dp, P(u64)]),
     "wg_dev_dwt2d": (i32, [vp, vp, u64, u64, i32, u64, vp]),
     "wg_dev_idwt2d": (i32, [vp, vp, u64, u64, i32, u64, vp]),
 }

@@ -1,0 +1,257 @@
+// lbm_kernels.cuh — the fused per-patch step for the D2Q9 LBM (9 components).
+//
+// A 65^2 x 9 fp64 patch is 304 KB and does not fit one SM's shared memory,
+// so a CTA works on one patch at a time in three rounds of three
+// components (three (N+2)^2 tiles in shared memory) and stages the nine
+// N*N population fields in a private scratch block that stays resident in
+// L2 (the kernel is persistent: one scratch block per CTA, reused for every
+// patch the CTA processes).  Per patch:
+//
+//   3 rounds: CSR decode + inverse DWT of 3 populations, ghost ring from the
+//             edge lines, pull streaming  f_q(x) <- f_q(x - c_q)  -> scratch
+//   collide:  BGK on every cell (physics.cuh lbm_collide)      -> scratch
+//   3 rounds: forward DWT, threshold, CSR compaction, reconstruction of the
+//             kept coefficients -> edge lines + trapezoid mass
+//   skip rule on the patch total of zeroed coefficients (pipeline.hpp:243-249)
+//
+// The D2Q9 scheme is NOT in the reference; its definition
+// is shared with oracle/ref_shim.cpp and oracle/wg_oracle.c.
+#pragma once
+
+#include "patch_phases.cuh"
+
+namespace wg {
+
+template <int N>
+struct LbmLayout {
+    static constexpr int TP = N + 2;
+    static constexpr int TILE = TP * TP;
+    static constexpr int SLOTS = 3;
+    static constexpr int NT = ((SLOTS * N + 31) / 32) * 32;
+    static constexpr size_t smem_bytes() {
+        return sizeof(double) * (size_t)(SLOTS * TILE + 2 * NT) + sizeof(unsigned long long) * NT;
+    }
+    static constexpr size_t scratch_doubles() { return (size_t)9 * N * N; }
+};
+
+template <int N, int L, int MODE>
+__global__ void __launch_bounds__(LbmLayout<N>::NT) k_lbm_step(const __grid_constant__ StepArgs a) {
+    using Lay = LbmLayout<N>;
+    constexpr int TP = Lay::TP, TILE = Lay::TILE, NT = Lay::NT, NN = N * N;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    double* tiles = reinterpret_cast<double*>(smem_raw);
+    double* red = tiles + Lay::SLOTS * TILE;
+    double* red_fv = red + NT;
+    unsigned long long* inc = reinterpret_cast<unsigned long long*>(red_fv + NT);
+    __shared__ uint64_t slot_off[3];
+    __shared__ int slot_ok[3];
+    __shared__ unsigned long long patch_bytes, patch_nnz, patch_zero;
+    __shared__ uint32_t comp_nnz[9];
+    __shared__ uint32_t row_k[3 * NT];  // CSR entry offset of each row, per round
+
+    const int t = threadIdx.x;
+    const int s = t / N;
+    const int li = t - s * N;
+    const bool lane_ok = t < Lay::SLOTS * N;
+    const ShardGeom& g = a.g;
+    double* T = tiles + (lane_ok ? s : 0) * TILE;
+    double* S = a.scratch + (size_t)blockIdx.x * Lay::scratch_doubles();
+    const bool from_list = MODE == MODE_RAW && a.raw_list != nullptr;
+    const uint32_t count = from_list ? *a.raw_count : g.npatch;
+
+    for (uint32_t k = blockIdx.x; k < count; k += gridDim.x) {
+        const uint32_t p = from_list ? a.raw_list[k] : k;
+        const PatchPos pp = patch_pos(p, g);
+
+        // ---- decode + pull streaming, 3 rounds of 3 populations ----------
+        for (int rd = 0; rd < 3; ++rd) {
+            const int q = 3 * rd + s;
+            bool raw_in = false;
+            if (lane_ok) {
+                raw_in = decode_row<N, L>(T, li, a.dir_in[(size_t)p * 9 + q], a.store_in);
+                if (MODE != MODE_DECODE) fill_ghosts<N>(T, li, a.ein, pp, q, g);
+            }
+            __syncthreads();
+            if (lane_ok) {
+                double v[N];
+                decode_col<N, L>(T, li, raw_in, v);
+                if (MODE == MODE_DECODE) {
+                    double* out = a.decode_out + ((size_t)p * 9 + q) * TILE;
+#pragma unroll
+                    for (int i = 0; i < N; ++i) out[(i + 1) * TP + li + 1] = v[i];
+                } else if (!raw_in) {
+                    store_col<N>(T, li, v);
+                }
+            }
+            __syncthreads();
+            if (MODE != MODE_DECODE && lane_ok) {
+                const int cx = lbm_cx(q), cy = lbm_cy(q);
+                double* Sq = S + (size_t)q * NN;
+                const int j = li;
+#pragma unroll 5
+                for (int i = 0; i < N; ++i) Sq[i * N + j] = T[(i + 1 - cx) * TP + (j + 1 - cy)];
+            }
+            __syncthreads();
+        }
+        if (MODE == MODE_DECODE) continue;
+
+        // ---- BGK collide on every cell -------------------------------------
+        double mfv = 0.0;
+        for (int c = t; c < NN; c += NT) {
+            double f[9];
+#pragma unroll
+            for (int q = 0; q < 9; ++q) f[q] = S[(size_t)q * NN + c];
+            lbm_collide(f, a.omega);
+            const int i = c / N, j = c - (c / N) * N;
+            const double w = ((i == 0 || i == N - 1) ? 0.5 : 1.0) * ((j == 0 || j == N - 1) ? 0.5 : 1.0);
+#pragma unroll
+            for (int q = 0; q < 9; ++q) {
+                S[(size_t)q * NN + c] = f[q];
+                mfv += w * f[q];
+            }
+        }
+        red_fv[t] = mfv;
+        __syncthreads();
+
+        double m = 0.0;
+        if (MODE == MODE_RAW) {
+            // ---- store the collided state uncompressed (skip rule) --------
+            for (int rd = 0; rd < 3; ++rd) {
+                const int q = 3 * rd + s;
+                if (lane_ok && li == 0) {
+                    const uint64_t bytes = round16((uint64_t)NN * 8);
+                    const uint64_t off = atomicAdd(a.bump_out, (unsigned long long)bytes);
+                    slot_ok[s] = off + bytes <= a.cap_out;
+                    if (!slot_ok[s]) {
+                        atomicOr(a.err, ERR_STORE_OVERFLOW);
+                        a.dir_out[(size_t)p * 9 + q] = DirEntry{0, 0u, DIR_DEAD};
+                    } else {
+                        slot_off[s] = off;
+                        a.dir_out[(size_t)p * 9 + q] = DirEntry{off, 0u, DIR_RAW};
+                    }
+                }
+                __syncthreads();
+                if (lane_ok && slot_ok[s]) {
+                    const int j = li;
+                    double v[N];
+                    double* d = reinterpret_cast<double*>(a.store_out + slot_off[s]);
+#pragma unroll
+                    for (int i = 0; i < N; ++i) {
+                        v[i] = S[(size_t)q * NN + i * N + j];
+                        d[i * N + j] = v[i];
+                    }
+                    write_edges<N>(a.eout, pp, q, g, j, v);
+                    m += col_mass<N>(j, v);
+                }
+                __syncthreads();
+            }
+        } else {
+            if (t == 0) {
+                patch_bytes = 0;
+                patch_nnz = 0;
+                patch_zero = 0;
+            }
+            // ---- pass 1: forward DWT + threshold of every population; the
+            // kept coefficients go back to the scratch (transposed: column-
+            // major, so both passes access it coalesced).  The skip rule
+            // needs the patch total of zeroed coefficients before anything
+            // is written to the store.
+            for (int rd = 0; rd < 3; ++rd) {
+                const int q = 3 * rd + s;
+                double v[N];
+                if (lane_ok) {
+                    const int j = li;
+#pragma unroll
+                    for (int i = 0; i < N; ++i) v[i] = S[(size_t)q * NN + i * N + j];
+                    fwd_col_to_tile<N, L>(T, j, v);
+                }
+                __syncthreads();
+                unsigned nz = 0, zr = 0;
+                if (lane_ok) {
+                    fwd_row_threshold<N, L>(T, li, a.thr, v, nz, zr);
+#pragma unroll
+                    for (int pc = 0; pc < N; ++pc) S[(size_t)q * NN + pc * N + li] = v[interleaved_of<N, L>(pc)];
+                }
+                cta_inclusive_scan<NT>(((unsigned long long)zr << 32) | nz, inc);
+                if (lane_ok) {
+                    const unsigned long long base = s == 0 ? 0ull : inc[s * N - 1];
+                    row_k[rd * NT + t] = (uint32_t)((inc[t] - base) & 0xffffffffu) - nz;
+                    if (li == 0) {
+                        const unsigned long long tot = inc[s * N + N - 1] - base;
+                        comp_nnz[q] = (uint32_t)(tot & 0xffffffffu);
+                        atomicAdd(&patch_bytes, 12ull * (tot & 0xffffffffu) + 4ull * (N + 1));
+                        atomicAdd(&patch_nnz, tot & 0xffffffffu);
+                        atomicAdd(&patch_zero, tot >> 32);
+                    }
+                }
+                __syncthreads();
+            }
+            const bool compressed = patch_zero != 0;
+            if (t == 0) {
+                PatchStats& st = a.stats[p];
+                st.comp_bytes = patch_bytes;
+                st.nnz = (uint32_t)patch_nnz;
+                st.zeroed = (uint32_t)patch_zero;
+                if (!compressed) {  // skip rule: the raw kernel stores the collided state
+                    const uint32_t kq = atomicAdd(a.raw_count, 1u);
+                    if (kq < a.raw_capacity) a.raw_list[kq] = p;
+                    else atomicOr(a.err, ERR_RAW_OVERFLOW);
+                }
+            }
+            // ---- pass 2: CSR blocks, reconstruction, edge lines, mass ------
+            for (int rd = 0; rd < 3 && compressed; ++rd) {
+                const int q = 3 * rd + s;
+                if (lane_ok && li == 0) {
+                    const uint64_t bytes = round16(12ull * comp_nnz[q] + 4ull * (N + 1));
+                    const uint64_t off = atomicAdd(a.bump_out, (unsigned long long)bytes);
+                    slot_ok[s] = off + bytes <= a.cap_out;
+                    if (!slot_ok[s]) {
+                        atomicOr(a.err, ERR_STORE_OVERFLOW);
+                        a.dir_out[(size_t)p * 9 + q] = DirEntry{0, 0u, DIR_DEAD};
+                    } else {
+                        slot_off[s] = off;
+                        a.dir_out[(size_t)p * 9 + q] = DirEntry{off, comp_nnz[q], 0u};
+                    }
+                }
+                __syncthreads();
+                const bool ok = lane_ok && slot_ok[s];
+                double v[N];
+                if (ok) {
+#pragma unroll
+                    for (int pc = 0; pc < N; ++pc) v[interleaved_of<N, L>(pc)] = S[(size_t)q * NN + pc * N + li];
+                    unsigned nz = 0;
+#pragma unroll
+                    for (int r = 0; r < N; ++r) nz += v[r] != 0.0 ? 1u : 0u;
+                    write_csr_row<N, L>(a.store_out + slot_off[s], comp_nnz[q], li, row_k[rd * NT + t], nz, v);
+                    inv_row_to_tile<N, L>(T, li, v);
+                }
+                __syncthreads();
+                if (ok) {
+                    decode_col<N, L>(T, li, false, v);
+                    write_edges<N>(a.eout, pp, q, g, li, v);
+                    m += col_mass<N>(li, v);
+                }
+                __syncthreads();
+            }
+        }
+        red[t] = m;
+        __syncthreads();
+        if (t < 32) {
+            const double mm = warp_sum_range(red, 0, NT);
+            const double mf = warp_sum_range(red_fv, 0, NT);
+            if (t == 0) {
+                PatchStats& st = a.stats[p];
+                st.mass = mm;
+                st.mass_fv = mf;
+                if (MODE == MODE_RAW && !from_list) {
+                    st.comp_bytes = 0;
+                    st.nnz = 0;
+                    st.zeroed = 0;
+                }
+            }
+        }
+        __syncthreads();
+    }
+}
+
+}  // namespace wg

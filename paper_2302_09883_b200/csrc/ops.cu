@@ -91,11 +91,11 @@ __global__ void k_idwt_lines(double* data, LineGeom g, int levels) {
 }
 
 void transform_nd_dev(double* d_data, const uint64_t* dims, uint32_t rank, int levels,
-                      bool inverse) {
+                      bool inverse, uint32_t first_dim = 0, cudaStream_t stream = 0) {
     uint64_t total = 1;
     for (uint32_t d = 0; d < rank; ++d) total *= dims[d];
-    for (uint32_t s = 0; s < rank; ++s) {
-        const uint32_t d = inverse ? rank - 1 - s : s;
+    for (uint32_t s = first_dim; s < rank; ++s) {
+        const uint32_t d = inverse ? rank - 1 - (s - first_dim) : s;
         LineGeom g;
         g.n = dims[d];
         g.inner = 1;
@@ -107,11 +107,8 @@ void transform_nd_dev(double* d_data, const uint64_t* dims, uint32_t rank, int l
         auto kern = inverse ? k_idwt_lines : k_dwt_lines;
         if (smem > 48 * 1024)
             WG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        for (uint64_t first = 0; first < nlines; first += 65535u * 1024u) {
-            (void)first;
-        }
         if (nlines > 0x7fffffffull) raise(WG_INVALID_ARGUMENT, "too many lines");
-        kern<<<(unsigned)nlines, 128, smem>>>(d_data, g, levels);
+        kern<<<(unsigned)nlines, 128, smem, stream>>>(d_data, g, levels);
         WG_LAUNCH_CHECK("line transform");
     }
 }
@@ -639,6 +636,29 @@ wg_status wg_fv_step(const wg_grid_desc* d, const double* cur, double* next, int
         WG_LAUNCH_CHECK("fv_step");
         check_device_error(read_err(err.p));
         n.download(next);
+    });
+}
+
+// Batched 2-D transforms on device buffers (batch x n0 x n1), async on `stream`.
+wg_status wg_dev_dwt2d(const double* in, double* out, uint64_t n0, uint64_t n1, int32_t levels,
+                       uint64_t batch, void* stream) {
+    return guard([&] {
+        const uint64_t dims[3] = {batch, n0, n1};
+        plan_validate(dims + 1, 2, levels);
+        auto st = static_cast<cudaStream_t>(stream);
+        if (out != in) WG_CUDA(cudaMemcpyAsync(out, in, batch * n0 * n1 * 8, cudaMemcpyDeviceToDevice, st));
+        if (levels > 0 && batch > 0) transform_nd_dev(out, dims, 3, levels, false, 1, st);
+    });
+}
+
+wg_status wg_dev_idwt2d(const double* in, double* out, uint64_t n0, uint64_t n1, int32_t levels,
+                        uint64_t batch, void* stream) {
+    return guard([&] {
+        const uint64_t dims[3] = {batch, n0, n1};
+        plan_validate(dims + 1, 2, levels);
+        auto st = static_cast<cudaStream_t>(stream);
+        if (out != in) WG_CUDA(cudaMemcpyAsync(out, in, batch * n0 * n1 * 8, cudaMemcpyDeviceToDevice, st));
+        if (levels > 0 && batch > 0) transform_nd_dev(out, dims, 3, levels, true, 1, st);
     });
 }
 

@@ -1,56 +1,23 @@
-// patch_kernels.cuh — the fused per-patch step for single-component schemes
-// (FV transport): one kernel runs, for every patch,
+// patch_kernels.cuh — the fused per-patch step for the FV transport scheme:
+// one kernel runs, for every patch,
 //
 //   CSR decode -> inverse DWT (rows, then columns)      [idwt_nd, wavelet.hpp:200-223]
 //   ghost ring from the neighbours' edge lines           [sync_ghosts, patchgrid.hpp:131-201]
 //   upwind FV update                                     [fv_step, solver.hpp:207-231]
 //   forward DWT (columns, then rows)                     [dwt_nd, wavelet.hpp:175-198]
-//   threshold + warp-scan stream compaction to CSR       [apply_threshold threshold.hpp:51-86,
+//   threshold + scan-based stream compaction to CSR      [apply_threshold threshold.hpp:51-86,
 //                                                         csr_encode codec.hpp:37-60]
 //   skip rule (nothing zeroed -> raw patch)              [pipeline.hpp:243-249]
 //   inverse DWT of the kept coefficients -> edge lines + trapezoid mass
 //                                                        [global_mass, patchgrid.hpp:244-266]
 //
-// so the uncompressed patch exists only in shared memory and registers.
-//
-// Work decomposition: a CTA owns P patches; thread (slot, li) owns line li of
-// its patch.  In a ROW phase li is a row, in a COLUMN phase a column; each
-// thread keeps its whole line (N doubles) in registers and runs the lifting
-// there (lifting.cuh).  Phases exchange data through one (N+2)^2 shared
-// tile per patch (odd pitch N+2: conflict-free for both row- and
-// column-ownership access patterns).
+// so the uncompressed patch exists only in shared memory and registers.  A
+// CTA owns P patches (P slots); see patch_phases.cuh for the ownership model.
 #pragma once
 
-#include "common.cuh"
-#include "lifting.cuh"
-#include "physics.cuh"
-#include "session.cuh"
+#include "patch_phases.cuh"
 
 namespace wg {
-
-constexpr int kMaxLevels = 8;
-
-struct StepArgs {
-    const unsigned char* store_in;
-    const DirEntry* dir_in;
-    EdgeSet ein;
-    unsigned char* store_out;
-    DirEntry* dir_out;
-    EdgeSet eout;
-    PatchStats* stats;
-    unsigned long long* bump_out;
-    uint64_t cap_out;
-    uint32_t* raw_list;   // MODE_RAW: patches to store raw (nullptr = all patches)
-    uint32_t* raw_count;
-    uint32_t raw_capacity;
-    unsigned* err;
-    double* decode_out;   // MODE_DECODE: grid buffer (true layout) of this shard
-    ShardGeom g;
-    double smax[4], smin[4], r;                          // transport faces, dt/dx
-    double thr[(kMaxLevels + 1) * (kMaxLevels + 1)];     // T[band_i][band_j]
-};
-
-enum { MODE_MAIN = 0, MODE_RAW = 1, MODE_DECODE = 2 };
 
 template <int N, int P>
 struct Layout {
@@ -61,39 +28,6 @@ struct Layout {
         return sizeof(double) * (size_t)(P * TILE + 2 * NT) + sizeof(unsigned long long) * NT;
     }
 };
-
-// Inclusive scan of one u64 per thread over the CTA (warp shuffles + one
-// shared pass); result written to inc[threadIdx.x].
-template <int NT>
-__device__ __forceinline__ void cta_inclusive_scan(unsigned long long x, unsigned long long* inc) {
-    __shared__ unsigned long long wtot[NT / 32];
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
-        if (lane >= o) x += y;
-    }
-    if (lane == 31) wtot[w] = x;
-    __syncthreads();
-    unsigned long long before = 0;
-#pragma unroll
-    for (int k = 0; k < NT / 32; ++k)
-        if (k < w) before += wtot[k];
-    inc[threadIdx.x] = x + before;
-    __syncthreads();
-}
-
-// Deterministic per-slot sum of red[slot*N .. slot*N+N): one warp per slot,
-// fixed lane->element assignment and a fixed shuffle tree.
-template <int N, int P, int NT>
-__device__ __forceinline__ double slot_sum(const double* red, int slot) {
-    const int lane = threadIdx.x & 31;
-    double s = 0.0;
-    for (int k = lane; k < N; k += 32) s += red[slot * N + k];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    return s;
-}
 
 template <int N, int L, int P, int MODE>
 __global__ void __launch_bounds__(Layout<N, P>::NT)
@@ -127,52 +61,14 @@ __global__ void __launch_bounds__(Layout<N, P>::NT)
         p = blockIdx.x * P + ps;
         valid = lane_ok && p < g.npatch;
     }
-    const uint32_t P1 = g.P1;
-    const int ar = (int)(p / P1);
-    const uint32_t b = p % P1;
+    const PatchPos pp = patch_pos(p, g);
     double* T = tiles + (lane_ok ? ps : 0) * TILE;
 
     // ---- ROW phase: decode row li, inverse transform along dim 1 ----------
     bool raw_in = false;
     if (valid) {
-        const DirEntry e = a.dir_in[p];
-        raw_in = (e.flags & DIR_RAW) != 0;
-        const unsigned char* base = a.store_in + e.off;
-        double* rowp = T + (li + 1) * TP + 1;
-        if (raw_in) {
-            const double* d = reinterpret_cast<const double*>(base) + (size_t)li * N;
-#pragma unroll 8
-            for (int j = 0; j < N; ++j) rowp[j] = d[j];
-        } else {
-            const double* v = reinterpret_cast<const double*>(base);
-            const uint32_t* col = reinterpret_cast<const uint32_t*>(base + 8ull * e.nnz);
-            const uint32_t* ro = col + e.nnz;
-            const uint32_t k0 = ro[li], k1 = ro[li + 1];
-#pragma unroll
-            for (int j = 0; j < N; ++j) rowp[j] = 0.0;
-            for (uint32_t k = k0; k < k1; ++k) rowp[col[k]] = v[k];
-            double x[N];
-#pragma unroll
-            for (int r = 0; r < N; ++r) x[r] = rowp[corner_pos<N, L>(r)];
-            idwt_line_reg<N, L>(x);
-#pragma unroll
-            for (int j = 0; j < N; ++j) rowp[j] = x[j];
-        }
-        if (MODE != MODE_DECODE) {
-            // ghost ring from the neighbours' reconstructed edge lines
-            const uint32_t su = row_slot(ar - 1, g), sd = row_slot(ar + 1, g);
-            const uint32_t bl = (b + P1 - 1) % P1, br = (b + 1) % P1;
-            T[(li + 1) * TP] = a.ein.colhi[((size_t)ar * P1 + bl) * N + li];
-            T[(li + 1) * TP + N + 1] = a.ein.collo[((size_t)ar * P1 + br) * N + li];
-            T[li + 1] = a.ein.rowhi[((size_t)su * P1 + b) * N + li];
-            T[(N + 1) * TP + li + 1] = a.ein.rowlo[((size_t)sd * P1 + b) * N + li];
-            if (li == 0) {
-                T[0] = a.ein.rowhi[((size_t)su * P1 + bl) * N + N - 2];
-                T[N + 1] = a.ein.rowhi[((size_t)su * P1 + br) * N + 1];
-                T[(N + 1) * TP] = a.ein.rowlo[((size_t)sd * P1 + bl) * N + N - 2];
-                T[(N + 1) * TP + N + 1] = a.ein.rowlo[((size_t)sd * P1 + br) * N + 1];
-            }
-        }
+        raw_in = decode_row<N, L>(T, li, a.dir_in[p], a.store_in);
+        if (MODE != MODE_DECODE) fill_ghosts<N>(T, li, a.ein, pp, 0, g);
     }
     __syncthreads();
 
@@ -180,22 +76,13 @@ __global__ void __launch_bounds__(Layout<N, P>::NT)
     double v[N];
     const int j = li;
     if (valid) {
-        if (raw_in) {
-#pragma unroll
-            for (int i = 0; i < N; ++i) v[i] = T[(i + 1) * TP + j + 1];
-        } else {
-#pragma unroll
-            for (int r = 0; r < N; ++r) v[r] = T[(corner_pos<N, L>(r) + 1) * TP + j + 1];
-            idwt_line_reg<N, L>(v);
-            if (MODE != MODE_DECODE) {
-#pragma unroll
-                for (int i = 0; i < N; ++i) T[(i + 1) * TP + j + 1] = v[i];
-            }
-        }
+        decode_col<N, L>(T, j, raw_in, v);
         if (MODE == MODE_DECODE) {
             double* out = a.decode_out + (size_t)p * TILE;
 #pragma unroll
             for (int i = 0; i < N; ++i) out[(i + 1) * TP + j + 1] = v[i];
+        } else if (!raw_in) {
+            store_col<N>(T, j, v);
         }
     }
     if (MODE == MODE_DECODE) return;
@@ -206,9 +93,8 @@ __global__ void __launch_bounds__(Layout<N, P>::NT)
     // x = dim 0 = i.  No FMA (-fmad=false).
     double mfv = 0.0;
     if (valid) {
-        double prev = T[j + 1];                  // ghost row 0
+        double prev = T[j + 1];                        // ghost row 0
         const double below = T[(N + 1) * TP + j + 1];  // ghost row N+1
-        const double wj = (j == 0 || j == N - 1) ? 0.5 : 1.0;
 #pragma unroll
         for (int i = 0; i < N; ++i) {
             const double x = v[i];
@@ -222,9 +108,8 @@ __global__ void __launch_bounds__(Layout<N, P>::NT)
             out -= a.r * flux_upwind(x, yl, a.smax[3], a.smin[3]);
             prev = x;
             v[i] = out;
-            const double wi = (i == 0 || i == N - 1) ? 0.5 : 1.0;
-            mfv += (wi * wj) * out;
         }
+        mfv = col_mass<N>(j, v);
     }
     red_fv[t] = mfv;
 
@@ -235,6 +120,7 @@ __global__ void __launch_bounds__(Layout<N, P>::NT)
             const uint64_t off = atomicAdd(a.bump_out, (unsigned long long)bytes);
             if (off + bytes > a.cap_out) {
                 atomicOr(a.err, ERR_STORE_OVERFLOW);
+                a.dir_out[p] = DirEntry{0, 0u, DIR_DEAD};
                 slot_mode[ps] = 2;
             } else {
                 slot_mode[ps] = 1;
@@ -251,36 +137,14 @@ __global__ void __launch_bounds__(Layout<N, P>::NT)
         red[t] = mfv;
     } else {
         // ---- forward DWT along dim 0 (columns) in registers ---------------
-        if (valid) dwt_line_reg<N, L>(v);
         __syncthreads();  // everyone done reading the state tile
-        if (valid) {
-#pragma unroll
-            for (int r = 0; r < N; ++r) T[(corner_pos<N, L>(r) + 1) * TP + j + 1] = v[r];
-        }
+        if (valid) fwd_col_to_tile<N, L>(T, j, v);
         __syncthreads();
 
         // ---- ROW phase: forward DWT along dim 1, threshold, count ---------
         const int i = li;
         unsigned nz = 0, zr = 0;
-        if (valid) {
-#pragma unroll
-            for (int jj = 0; jj < N; ++jj) v[jj] = T[(i + 1) * TP + jj + 1];
-            dwt_line_reg<N, L>(v);
-            const int bi = band_of_pos(N, L, i);
-            double trow[L + 1];
-#pragma unroll
-            for (int bj = 0; bj <= L; ++bj) trow[bj] = a.thr[bi * (L + 1) + bj];
-#pragma unroll
-            for (int r = 0; r < N; ++r) {
-                const double x = v[r];
-                const bool nzx = x != 0.0;
-                const bool kill = fabs(x) < trow[band_of_r<N, L>(r)];
-                zr += (nzx && kill) ? 1u : 0u;
-                const bool keep = nzx && !kill;
-                v[r] = keep ? x : 0.0;  // also maps -0.0 to +0.0 like the CSR round trip
-                nz += keep ? 1u : 0u;
-            }
-        }
+        if (valid) fwd_row_threshold<N, L>(T, i, a.thr, v, nz, zr);
         cta_inclusive_scan<NT>(((unsigned long long)zr << 32) | nz, inc);
         unsigned long long slot_base = 0, slot_tot = 0;
         if (lane_ok) {
@@ -304,6 +168,7 @@ __global__ void __launch_bounds__(Layout<N, P>::NT)
                 const uint64_t off = atomicAdd(a.bump_out, (unsigned long long)bytes);
                 if (off + bytes > a.cap_out) {
                     atomicOr(a.err, ERR_STORE_OVERFLOW);
+                    a.dir_out[p] = DirEntry{0, 0u, DIR_DEAD};
                     slot_mode[ps] = 2;
                 } else {
                     slot_mode[ps] = 0;
@@ -315,79 +180,40 @@ __global__ void __launch_bounds__(Layout<N, P>::NT)
         __syncthreads();
         const bool compressed = valid && slot_mode[ps] == 0;
         if (compressed) {
-            // ordered CSR write of row i (ascending corner-layout columns)
-            unsigned char* base = a.store_out + slot_off[ps];
-            double* vo = reinterpret_cast<double*>(base);
-            uint32_t* co = reinterpret_cast<uint32_t*>(base + 8ull * nnz_tot);
-            uint32_t* ro = co + nnz_tot;
-            uint32_t k = (uint32_t)((inc[t] - slot_base) & 0xffffffffu) - nz;
-            if (i == 0) ro[0] = 0;
-            ro[i + 1] = k + nz;
-#pragma unroll
-            for (int pc = 0; pc < N; ++pc) {
-                const double x = v[interleaved_of<N, L>(pc)];
-                if (x != 0.0) {
-                    vo[k] = x;
-                    co[k] = (uint32_t)pc;
-                    ++k;
-                }
-            }
-            // reconstruction, dim 1 inverse (the decode of the next step)
-            idwt_line_reg<N, L>(v);
-#pragma unroll
-            for (int jj = 0; jj < N; ++jj) T[(i + 1) * TP + jj + 1] = v[jj];
+            const uint32_t k = (uint32_t)((inc[t] - slot_base) & 0xffffffffu) - nz;
+            write_csr_row<N, L>(a.store_out + slot_off[ps], nnz_tot, i, k, nz, v);
+            inv_row_to_tile<N, L>(T, i, v);  // reconstruction, dim 1 inverse
         }
         __syncthreads();
         double m = 0.0;
         if (compressed) {
-#pragma unroll
-            for (int r = 0; r < N; ++r) v[r] = T[(corner_pos<N, L>(r) + 1) * TP + j + 1];
-            idwt_line_reg<N, L>(v);
-            const double wj = (j == 0 || j == N - 1) ? 0.5 : 1.0;
-#pragma unroll
-            for (int ii = 0; ii < N; ++ii) {
-                const double wi = (ii == 0 || ii == N - 1) ? 0.5 : 1.0;
-                m += (wi * wj) * v[ii];
-            }
+            decode_col<N, L>(T, j, false, v);
+            m = col_mass<N>(j, v);
         }
         red[t] = m;
     }
 
     // ---- edge lines of the new state (ghost source of the next step) -----
-    const bool write_edges = valid && slot_mode[ps] == (MODE == MODE_RAW ? 1 : 0);
-    if (write_edges) {
-        const size_t own = ((size_t)(ar + 1) * P1 + b) * N;
-        a.eout.rowlo[own + j] = v[1];
-        a.eout.rowhi[own + j] = v[N - 2];
-        const size_t oc = ((size_t)ar * P1 + b) * N;
-        if (j == 1) {
-#pragma unroll
-            for (int i = 0; i < N; ++i) a.eout.collo[oc + i] = v[i];
-        }
-        if (j == N - 2) {
-#pragma unroll
-            for (int i = 0; i < N; ++i) a.eout.colhi[oc + i] = v[i];
-        }
-    }
+    if (valid && slot_mode[ps] == (MODE == MODE_RAW ? 1 : 0)) write_edges<N>(a.eout, pp, 0, g, j, v);
     __syncthreads();
     // ---- per-patch trapezoid masses (deterministic) ----------------------
     const int warp = t >> 5;
     for (int s = warp; s < P; s += NT / 32) {
-        const double mm = slot_sum<N, P, NT>(red, s);
-        const double mf = slot_sum<N, P, NT>(red_fv, s);
+        const double mm = warp_sum_range(red, s * N, N);
+        const double mf = warp_sum_range(red_fv, s * N, N);
         if ((t & 31) == 0) {
-            uint32_t ps_patch;
+            uint32_t q;
             bool ok;
             if (MODE == MODE_RAW && a.raw_list) {
                 const uint32_t k = blockIdx.x * P + s;
                 ok = k < *a.raw_count;
-                ps_patch = ok ? a.raw_list[k] : 0;
+                q = ok ? a.raw_list[k] : 0;
             } else {
-                ps_patch = blockIdx.x * P + s;
-                ok = ps_patch < g.npatch;
+                q = blockIdx.x * P + s;
+                ok = q < g.npatch;
             }
             if (ok && slot_mode[s] != 2) {
-                PatchStats& st = a.stats[ps_patch];
+                PatchStats& st = a.stats[q];
                 if (MODE == MODE_RAW) {
                     st.mass = mm;
                     st.mass_fv = mf;

@@ -1,0 +1,282 @@
+// patch_phases.cuh — the phases of the per-patch compression cycle as device
+// helpers shared by the transport and D2Q9 kernels.
+//
+// Ownership model: a "slot" is one (patch, component) tile of (N+2)^2
+// doubles in shared memory (odd pitch N+2: conflict-free for both the row-
+// and the column-ownership access pattern).  Thread li of a slot owns row li
+// in a ROW phase and column li in a COLUMN phase and keeps that whole line
+// in registers (double v[N]) while lifting (lifting.cuh).
+#pragma once
+
+#include "common.cuh"
+#include "lifting.cuh"
+#include "physics.cuh"
+#include "session.cuh"
+
+namespace wg {
+
+constexpr int kMaxLevels = 8;
+
+struct StepArgs {
+    const unsigned char* store_in;
+    const DirEntry* dir_in;
+    EdgeSet ein;
+    unsigned char* store_out;
+    DirEntry* dir_out;
+    EdgeSet eout;
+    PatchStats* stats;
+    unsigned long long* bump_out;
+    uint64_t cap_out;
+    uint32_t* raw_list;   // MODE_RAW: patches to store raw (nullptr = all patches)
+    uint32_t* raw_count;
+    uint32_t raw_capacity;
+    unsigned* err;
+    double* decode_out;   // MODE_DECODE: grid buffer (true layout) of this shard
+    double* scratch;      // D2Q9: per-CTA L2-resident staging of 9 N*N fields
+    ShardGeom g;
+    double smax[4], smin[4], r;                          // transport faces, dt/dx
+    double omega;                                        // D2Q9: 1/tau
+    double thr[(kMaxLevels + 1) * (kMaxLevels + 1)];     // T[band_i][band_j]
+};
+
+enum { MODE_MAIN = 0, MODE_RAW = 1, MODE_DECODE = 2 };
+
+struct PatchPos {
+    int ar;       // local patch row
+    uint32_t b;   // patch column
+    uint32_t bl, br;
+    uint32_t su, sd;  // edge row slots of the rows above / below
+};
+
+__device__ __forceinline__ PatchPos patch_pos(uint32_t p, const ShardGeom& g) {
+    PatchPos pp;
+    pp.ar = (int)(p / g.P1);
+    pp.b = p % g.P1;
+    pp.bl = (pp.b + g.P1 - 1) % g.P1;
+    pp.br = (pp.b + 1) % g.P1;
+    pp.su = row_slot(pp.ar - 1, g);
+    pp.sd = row_slot(pp.ar + 1, g);
+    return pp;
+}
+
+// Index of an edge line element: line arrays are [slot][P1][m][N].
+__device__ __forceinline__ size_t edge_ix(uint32_t slot, uint32_t b, uint32_t q, const ShardGeom& g,
+                                          int N) {
+    return (((size_t)slot * g.P1 + b) * g.m + q) * (size_t)N;
+}
+
+// ROW phase of the decode: row li of component (p, q) from the store into
+// the tile (CSR scatter or raw copy), inverse transform along dim 1
+// (idwt_nd, wavelet.hpp:200-223 does the last dimension first).  Returns
+// whether the stored block is raw.
+template <int N, int L>
+__device__ __forceinline__ bool decode_row(double* T, int li, const DirEntry e,
+                                           const unsigned char* store) {
+    constexpr int TP = N + 2;
+    const bool raw = (e.flags & DIR_RAW) != 0;
+    const unsigned char* base = store + e.off;
+    double* rowp = T + (li + 1) * TP + 1;
+    if (e.flags & DIR_DEAD) {  // overflowed block (error already raised): zeros, never garbage
+#pragma unroll
+        for (int j = 0; j < N; ++j) rowp[j] = 0.0;
+        return true;
+    }
+    if (raw) {
+        const double* d = reinterpret_cast<const double*>(base) + (size_t)li * N;
+#pragma unroll 8
+        for (int j = 0; j < N; ++j) rowp[j] = d[j];
+    } else {
+        const double* v = reinterpret_cast<const double*>(base);
+        const uint32_t* col = reinterpret_cast<const uint32_t*>(base + 8ull * e.nnz);
+        const uint32_t* ro = col + e.nnz;
+        const uint32_t k0 = ro[li], k1 = ro[li + 1];
+#pragma unroll
+        for (int j = 0; j < N; ++j) rowp[j] = 0.0;
+        for (uint32_t k = k0; k < k1; ++k) rowp[col[k]] = v[k];
+        double x[N];
+#pragma unroll
+        for (int r = 0; r < N; ++r) x[r] = rowp[corner_pos<N, L>(r)];
+        idwt_line_reg<N, L>(x);
+#pragma unroll
+        for (int j = 0; j < N; ++j) rowp[j] = x[j];
+    }
+    return raw;
+}
+
+// Ghost ring of the tile from the neighbours' reconstructed edge lines
+// (sync_ghosts, patchgrid.hpp:131-201: low ghost <- neighbour logical n-2,
+// high ghost <- neighbour logical 1; corners from the diagonal neighbours).
+template <int N>
+__device__ __forceinline__ void fill_ghosts(double* T, int li, const EdgeSet& e, const PatchPos& pp,
+                                            uint32_t q, const ShardGeom& g) {
+    constexpr int TP = N + 2;
+    const uint32_t own = row_slot(pp.ar, g);  // == ar + 1
+    (void)own;
+    T[(li + 1) * TP] = e.colhi[edge_ix(pp.ar, pp.bl, q, g, N) + li];
+    T[(li + 1) * TP + N + 1] = e.collo[edge_ix(pp.ar, pp.br, q, g, N) + li];
+    T[li + 1] = e.rowhi[edge_ix(pp.su, pp.b, q, g, N) + li];
+    T[(N + 1) * TP + li + 1] = e.rowlo[edge_ix(pp.sd, pp.b, q, g, N) + li];
+    if (li == 0) {
+        T[0] = e.rowhi[edge_ix(pp.su, pp.bl, q, g, N) + N - 2];
+        T[N + 1] = e.rowhi[edge_ix(pp.su, pp.br, q, g, N) + 1];
+        T[(N + 1) * TP] = e.rowlo[edge_ix(pp.sd, pp.bl, q, g, N) + N - 2];
+        T[(N + 1) * TP + N + 1] = e.rowlo[edge_ix(pp.sd, pp.br, q, g, N) + 1];
+    }
+}
+
+// COLUMN phase of the decode: column j -> registers (natural order), inverse
+// transform along dim 0 unless raw.
+template <int N, int L>
+__device__ __forceinline__ void decode_col(const double* T, int j, bool raw, double (&v)[N]) {
+    constexpr int TP = N + 2;
+    if (raw) {
+#pragma unroll
+        for (int i = 0; i < N; ++i) v[i] = T[(i + 1) * TP + j + 1];
+    } else {
+#pragma unroll
+        for (int r = 0; r < N; ++r) v[r] = T[(corner_pos<N, L>(r) + 1) * TP + j + 1];
+        idwt_line_reg<N, L>(v);
+    }
+}
+
+template <int N>
+__device__ __forceinline__ void store_col(double* T, int j, const double (&v)[N]) {
+    constexpr int TP = N + 2;
+#pragma unroll
+    for (int i = 0; i < N; ++i) T[(i + 1) * TP + j + 1] = v[i];
+}
+
+// Forward transform along dim 0 of a register column, stored into the tile
+// in corner layout.
+template <int N, int L>
+__device__ __forceinline__ void fwd_col_to_tile(double* T, int j, double (&v)[N]) {
+    constexpr int TP = N + 2;
+    dwt_line_reg<N, L>(v);
+#pragma unroll
+    for (int r = 0; r < N; ++r) T[(corner_pos<N, L>(r) + 1) * TP + j + 1] = v[r];
+}
+
+// ROW phase of the compression: forward transform along dim 1 of row i,
+// threshold (threshold.hpp:51-86: samples untouched, strict <, v != 0),
+// count kept and zeroed coefficients.  -0.0 becomes +0.0 like the CSR
+// round trip of pipeline.hpp:234-237.
+template <int N, int L>
+__device__ __forceinline__ void fwd_row_threshold(const double* T, int i, const double* thr,
+                                                  double (&v)[N], unsigned& nz, unsigned& zr) {
+    constexpr int TP = N + 2;
+#pragma unroll
+    for (int jj = 0; jj < N; ++jj) v[jj] = T[(i + 1) * TP + jj + 1];
+    dwt_line_reg<N, L>(v);
+    const int bi = band_of_pos(N, L, i);
+    double trow[L + 1];
+#pragma unroll
+    for (int bj = 0; bj <= L; ++bj) trow[bj] = thr[bi * (L + 1) + bj];
+    nz = 0;
+    zr = 0;
+#pragma unroll
+    for (int r = 0; r < N; ++r) {
+        const double x = v[r];
+        const bool nzx = x != 0.0;
+        const bool kill = fabs(x) < trow[band_of_r<N, L>(r)];
+        zr += (nzx && kill) ? 1u : 0u;
+        const bool keep = nzx && !kill;
+        v[r] = keep ? x : 0.0;
+        nz += keep ? 1u : 0u;
+    }
+}
+
+// Ordered CSR write of row i (csr_encode, codec.hpp:37-60: row-major,
+// ascending columns, u32 offsets from 0) at entry offset k.
+template <int N, int L>
+__device__ __forceinline__ void write_csr_row(unsigned char* base, uint32_t nnz_tot, int i, uint32_t k,
+                                              unsigned nz, const double (&v)[N]) {
+    double* vo = reinterpret_cast<double*>(base);
+    uint32_t* co = reinterpret_cast<uint32_t*>(base + 8ull * nnz_tot);
+    uint32_t* ro = co + nnz_tot;
+    if (i == 0) ro[0] = 0;
+    ro[i + 1] = k + nz;
+#pragma unroll
+    for (int pc = 0; pc < N; ++pc) {
+        const double x = v[interleaved_of<N, L>(pc)];
+        if (x != 0.0) {
+            vo[k] = x;
+            co[k] = (uint32_t)pc;
+            ++k;
+        }
+    }
+}
+
+// Inverse transform of a thresholded register row, stored into the tile.
+template <int N, int L>
+__device__ __forceinline__ void inv_row_to_tile(double* T, int i, double (&v)[N]) {
+    constexpr int TP = N + 2;
+    idwt_line_reg<N, L>(v);
+#pragma unroll
+    for (int jj = 0; jj < N; ++jj) T[(i + 1) * TP + jj + 1] = v[jj];
+}
+
+// Edge lines of the new state from a register column j (natural order).
+template <int N>
+__device__ __forceinline__ void write_edges(const EdgeSet& e, const PatchPos& pp, uint32_t q,
+                                            const ShardGeom& g, int j, const double (&v)[N]) {
+    const size_t own = edge_ix((uint32_t)(pp.ar + 1), pp.b, q, g, N);
+    e.rowlo[own + j] = v[1];
+    e.rowhi[own + j] = v[N - 2];
+    const size_t oc = edge_ix((uint32_t)pp.ar, pp.b, q, g, N);
+    if (j == 1) {
+#pragma unroll
+        for (int i = 0; i < N; ++i) e.collo[oc + i] = v[i];
+    }
+    if (j == N - 2) {
+#pragma unroll
+        for (int i = 0; i < N; ++i) e.colhi[oc + i] = v[i];
+    }
+}
+
+// Trapezoid-weighted column sum (global_mass weights, patchgrid.hpp:244-266).
+template <int N>
+__device__ __forceinline__ double col_mass(int j, const double (&v)[N]) {
+    const double wj = (j == 0 || j == N - 1) ? 0.5 : 1.0;
+    double m = 0.0;
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+        const double wi = (i == 0 || i == N - 1) ? 0.5 : 1.0;
+        m += (wi * wj) * v[i];
+    }
+    return m;
+}
+
+// Inclusive scan of one u64 per thread over the CTA (warp shuffles + one
+// shared pass); result written to inc[threadIdx.x].  Contains barriers.
+template <int NT>
+__device__ __forceinline__ void cta_inclusive_scan(unsigned long long x, unsigned long long* inc) {
+    __shared__ unsigned long long wtot[NT / 32];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    __syncthreads();  // wtot may still be read by a previous scan
+    if (lane == 31) wtot[w] = x;
+    __syncthreads();
+    unsigned long long before = 0;
+#pragma unroll
+    for (int k = 0; k < NT / 32; ++k)
+        if (k < w) before += wtot[k];
+    inc[threadIdx.x] = x + before;
+    __syncthreads();
+}
+
+// Deterministic sum of red[base .. base+n): fixed lane assignment and a
+// fixed shuffle tree (called by a whole warp).
+__device__ __forceinline__ double warp_sum_range(const double* red, int base, int n) {
+    const int lane = threadIdx.x & 31;
+    double s = 0.0;
+    for (int k = lane; k < n; k += 32) s += red[base + k];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    return s;
+}
+
+}  // namespace wg

@@ -18,6 +18,7 @@
 
 #include "common.cuh"
 #include "host_model.h"
+#include "lbm_kernels.cuh"
 #include "patch_kernels.cuh"
 
 namespace wg {
@@ -31,10 +32,43 @@ struct KernelSet {
     void (*main)(StepArgs);
     void (*raw)(StepArgs);
     void (*decode)(StepArgs);
-    int P;
+    int P;               // patches per CTA (non-persistent kernels)
     int threads;
     size_t smem;
+    bool persistent;     // D2Q9: grid-stride over patches with per-CTA scratch
+    size_t scratch_doubles;  // per CTA
 };
+
+template <int N, int L>
+KernelSet make_lbm_set() {
+    using Lay = LbmLayout<N>;
+    KernelSet k;
+    k.main = k_lbm_step<N, L, MODE_MAIN>;
+    k.raw = k_lbm_step<N, L, MODE_RAW>;
+    k.decode = k_lbm_step<N, L, MODE_DECODE>;
+    k.P = 1;
+    k.threads = Lay::NT;
+    k.smem = Lay::smem_bytes();
+    k.persistent = true;
+    k.scratch_doubles = Lay::scratch_doubles();
+    for (auto f : {k.main, k.raw, k.decode}) {
+        WG_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k.smem));
+    }
+    return k;
+}
+
+template <int N, int L = 0>
+bool pick_lbm_levels(int levels, KernelSet& out) {
+    if constexpr ((1 << L) <= N - 1 && L <= 6) {
+        if (levels == L) {
+            out = make_lbm_set<N, L>();
+            return true;
+        }
+        return pick_lbm_levels<N, L + 1>(levels, out);
+    } else {
+        return false;
+    }
+}
 
 template <int N, int L, int P>
 KernelSet make_set() {
@@ -46,6 +80,8 @@ KernelSet make_set() {
     k.P = P;
     k.threads = Lay::NT;
     k.smem = Lay::smem_bytes();
+    k.persistent = false;
+    k.scratch_doubles = 0;
     for (auto f : {k.main, k.raw, k.decode}) {
         WG_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k.smem));
     }
@@ -65,9 +101,21 @@ bool pick_levels(int levels, KernelSet& out) {
     }
 }
 
-KernelSet select_kernels(uint64_t n, int levels) {
+KernelSet select_kernels(int scheme, uint64_t n, int levels) {
     KernelSet k{};
     bool ok = false;
+    if (scheme == WG_SCHEME_LBM_D2Q9) {
+        switch (n) {
+            case 17: ok = pick_lbm_levels<17>(levels, k); break;
+            case 33: ok = pick_lbm_levels<33>(levels, k); break;
+            case 65: ok = pick_lbm_levels<65>(levels, k); break;
+            default: break;
+        }
+        if (!ok)
+            raise(WG_INVALID_ARGUMENT, "device session (D2Q9): patch side " + std::to_string(n) + " with " +
+                                           std::to_string(levels) + " levels is not supported (n in 17,33,65)");
+        return k;
+    }
     switch (n) {
         case 9: ok = pick_levels<9, 7>(levels, k); break;
         case 17: ok = pick_levels<17, 15>(levels, k); break;
@@ -194,6 +242,8 @@ struct Session {
     EdgeSet edges[2]{};
     double* edge_mem[2] = {nullptr, nullptr};
     PatchStats* stats = nullptr;
+    double* scratch = nullptr;           // D2Q9 per-CTA staging (L2-resident)
+    unsigned grid = 0;                   // launch grid of the step kernels
     unsigned long long* bump = nullptr;  // [2]
     uint32_t* raw_list = nullptr;
     uint32_t* raw_count = nullptr;
@@ -209,10 +259,37 @@ struct Session {
     double time = 0.0;
     double thr[(kMaxLevels + 1) * (kMaxLevels + 1)] = {};
 
+    // optional per-launch timing of the fused kernel (bench roofline)
+    bool profiling = false;
+    std::vector<cudaEvent_t> ev_pool;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_main;
+
     ~Session() { release(); }
+
+    cudaEvent_t take_event() {
+        cudaEvent_t e;
+        if (!ev_pool.empty()) {
+            e = ev_pool.back();
+            ev_pool.pop_back();
+        } else {
+            WG_CUDA(cudaEventCreate(&e));
+        }
+        return e;
+    }
+
+    void clear_profile() {
+        for (auto& pr : ev_main) {
+            ev_pool.push_back(pr.first);
+            ev_pool.push_back(pr.second);
+        }
+        ev_main.clear();
+    }
 
     void release() {
         if (stream) cudaStreamSynchronize(stream);
+        clear_profile();
+        for (auto e : ev_pool) cudaEventDestroy(e);
+        ev_pool.clear();
         for (int k = 0; k < 2; ++k) {
             cudaFree(store[k]);
             cudaFree(dir[k]);
@@ -222,6 +299,8 @@ struct Session {
             edge_mem[k] = nullptr;
         }
         cudaFree(stats);
+        cudaFree(scratch);
+        scratch = nullptr;
         cudaFree(bump);
         cudaFree(raw_list);
         cudaFree(raw_count);
@@ -254,8 +333,10 @@ struct Session {
     void create(const wg_run_config& c, const wg_shard* sh, void* strm) {
         cfg = c;
         if (cfg.codec != 1) raise(WG_INVALID_ARGUMENT, "only Codec::csr is on the hot path");
-        if (cfg.scheme != WG_SCHEME_TRANSPORT)
+        if (cfg.scheme != WG_SCHEME_TRANSPORT && cfg.scheme != WG_SCHEME_LBM_D2Q9)
             raise(WG_INVALID_ARGUMENT, "device session: scheme not supported by this build");
+        if (cfg.scheme == WG_SCHEME_LBM_D2Q9 && cfg.lbm_tau <= 0.5)
+            raise(WG_INVALID_ARGUMENT, "LBM: tau must exceed 1/2");
         geo = run_geometry(cfg);
         if (geo.n[0] != geo.n[1]) raise(WG_INVALID_ARGUMENT, "device session: square patches only");
         N = (uint32_t)geo.n[0];
@@ -286,7 +367,16 @@ struct Session {
         sg.m = geo.m;
         sg.world = shard.world;
         sg.npatch = sg.R * sg.P1;
-        ks = select_kernels(N, levels);
+        ks = select_kernels(cfg.scheme, N, levels);
+        if (ks.persistent) {
+            int per_sm = 0, sms = 0;
+            WG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ks.main, ks.threads, ks.smem));
+            WG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, shard.device));
+            grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(sg.npatch, (uint64_t)std::max(per_sm, 1) * sms));
+            scratch = dalloc<double>((uint64_t)grid * ks.scratch_doubles);
+        } else {
+            grid = (sg.npatch + ks.P - 1) / ks.P;
+        }
         // thresholds (threshold.hpp:31-47) — the "c == 0 or levels == 0"
         // early return of apply_threshold (threshold.hpp:53) is T = 0.
         if (cfg.c == 0.0 || levels == 0) std::fill(std::begin(thr), std::end(thr), 0.0);
@@ -391,14 +481,25 @@ struct Session {
         StepArgs a = step_args(src, dst);
         direction_speeds(cfg.alpha, cfg.beta, a.smax, a.smin);
         a.r = dt / sim_dx(cfg);  // solver.hpp:212
-        const unsigned grid = (sg.npatch + ks.P - 1) / ks.P;
+        a.omega = 1.0 / cfg.lbm_tau;
+        a.scratch = scratch;
         if (cfg.no_compression) {
             a.raw_list = nullptr;
             ks.raw<<<grid, ks.threads, ks.smem, stream>>>(a);
             WG_LAUNCH_CHECK("raw step");
         } else {
+            cudaEvent_t e0 = nullptr, e1 = nullptr;
+            if (profiling) {
+                e0 = take_event();
+                e1 = take_event();
+                WG_CUDA(cudaEventRecord(e0, stream));
+            }
             ks.main<<<grid, ks.threads, ks.smem, stream>>>(a);
             WG_LAUNCH_CHECK("fused step");
+            if (profiling) {
+                WG_CUDA(cudaEventRecord(e1, stream));
+                ev_main.emplace_back(e0, e1);
+            }
             ks.raw<<<grid, ks.threads, ks.smem, stream>>>(a);
             WG_LAUNCH_CHECK("skip-rule step");
         }
@@ -435,7 +536,7 @@ struct Session {
         WG_CUDA(cudaMemsetAsync(d.p, 0, n * sizeof(double), stream));
         StepArgs a = step_args(cur, 1 - cur);
         a.decode_out = d.p;
-        const unsigned grid = (sg.npatch + ks.P - 1) / ks.P;
+        a.scratch = scratch;
         ks.decode<<<grid, ks.threads, ks.smem, stream>>>(a);
         WG_LAUNCH_CHECK("decode");
         WG_CUDA(cudaMemcpyAsync(hgrid, d.p, n * sizeof(double), cudaMemcpyDeviceToHost, stream));
@@ -541,6 +642,30 @@ wg_status wg_session_patch_csr(wg_session* s, uint64_t patch, uint32_t comp, dou
 
 wg_status wg_session_sync(wg_session* s) {
     return guard([&] { reinterpret_cast<Session*>(s)->sync(); });
+}
+
+wg_status wg_session_profile(wg_session* sp, int32_t enable) {
+    return guard([&] {
+        Session* s = reinterpret_cast<Session*>(sp);
+        s->sync();
+        s->clear_profile();
+        s->profiling = enable != 0;
+    });
+}
+
+wg_status wg_session_profile_read(wg_session* sp, double* main_ms, uint64_t* launches) {
+    return guard([&] {
+        Session* s = reinterpret_cast<Session*>(sp);
+        s->sync();
+        double tot = 0.0;
+        for (auto& pr : s->ev_main) {
+            float ms = 0.f;
+            WG_CUDA(cudaEventElapsedTime(&ms, pr.first, pr.second));
+            tot += ms;
+        }
+        if (main_ms) *main_ms = tot;
+        if (launches) *launches = s->ev_main.size();
+    });
 }
 
 // run(RunConfig) (pipeline.hpp:129-305) on one device through a session.

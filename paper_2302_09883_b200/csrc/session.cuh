@@ -21,6 +21,7 @@
 namespace wg {
 
 constexpr uint32_t DIR_RAW = 1u;
+constexpr uint32_t DIR_DEAD = 2u;  // block lost to a store overflow: decodes as zeros, error raised
 
 struct DirEntry {
     uint64_t off;    // byte offset in the pool

@@ -173,3 +173,46 @@ def test_budget_overflow_fails_loudly(product):
             product.check(product.wg_session_upload(s, abi.dptr(g0.data)))
     finally:
         product.wg_session_destroy(s)
+
+
+# ---- D2Q9 LBM (builder-defined scheme on the reference's compression machinery) ----
+
+
+def lbm_cfg(nx, splits, levels, c, steps, mode="capped", **kw):
+    return api.RunConfig(scheme="lbm", nx=nx, splits=splits, levels=levels, lbm_steps=steps,
+                         spec=api.ThresholdSpec(mode, c), **kw)
+
+
+@pytest.mark.parametrize(
+    "nx,splits,levels,c,steps",
+    [(129, (4, 4), 4, 1e-3, 10),   # 33^2 patches
+     (129, (2, 2), 4, 1e-3, 6),    # 65^2 patches (C2 patch shape)
+     (129, (2, 2), 5, 1e-5, 5),    # L = 5 on 65^2, smallest threshold of the C2 sweep
+     (65, (4, 4), 3, 1e-2, 8),     # 17^2 patches, largest threshold of the sweep
+     (65, (1, 1), 3, 1e-4, 4),     # single periodic patch
+     (129, (2, 2), 4, 0.0, 3)],    # nothing zeroed: every patch raw (skip rule)
+)
+def test_lbm_parity(product, oracle, nx, splits, levels, c, steps):
+    cfg = lbm_cfg(nx, splits, levels, c, steps)
+    compare_runs(api.run(cfg, lib=product), api.run(cfg, lib=oracle))
+
+
+def test_lbm_no_compression_parity(product, oracle):
+    cfg = lbm_cfg(129, (4, 4), 4, 1e-3, 6, no_compression=True)
+    compare_runs(api.run(cfg, lib=product), api.run(cfg, lib=oracle))
+
+
+def test_lbm_golden(product):
+    gold = json.loads((GOLDEN / "small_lbm.json").read_text())
+    r = api.run(lbm_cfg(129, (4, 4), 4, 1e-3, 20), lib=product)
+    assert len(r.rows) == gold["steps"]
+    for row, g in zip(r.rows, gold["rows"]):
+        assert (row["nnz"], row["zeroed"], row["compressed_bytes"]) == (g["nnz"], g["zeroed"], g["compressed_bytes"])
+    import hashlib
+    assert hashlib.sha256(np.ascontiguousarray(r.grid.logical_view()).tobytes()).hexdigest() == gold["state_sha256"]
+
+
+def test_lbm_mass_conserved(product):
+    r = api.run(lbm_cfg(129, (2, 2), 4, 1e-3, 30), lib=product)
+    m0 = r.rows[0]["global_mass"]
+    assert all(abs(x["global_mass"] - m0) <= 1e-12 * abs(m0) for x in r.rows)
