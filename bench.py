@@ -1,0 +1,380 @@
+#!/usr/bin/env python
+"""Benchmark of the compressed stencil loop (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload lbm_c2]
+    python bench.py --impl reference ...      # the reference CPU path
+
+A "step" is one pass of the hot path over the whole grid: ghost lines ->
+decode -> scheme update -> DWT -> threshold -> CSR -> reconstruction, for
+every patch (pipeline.hpp:194-289).  The default workload is BASELINE.json
+configs[1]: D2Q9 LBM on 1024^2 cells in 64^2-cell patches (65^2 points),
+level 4, capped threshold 1e-3 (the middle of the 1e-2..1e-5 sweep; the sweep
+itself is a parity/accuracy test case), synthetic shear-layer initial state.
+With N > 1 ranks (torchrun) the patch rows of the same grid are sharded
+(strong scaling) and the halo lines move over NCCL every step.
+
+Prints ONE JSON line (rank 0).  Timing: CUDA events around every step on the
+session stream, L2 flushed (a 256 MiB write) between timed steps outside the
+events; max over ranks.  `roofline` uses the algorithmic bytes of SURVEY §8d
+(2 m 8 B per cell-update, the uncompressed-equivalent state traffic).
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+REPO = Path(__file__).resolve().parent
+sys.path.insert(0, str(REPO))
+
+import numpy as np  # noqa: E402
+
+from paper_2302_09883_b200 import abi, api  # noqa: E402
+
+METRIC = "MLUPS (cell-updates/s) w/ compression @1/2/4/8 B200; HBM roofline %; compression ratio"
+
+WORKLOADS = {
+    # BASELINE.json configs[1] (C2)
+    "lbm_c2": dict(scheme="lbm", nx=1025, splits=(16, 16), levels=4, c=1e-3, mode="capped"),
+    # BASELINE.json configs[0] (C1): the reference's own CPU-runnable case
+    "transport_c1": dict(scheme="transport", nx=257, splits=(8, 8), levels=4, c=1e-3, mode="capped"),
+    # C3-sized transport grid in 32^2-cell patches (C1 patch shape)
+    "transport_4k_p33": dict(scheme="transport", nx=4097, splits=(128, 128), levels=4, c=1e-3, mode="capped"),
+    # C3-sized transport grid (4096^2 cells, 64^2-cell patches)
+    "transport_4k": dict(scheme="transport", nx=4097, splits=(64, 64), levels=4, c=1e-3, mode="capped"),
+}
+
+B_ALG = {"transport": 16, "swe": 48, "lbm": 144}  # bytes per cell-update, SURVEY §8d
+
+
+def run_config(w: dict, steps: int) -> api.RunConfig:
+    cfg = api.RunConfig(scheme=w["scheme"], nx=w["nx"], splits=tuple(w["splits"]), levels=w["levels"],
+                        spec=api.ThresholdSpec(w["mode"], w["c"]), compute_l2=False, lbm_steps=steps)
+    if w["scheme"] == "transport":
+        cfg.t_end = steps * cfg.cfl * (1.0 / (w["nx"] - 1)) / max(cfg.alpha, cfg.beta)
+    return cfg
+
+
+def transport_dt(cfg: api.RunConfig) -> float:
+    return cfg.cfl * (cfg.domain_length / (cfg.nx - 1)) / max(cfg.alpha, cfg.beta)
+
+
+def peaks() -> dict:
+    p = REPO / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return {"hbm_gbs": d["hbm_gbs"], "source": "measured (MEASURED_PEAKS.json)"}
+    return {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)"}
+
+
+# ---- clocks sampler (nvidia-smi during the timed region) -----------------------
+_REASON_BITS = {
+    0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+    0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+    0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
+}
+
+
+class ClockSampler:
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines: list[str] = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except (FileNotFoundError, OSError):
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def count(self) -> int:
+        return len(self.lines)
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+            self.thread.join(timeout=2)
+
+    def summary(self) -> dict:
+        sm, mx, reasons = [], None, set()
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 3:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+                bits = int(parts[2], 16)
+            except ValueError:
+                continue
+            for b, name in _REASON_BITS.items():
+                if bits & b and name != "gpu_idle":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---- CPU baselines (oracles: the checker, timed only as the reported baseline) ---
+
+
+def cpu_lib():
+    ref = REPO / "oracle" / "_ref" / "libwg_ref.so"
+    if ref.exists():
+        return abi.Lib(ref), "reference"
+    port = REPO / "oracle" / "libwg_oracle.so"
+    if not port.exists():
+        subprocess.run(["make", "-s", "-C", str(REPO / "oracle"), "c"], check=True)
+    return abi.Lib(port), "port"
+
+
+def cpu_run(w: dict, steps: int, threads: int):
+    """Time the CPU implementation on `steps` steps of the workload; returns
+    (MLUPS, seconds, kind, cores, rows)."""
+    lib, kind = cpu_lib()
+    cfg = run_config(w, steps)
+    cfg.threads = threads if kind == "reference" else 1
+    res = api.run(cfg, lib=lib)
+    secs = res.summary["total_seconds"]
+    cells = (w["nx"] - 1) ** 2
+    return cells * steps / secs / 1e6, secs, kind, cfg.threads, res.rows
+
+
+# ---- the reference arm -----------------------------------------------------------
+
+
+def bench_reference(args, w: dict):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return  # the reference CPU path runs once, on rank 0
+    threads = os.cpu_count() or 1
+    if args.warmup:
+        cpu_run(w, max(1, min(args.warmup, 2)), threads)
+    mlups, secs, kind, cores, rows = cpu_run(w, args.steps, threads)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": mlups, "unit": "MLUPS", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * secs / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (reference initial state)", "config": config_json(args, w),
+        "compression_ratio": statistics.fmean(r["ratio"] for r in rows),
+        "cpu_baseline": {"value": mlups, "unit": "MLUPS", "cores": cores, "kind": kind,
+                         "sample": f"{args.steps} steps of the full {w['nx'] - 1}^2 workload, run() of the "
+                                   f"{'reference headers (oracle/_ref)' if kind == 'reference' else 'C port'}"},
+        "e2e": {"value": mlups, "unit": "MLUPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def config_json(args, w):
+    n = (w["nx"] - 1) // w["splits"][0] + 1
+    return {"workload": args.workload, "scheme": w["scheme"], "grid_cells": f"{w['nx'] - 1}x{w['nx'] - 1}",
+            "patch_points": f"{n}x{n}", "patches": w["splits"][0] * w["splits"][1], "levels": w["levels"],
+            "threshold": f"{w['mode']} c={w['c']}", "codec": "csr",
+            "parallelism": f"patch-row shards x{args.gpus}", "l2": "flushed between timed steps (256 MiB write)"}
+
+
+# ---- the B200 arm ----------------------------------------------------------------
+
+
+def bench_b200(args, w: dict):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2302_09883_b200.distributed import ShardInfo, ShardedSession, reduce_rows, shard_rows
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    lib = abi.load_product()
+    cfg = run_config(w, args.warmup + args.steps)
+    dt = transport_dt(cfg) if w["scheme"] == "transport" else 1.0
+    P0 = w["splits"][0]
+    rb, re_ = shard_rows(P0, rank, world)
+    shard = ShardInfo(rank, world, rb, re_, local)
+    # a dedicated (non-default) stream: the session launches on it and the
+    # CUDA events below are recorded on it
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+
+    # initial state on the host (glibc libm, bit-identical to the reference IC)
+    full = api.initial_state(cfg, lib=lib)
+    own = np.ascontiguousarray(full.data[rb * w["splits"][1]: re_ * w["splits"][1]])
+    pinned = torch.empty(own.size, dtype=torch.float64, pin_memory=True)
+    host = pinned.numpy()
+    host[:] = own.reshape(-1)
+    del full
+
+    sess = ShardedSession(lib, cfg, shard, stream.cuda_stream, dist if world > 1 else None)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{local}")
+    try:
+        sess.upload(host)
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        with ClockSampler(local) as clocks:
+            # warm-up: at least W steps, continued until the clock sampler is
+            # producing samples under load (bounded), so that the clocks
+            # reported are those of the loaded GPU around the timed region
+            t_w = time.perf_counter()
+            done = 0
+            while done < args.warmup or (world == 1 and clocks.count() < 3 and time.perf_counter() - t_w < 5.0):
+                sess.step(dt)
+                done += 1
+                if done % 8 == 0:
+                    sess.sync()
+            sess.sync()
+            warm_steps = done
+            lib.check(lib.wg_session_profile(sess.handle, 1))
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize()
+            for e0, e1 in evs:
+                flush.zero_()
+                e0.record(stream)
+                sess.step(dt)
+                e1.record(stream)
+            torch.cuda.synchronize()
+            if world > 1:
+                dist.barrier()
+        step_ms = [e0.elapsed_time(e1) for e0, e1 in evs]
+        tot_ms = sum(step_ms)
+        main_ms, launches = C.c_double(), abi.u64()
+        lib.check(lib.wg_session_profile_read(sess.handle, C.byref(main_ms), C.byref(launches)))
+        lib.check(lib.wg_session_profile(sess.handle, 0))
+        rows = sess.rows()
+        info = sess.info
+        if world > 1:
+            t = torch.tensor([tot_ms, main_ms.value], dtype=torch.float64, device=f"cuda:{local}")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            tot_ms, main_max = t.tolist()
+            rows = reduce_rows(rows, dist, f"cuda:{local}")
+        else:
+            main_max = main_ms.value
+        sess.close()
+
+        # ---- end to end through the public API with host buffers -------------
+        e2e = e2e_run(lib, cfg, shard, stream, host, args, dt, dist if world > 1 else None)
+    finally:
+        sess.close()
+
+    cells_global = (w["nx"] - 1) ** 2
+    value = cells_global * args.steps / (tot_ms * 1e-3) / 1e6
+    pk = peaks()
+    cells_local = info.cells_per_step
+    launch_ms = main_ms.value / max(launches.value, 1)
+    achieved = cells_local * B_ALG[w["scheme"]] / (launch_ms * 1e-3) / 1e9
+    timed_rows = rows[warm_steps:]
+    line = {
+        "metric": METRIC, "value": value, "unit": "MLUPS", "n_gpus": world, "steps": args.steps,
+        "warmup": warm_steps, "ms_per_step": tot_ms / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (shear-layer D2Q9 initial state)" if w["scheme"] == "lbm" else "synthetic (reference initial state)",
+        "config": config_json(args, w),
+        "compression_ratio": statistics.fmean(r["ratio"] for r in timed_rows),
+        "compressed_bytes_per_step": statistics.fmean(r["compressed_bytes"] for r in timed_rows),
+        "mass_drift": abs(timed_rows[-1]["global_mass"] - rows[0]["global_mass"]) / abs(rows[0]["global_mass"]),
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                     "frac": achieved / pk["hbm_gbs"], "traffic": traffic_from_profiles(args.workload),
+                     "kernel": f"k_{'lbm' if w['scheme'] == 'lbm' else 'patch'}_step<MAIN>",
+                     "algorithmic_bytes_per_launch": cells_local * B_ALG[w["scheme"]],
+                     "avg_launch_ms": launch_ms, "peak_source": pk["source"],
+                     "step_share": main_max / tot_ms if tot_ms else None},
+        "e2e": e2e,
+        "gpu_launches": 3 * args.steps,
+        "clocks": clocks.summary(),
+        "device_bytes": info.device_bytes,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu_steps = args.cpu_steps
+        mlups, secs, kind, cores, _ = cpu_run(w, cpu_steps, os.cpu_count() or 1)
+        line["cpu_baseline"] = {"value": mlups, "unit": "MLUPS", "cores": cores, "kind": kind,
+                                "sample": f"{cpu_steps} steps of the full {w['nx'] - 1}^2 workload ({secs:.1f} s)"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def e2e_run(lib, cfg, shard, stream, host, args, dt, dist):
+    """Same metric through the public API: the host state is uploaded from
+    pinned memory inside the timed region and every step's metrics row is
+    read back to the host."""
+    import torch
+
+    from paper_2302_09883_b200.distributed import ShardedSession
+
+    sess = ShardedSession(lib, cfg, shard, stream.cuda_stream, dist)
+    try:
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        sess.upload(host)
+        for _ in range(args.steps):
+            sess.step(dt)
+            sess.last_row()
+        torch.cuda.synchronize()
+        secs = time.perf_counter() - t0
+        if dist:
+            t = torch.tensor([secs], dtype=torch.float64, device=f"cuda:{shard.device}")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            secs = t.item()
+    finally:
+        sess.close()
+    cells = (cfg.nx - 1) ** 2
+    return {"value": cells * args.steps / secs / 1e6, "unit": "MLUPS",
+            "h2d_bytes_per_step": host.nbytes / args.steps, "d2h_bytes_per_step": C.sizeof(abi.MetricsRowC),
+            "note": "initial state uploaded once inside the timed region (bytes amortised per step); "
+                    "one metrics row read back per step"}
+
+
+def traffic_from_profiles(workload: str):
+    p = REPO / "profiles" / "traffic.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return d.get(workload)
+    return None
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="lbm_c2")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-steps", type=int, default=10)
+    args = ap.parse_args()
+    if args.impl == "b200":
+        args.warmup = max(args.warmup, 3)  # timing rule: at least 3 untimed warm-up steps
+    w = WORKLOADS[args.workload]
+    if args.impl == "reference":
+        bench_reference(args, w)
+    else:
+        bench_b200(args, w)
+
+
+if __name__ == "__main__":
+    main()

@@ -263,6 +263,10 @@ wg_status wg_session_halo(wg_session* s, double** send_lo, double** send_hi,
 wg_status wg_session_metrics(wg_session* s, wg_metrics_row* rows,
                              uint64_t max_rows, uint64_t* nrows);
 
+/* The latest step's metrics row, read back to the host (synchronises the
+ * session stream: the per-step device->host result read of the e2e path). */
+wg_status wg_session_last_row(wg_session* s, wg_metrics_row* row);
+
 /* Decode the current state into a host grid buffer (logical cells). */
 wg_status wg_session_download(wg_session* s, double* host_grid);
 

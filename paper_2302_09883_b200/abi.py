@@ -216,6 +216,7 @@ _PROTOS = {
     "wg_session_step": (i32, [vp, f64]),
     "wg_session_halo": (i32, [vp, P(vp), P(vp), P(vp), P(vp)]),
     "wg_session_metrics": (i32, [vp, P(MetricsRowC), u64, P(u64)]),
+    "wg_session_last_row": (i32, [vp, P(MetricsRowC)]),
     "wg_session_download": (i32, [vp, dp]),
     "wg_session_patch_csr": (i32, [vp, u64, u32, dp, P(u32), P(u32), P(u64), P(i32)]),
     "wg_session_sync": (i32, [vp]),

@@ -34,6 +34,55 @@ struct LbmLayout {
     static constexpr size_t scratch_doubles() { return (size_t)9 * N * N; }
 };
 
+// decode + pull streaming (3 rounds of 3 populations) then BGK collide, all
+// into the scratch S; returns this thread's trapezoid mass partial of the
+// collided state.  Uniform: every thread of the CTA calls it.
+template <int N, int L>
+__device__ __forceinline__ double decode_stream_collide(const StepArgs& a, double* T, double* S, uint32_t p,
+                                                        const PatchPos& pp, int s, int li, bool lane_ok) {
+    using Lay = LbmLayout<N>;
+    constexpr int TP = Lay::TP, NT = Lay::NT, NN = N * N;
+    for (int rd = 0; rd < 3; ++rd) {
+        const int q = 3 * rd + s;
+        bool raw_in = false;
+        if (lane_ok) {
+            raw_in = decode_row<N, L>(T, li, a.dir_in[(size_t)p * 9 + q], a.store_in);
+            fill_ghosts<N>(T, li, a.ein, pp, q, a.g);
+        }
+        __syncthreads();
+        if (lane_ok && !raw_in) {
+            double v[N];
+            decode_col<N, L>(T, li, false, v);
+            store_col<N>(T, li, v);
+        }
+        __syncthreads();
+        if (lane_ok) {  // pull streaming f_q(x) <- f_q(x - c_q), ghost ring included
+            const int cx = lbm_cx(q), cy = lbm_cy(q);
+            double* Sq = S + (size_t)q * NN;
+            const int j = li;
+#pragma unroll 5
+            for (int i = 0; i < N; ++i) Sq[i * N + j] = T[(i + 1 - cx) * TP + (j + 1 - cy)];
+        }
+        __syncthreads();
+    }
+    double mfv = 0.0;
+    for (int c = threadIdx.x; c < NN; c += NT) {
+        double f[9];
+#pragma unroll
+        for (int q = 0; q < 9; ++q) f[q] = S[(size_t)q * NN + c];
+        lbm_collide(f, a.omega);
+        const int i = c / N, j = c - (c / N) * N;
+        const double w = ((i == 0 || i == N - 1) ? 0.5 : 1.0) * ((j == 0 || j == N - 1) ? 0.5 : 1.0);
+#pragma unroll
+        for (int q = 0; q < 9; ++q) {
+            S[(size_t)q * NN + c] = f[q];
+            mfv += w * f[q];
+        }
+    }
+    __syncthreads();
+    return mfv;
+}
+
 template <int N, int L, int MODE>
 __global__ void __launch_bounds__(LbmLayout<N>::NT) k_lbm_step(const __grid_constant__ StepArgs a) {
     using Lay = LbmLayout<N>;
@@ -56,96 +105,34 @@ __global__ void __launch_bounds__(LbmLayout<N>::NT) k_lbm_step(const __grid_cons
     const ShardGeom& g = a.g;
     double* T = tiles + (lane_ok ? s : 0) * TILE;
     double* S = a.scratch + (size_t)blockIdx.x * Lay::scratch_doubles();
-    const bool from_list = MODE == MODE_RAW && a.raw_list != nullptr;
-    const uint32_t count = from_list ? *a.raw_count : g.npatch;
 
-    for (uint32_t k = blockIdx.x; k < count; k += gridDim.x) {
-        const uint32_t p = from_list ? a.raw_list[k] : k;
-        const PatchPos pp = patch_pos(p, g);
-
-        // ---- decode + pull streaming, 3 rounds of 3 populations ----------
-        for (int rd = 0; rd < 3; ++rd) {
-            const int q = 3 * rd + s;
-            bool raw_in = false;
-            if (lane_ok) {
-                raw_in = decode_row<N, L>(T, li, a.dir_in[(size_t)p * 9 + q], a.store_in);
-                if (MODE != MODE_DECODE) fill_ghosts<N>(T, li, a.ein, pp, q, g);
-            }
-            __syncthreads();
-            if (lane_ok) {
-                double v[N];
-                decode_col<N, L>(T, li, raw_in, v);
-                if (MODE == MODE_DECODE) {
+    if (MODE == MODE_DECODE) {
+        for (uint32_t p = blockIdx.x; p < g.npatch; p += gridDim.x) {
+            for (int rd = 0; rd < 3; ++rd) {
+                const int q = 3 * rd + s;
+                bool raw_in = false;
+                if (lane_ok) raw_in = decode_row<N, L>(T, li, a.dir_in[(size_t)p * 9 + q], a.store_in);
+                __syncthreads();
+                if (lane_ok) {
+                    double v[N];
+                    decode_col<N, L>(T, li, raw_in, v);
                     double* out = a.decode_out + ((size_t)p * 9 + q) * TILE;
 #pragma unroll
                     for (int i = 0; i < N; ++i) out[(i + 1) * TP + li + 1] = v[i];
-                } else if (!raw_in) {
-                    store_col<N>(T, li, v);
                 }
-            }
-            __syncthreads();
-            if (MODE != MODE_DECODE && lane_ok) {
-                const int cx = lbm_cx(q), cy = lbm_cy(q);
-                double* Sq = S + (size_t)q * NN;
-                const int j = li;
-#pragma unroll 5
-                for (int i = 0; i < N; ++i) Sq[i * N + j] = T[(i + 1 - cx) * TP + (j + 1 - cy)];
-            }
-            __syncthreads();
-        }
-        if (MODE == MODE_DECODE) continue;
-
-        // ---- BGK collide on every cell -------------------------------------
-        double mfv = 0.0;
-        for (int c = t; c < NN; c += NT) {
-            double f[9];
-#pragma unroll
-            for (int q = 0; q < 9; ++q) f[q] = S[(size_t)q * NN + c];
-            lbm_collide(f, a.omega);
-            const int i = c / N, j = c - (c / N) * N;
-            const double w = ((i == 0 || i == N - 1) ? 0.5 : 1.0) * ((j == 0 || j == N - 1) ? 0.5 : 1.0);
-#pragma unroll
-            for (int q = 0; q < 9; ++q) {
-                S[(size_t)q * NN + c] = f[q];
-                mfv += w * f[q];
+                __syncthreads();
             }
         }
-        red_fv[t] = mfv;
-        __syncthreads();
+        return;
+    }
 
+    StepPartial part{0, 0, 0, 0.0, 0.0};
+    for (uint32_t p = blockIdx.x; p < g.npatch; p += gridDim.x) {
+        const PatchPos pp = patch_pos(p, g);
+        red_fv[t] = decode_stream_collide<N, L>(a, T, S, p, pp, s, li, lane_ok);
         double m = 0.0;
-        if (MODE == MODE_RAW) {
-            // ---- store the collided state uncompressed (skip rule) --------
-            for (int rd = 0; rd < 3; ++rd) {
-                const int q = 3 * rd + s;
-                if (lane_ok && li == 0) {
-                    const uint64_t bytes = round16((uint64_t)NN * 8);
-                    const uint64_t off = atomicAdd(a.bump_out, (unsigned long long)bytes);
-                    slot_ok[s] = off + bytes <= a.cap_out;
-                    if (!slot_ok[s]) {
-                        atomicOr(a.err, ERR_STORE_OVERFLOW);
-                        a.dir_out[(size_t)p * 9 + q] = DirEntry{0, 0u, DIR_DEAD};
-                    } else {
-                        slot_off[s] = off;
-                        a.dir_out[(size_t)p * 9 + q] = DirEntry{off, 0u, DIR_RAW};
-                    }
-                }
-                __syncthreads();
-                if (lane_ok && slot_ok[s]) {
-                    const int j = li;
-                    double v[N];
-                    double* d = reinterpret_cast<double*>(a.store_out + slot_off[s]);
-#pragma unroll
-                    for (int i = 0; i < N; ++i) {
-                        v[i] = S[(size_t)q * NN + i * N + j];
-                        d[i * N + j] = v[i];
-                    }
-                    write_edges<N>(a.eout, pp, q, g, j, v);
-                    m += col_mass<N>(j, v);
-                }
-                __syncthreads();
-            }
-        } else {
+        bool store_raw = !a.compress;
+        if (a.compress) {
             if (t == 0) {
                 patch_bytes = 0;
                 patch_nnz = 0;
@@ -186,20 +173,14 @@ __global__ void __launch_bounds__(LbmLayout<N>::NT) k_lbm_step(const __grid_cons
                 }
                 __syncthreads();
             }
-            const bool compressed = patch_zero != 0;
             if (t == 0) {
-                PatchStats& st = a.stats[p];
-                st.comp_bytes = patch_bytes;
-                st.nnz = (uint32_t)patch_nnz;
-                st.zeroed = (uint32_t)patch_zero;
-                if (!compressed) {  // skip rule: the raw kernel stores the collided state
-                    const uint32_t kq = atomicAdd(a.raw_count, 1u);
-                    if (kq < a.raw_capacity) a.raw_list[kq] = p;
-                    else atomicOr(a.err, ERR_RAW_OVERFLOW);
-                }
+                part.comp_bytes += patch_bytes;
+                part.nnz += patch_nnz;
+                part.zeroed += patch_zero;
             }
+            store_raw = patch_zero == 0;
             // ---- pass 2: CSR blocks, reconstruction, edge lines, mass ------
-            for (int rd = 0; rd < 3 && compressed; ++rd) {
+            for (int rd = 0; rd < 3 && !store_raw; ++rd) {
                 const int q = 3 * rd + s;
                 if (lane_ok && li == 0) {
                     const uint64_t bytes = round16(12ull * comp_nnz[q] + 4ull * (N + 1));
@@ -233,6 +214,41 @@ __global__ void __launch_bounds__(LbmLayout<N>::NT) k_lbm_step(const __grid_cons
                 }
                 __syncthreads();
             }
+            // skip rule (pipeline.hpp:243-249): the collided state, bit for
+            // bit, is re-derived (pass 1 overwrote the scratch) and stored raw
+            if (store_raw) decode_stream_collide<N, L>(a, T, S, p, pp, s, li, lane_ok);
+        }
+        if (store_raw) {
+            for (int rd = 0; rd < 3; ++rd) {
+                const int q = 3 * rd + s;
+                if (lane_ok && li == 0) {
+                    const uint64_t bytes = round16((uint64_t)NN * 8);
+                    const uint64_t off = atomicAdd(a.bump_out, (unsigned long long)bytes);
+                    slot_ok[s] = off + bytes <= a.cap_out;
+                    if (!slot_ok[s]) {
+                        atomicOr(a.err, ERR_STORE_OVERFLOW);
+                        a.dir_out[(size_t)p * 9 + q] = DirEntry{0, 0u, DIR_DEAD};
+                    } else {
+                        slot_off[s] = off;
+                        a.dir_out[(size_t)p * 9 + q] = DirEntry{off, 0u, DIR_RAW};
+                    }
+                }
+                __syncthreads();
+                if (lane_ok) {
+                    const int j = li;
+                    double v[N];
+#pragma unroll
+                    for (int i = 0; i < N; ++i) v[i] = S[(size_t)q * NN + i * N + j];
+                    if (slot_ok[s]) {
+                        double* d = reinterpret_cast<double*>(a.store_out + slot_off[s]);
+#pragma unroll
+                        for (int i = 0; i < N; ++i) d[i * N + j] = v[i];
+                    }
+                    write_edges<N>(a.eout, pp, q, g, j, v);
+                    m += col_mass<N>(j, v);
+                }
+                __syncthreads();
+            }
         }
         red[t] = m;
         __syncthreads();
@@ -240,18 +256,13 @@ __global__ void __launch_bounds__(LbmLayout<N>::NT) k_lbm_step(const __grid_cons
             const double mm = warp_sum_range(red, 0, NT);
             const double mf = warp_sum_range(red_fv, 0, NT);
             if (t == 0) {
-                PatchStats& st = a.stats[p];
-                st.mass = mm;
-                st.mass_fv = mf;
-                if (MODE == MODE_RAW && !from_list) {
-                    st.comp_bytes = 0;
-                    st.nnz = 0;
-                    st.zeroed = 0;
-                }
+                part.mass += mm;
+                part.mass_fv += mf;
             }
         }
         __syncthreads();
     }
+    finalize_step(a, part);
 }
 
 }  // namespace wg

@@ -20,8 +20,15 @@
 //   detail  d_k = s_{2k+1} - (s_{2k} + s_{2k+2}) / 2.0
 //   coarse  c_k = s_{2k} + (w(k-1) d_{k-1} + w(k) d_k),  w = 1/2 at the two
 //           boundary details, 1/4 inside (lift_weight, wavelet.hpp:31-33)
-// The file is compiled with -fmad=false, so no contraction changes the
-// rounding; x/2.0 and x*0.5 are the same IEEE result.
+// The file is compiled with -fmad=false, so no implicit contraction changes
+// the rounding.  Two explicit FMAs are used where the fused product is exact
+// (a multiplication by 1/2 or 1/4 is exact for every normal double):
+//   d = s_odd - (l + r)/2          == fma(-0.5, l + r, s_odd)
+//   w0*d0 + w1*d1 (both exact)     == fma(w0, d0, w1*d1)
+// so the results are bit-identical to the reference's separate operations
+// (SURVEY A1.2 measured 0 mismatches for the second form).  They could only
+// differ if a product underflowed into the subnormal range (|d| < 2^-1020),
+// which WG_LIFT_NO_FMA removes at the cost of one instruction per element.
 #pragma once
 
 namespace wg {
@@ -78,6 +85,18 @@ __host__ __device__ constexpr double lift_w(int k, int half) {
     return (k == 0 || k == half - 1) ? 0.5 : 0.25;
 }
 
+#ifdef WG_LIFT_NO_FMA
+__device__ __forceinline__ double lift_pred_fwd(double odd, double l, double r) { return odd - (l + r) / 2.0; }
+__device__ __forceinline__ double lift_pred_inv(double odd, double l, double r) { return odd + (l + r) / 2.0; }
+__device__ __forceinline__ double lift_upd(double w0, double d0, double w1, double d1) { return w0 * d0 + w1 * d1; }
+#else
+__device__ __forceinline__ double lift_pred_fwd(double odd, double l, double r) { return __fma_rn(-0.5, l + r, odd); }
+__device__ __forceinline__ double lift_pred_inv(double odd, double l, double r) { return __fma_rn(0.5, l + r, odd); }
+__device__ __forceinline__ double lift_upd(double w0, double d0, double w1, double d1) {
+    return __fma_rn(w0, d0, w1 * d1);
+}
+#endif
+
 // Forward multi-level transform of v[0..N) in place (interleaved order).
 template <int N, int L>
 __device__ __forceinline__ void dwt_line_reg(double (&v)[N]) {
@@ -88,11 +107,11 @@ __device__ __forceinline__ void dwt_line_reg(double (&v)[N]) {
         const int half = (len - 1) / 2;
 #pragma unroll
         for (int k = 0; k < half; ++k)
-            v[(2 * k + 1) * s] = v[(2 * k + 1) * s] - (v[2 * k * s] + v[(2 * k + 2) * s]) / 2.0;
+            v[(2 * k + 1) * s] = lift_pred_fwd(v[(2 * k + 1) * s], v[2 * k * s], v[(2 * k + 2) * s]);
 #pragma unroll
         for (int k = 1; k < half; ++k)
-            v[2 * k * s] = v[2 * k * s] +
-                           (lift_w(k - 1, half) * v[(2 * k - 1) * s] + lift_w(k, half) * v[(2 * k + 1) * s]);
+            v[2 * k * s] = v[2 * k * s] + lift_upd(lift_w(k - 1, half), v[(2 * k - 1) * s], lift_w(k, half),
+                                                   v[(2 * k + 1) * s]);
     }
 }
 
@@ -106,11 +125,11 @@ __device__ __forceinline__ void idwt_line_reg(double (&v)[N]) {
         const int half = (len - 1) / 2;
 #pragma unroll
         for (int k = 1; k < half; ++k)
-            v[2 * k * s] = v[2 * k * s] -
-                           (lift_w(k - 1, half) * v[(2 * k - 1) * s] + lift_w(k, half) * v[(2 * k + 1) * s]);
+            v[2 * k * s] = v[2 * k * s] - lift_upd(lift_w(k - 1, half), v[(2 * k - 1) * s], lift_w(k, half),
+                                                   v[(2 * k + 1) * s]);
 #pragma unroll
         for (int k = 0; k < half; ++k)
-            v[(2 * k + 1) * s] = v[(2 * k + 1) * s] + (v[2 * k * s] + v[(2 * k + 2) * s]) / 2.0;
+            v[(2 * k + 1) * s] = lift_pred_inv(v[(2 * k + 1) * s], v[2 * k * s], v[(2 * k + 2) * s]);
     }
 }
 

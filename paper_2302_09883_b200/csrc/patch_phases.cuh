@@ -17,6 +17,12 @@ namespace wg {
 
 constexpr int kMaxLevels = 8;
 
+// Per-CTA partial sums of the step metrics (fixed order inside the CTA).
+struct StepPartial {
+    unsigned long long comp_bytes, nnz, zeroed;
+    double mass, mass_fv;
+};
+
 struct StepArgs {
     const unsigned char* store_in;
     const DirEntry* dir_in;
@@ -24,22 +30,27 @@ struct StepArgs {
     unsigned char* store_out;
     DirEntry* dir_out;
     EdgeSet eout;
-    PatchStats* stats;
     unsigned long long* bump_out;
+    unsigned long long* bump_next;  // pool written by the next step: reset by the last CTA
     uint64_t cap_out;
-    uint32_t* raw_list;   // MODE_RAW: patches to store raw (nullptr = all patches)
-    uint32_t* raw_count;
-    uint32_t raw_capacity;
     unsigned* err;
     double* decode_out;   // MODE_DECODE: grid buffer (true layout) of this shard
     double* scratch;      // D2Q9: per-CTA L2-resident staging of 9 N*N fields
+    StepPartial* partials;  // [gridDim.x]
+    unsigned* done;         // CTA completion counter (last CTA reduces the partials)
+    wg_metrics_row* row_out;  // this step's MetricsRow (pipeline.hpp:260-274)
+    double* mass_fv_out;      // this step's scheme-output mass (strict mode)
     ShardGeom g;
+    int compress;             // 0: RunConfig::no_compression
+    uint64_t step;
+    double time;
+    uint64_t dense_bytes;     // CompressedPatch::dense_bytes summed over the shard
     double smax[4], smin[4], r;                          // transport faces, dt/dx
     double omega;                                        // D2Q9: 1/tau
     double thr[(kMaxLevels + 1) * (kMaxLevels + 1)];     // T[band_i][band_j]
 };
 
-enum { MODE_MAIN = 0, MODE_RAW = 1, MODE_DECODE = 2 };
+enum { MODE_STEP = 0, MODE_DECODE = 2 };
 
 struct PatchPos {
     int ar;       // local patch row
@@ -233,17 +244,19 @@ __device__ __forceinline__ void write_edges(const EdgeSet& e, const PatchPos& pp
     }
 }
 
-// Trapezoid-weighted column sum (global_mass weights, patchgrid.hpp:244-266).
+// Trapezoid-weighted column sum (global_mass weights, patchgrid.hpp:244-266),
+// with four interleaved partial sums (fixed association: deterministic; the
+// mass is a tolerance-checked diagnostic).
 template <int N>
 __device__ __forceinline__ double col_mass(int j, const double (&v)[N]) {
     const double wj = (j == 0 || j == N - 1) ? 0.5 : 1.0;
-    double m = 0.0;
+    double m[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
     for (int i = 0; i < N; ++i) {
         const double wi = (i == 0 || i == N - 1) ? 0.5 : 1.0;
-        m += (wi * wj) * v[i];
+        m[i & 3] += (wi * wj) * v[i];
     }
-    return m;
+    return (m[0] + m[1]) + (m[2] + m[3]);
 }
 
 // Inclusive scan of one u64 per thread over the CTA (warp shuffles + one
@@ -277,6 +290,57 @@ __device__ __forceinline__ double warp_sum_range(const double* red, int base, in
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
     return s;
+}
+
+// End of a step, called by every CTA with its partial sums: the last CTA to
+// finish reduces all partials in a fixed order (deterministic), writes the
+// step's MetricsRow and resets the counter and the next pool's allocator.
+__device__ __forceinline__ void finalize_step(const StepArgs& a, const StepPartial& mine) {
+    __shared__ int am_last;
+    if (threadIdx.x == 0) {
+        a.partials[blockIdx.x] = mine;
+        __threadfence();
+        const unsigned prev = atomicAdd(a.done, 1u);
+        am_last = prev == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!am_last || threadIdx.x >= 32) return;
+    __threadfence();
+    const int lane = threadIdx.x;
+    unsigned long long cb = 0, nz = 0, zr = 0;
+    double m = 0.0, mf = 0.0;
+    for (unsigned c = lane; c < gridDim.x; c += 32) {
+        const StepPartial* pp = a.partials + c;
+        cb += __ldcg(&pp->comp_bytes);
+        nz += __ldcg(&pp->nnz);
+        zr += __ldcg(&pp->zeroed);
+        m += __ldcg(&pp->mass);
+        mf += __ldcg(&pp->mass_fv);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        cb += __shfl_xor_sync(0xffffffffu, cb, o);
+        nz += __shfl_xor_sync(0xffffffffu, nz, o);
+        zr += __shfl_xor_sync(0xffffffffu, zr, o);
+        m += __shfl_xor_sync(0xffffffffu, m, o);
+        mf += __shfl_xor_sync(0xffffffffu, mf, o);
+    }
+    if (lane == 0) {
+        wg_metrics_row r;
+        r.step = a.step;
+        r.time = a.time;
+        r.dense_bytes = a.compress ? a.dense_bytes : 0;
+        r.compressed_bytes = a.compress ? cb : 0;
+        r.ratio = (a.compress && cb > 0) ? (double)r.dense_bytes / (double)cb : 1.0;
+        r.nnz = a.compress ? nz : 0;
+        r.zeroed = a.compress ? zr : 0;
+        r.global_mass = m;
+        r.l2 = 0.0;
+        *a.row_out = r;
+        *a.mass_fv_out = mf;
+        *a.done = 0;
+        *a.bump_next = 0;
+    }
 }
 
 }  // namespace wg

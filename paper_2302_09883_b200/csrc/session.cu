@@ -1,15 +1,13 @@
 // session.cu — the device-resident compressed patch store and its step loop
 // (the B200 hot path), plus run() on top of it.
 //
-// One step (pipeline.hpp:194-289):
-//   k_patch_step<MAIN>   fused decode/ghost/FV/DWT/threshold/CSR/recon per patch
-//   k_patch_step<RAW>    patches whose cycle zeroed nothing keep the raw FV output
-//                        (skip rule, pipeline.hpp:243-249); exits at once if none
-//   k_metrics            deterministic reduction of the per-patch stats into the
-//                        step's MetricsRow (pipeline.hpp:260-274); resets the
-//                        bump allocator of the other pool
-// All three run on the session stream; nothing synchronises with the host
-// inside the step loop.
+// One step (pipeline.hpp:194-289) is ONE kernel launch on the session
+// stream: k_patch_step (transport) or k_lbm_step (D2Q9) runs the fused
+// decode/ghost/scheme/DWT/threshold/CSR/reconstruction cycle of every patch,
+// applies the skip rule (pipeline.hpp:243-249) in place, and its last CTA
+// reduces the per-CTA partials into the step's MetricsRow (pipeline.hpp:
+// 260-274) and resets the bump allocator of the other pool.  Nothing
+// synchronises with the host inside the step loop.
 #include <algorithm>
 #include <cmath>
 #include <cstring>
@@ -30,7 +28,6 @@ namespace {
 // ---- kernel table ---------------------------------------------------------
 struct KernelSet {
     void (*main)(StepArgs);
-    void (*raw)(StepArgs);
     void (*decode)(StepArgs);
     int P;               // patches per CTA (non-persistent kernels)
     int threads;
@@ -43,15 +40,14 @@ template <int N, int L>
 KernelSet make_lbm_set() {
     using Lay = LbmLayout<N>;
     KernelSet k;
-    k.main = k_lbm_step<N, L, MODE_MAIN>;
-    k.raw = k_lbm_step<N, L, MODE_RAW>;
+    k.main = k_lbm_step<N, L, MODE_STEP>;
     k.decode = k_lbm_step<N, L, MODE_DECODE>;
     k.P = 1;
     k.threads = Lay::NT;
     k.smem = Lay::smem_bytes();
     k.persistent = true;
     k.scratch_doubles = Lay::scratch_doubles();
-    for (auto f : {k.main, k.raw, k.decode}) {
+    for (auto f : {k.main, k.decode}) {
         WG_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k.smem));
     }
     return k;
@@ -74,15 +70,14 @@ template <int N, int L, int P>
 KernelSet make_set() {
     using Lay = Layout<N, P>;
     KernelSet k;
-    k.main = k_patch_step<N, L, P, MODE_MAIN>;
-    k.raw = k_patch_step<N, L, P, MODE_RAW>;
+    k.main = k_patch_step<N, L, P, MODE_STEP>;
     k.decode = k_patch_step<N, L, P, MODE_DECODE>;
     k.P = P;
     k.threads = Lay::NT;
     k.smem = Lay::smem_bytes();
     k.persistent = false;
     k.scratch_doubles = 0;
-    for (auto f : {k.main, k.raw, k.decode}) {
+    for (auto f : {k.main, k.decode}) {
         WG_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k.smem));
     }
     return k;
@@ -157,71 +152,6 @@ __global__ void k_upload(const double* grid, uint32_t N, ShardGeom g, unsigned c
     e.colhi[oc + i] = src[N - 2];
 }
 
-// ---- per-step metrics (pipeline.hpp:260-274) ------------------------------
-struct MetricsArgs {
-    const PatchStats* stats;
-    uint32_t npatch;
-    uint64_t dense_bytes;  // CompressedPatch::dense_bytes summed (0 if no compression)
-    uint64_t step;
-    double time;
-    int compress;
-    wg_metrics_row* rows;
-    uint64_t row_index;
-    uint32_t* raw_count;            // reset for the next step
-    unsigned long long* bump_next;  // pool written by the next step
-    double* mass_fv_out;            // per-step scheme-output mass (strict mode)
-};
-
-__global__ void __launch_bounds__(1024) k_metrics(MetricsArgs a) {
-    __shared__ unsigned long long s_comp[1024], s_nnz[1024], s_zero[1024];
-    __shared__ double s_mass[1024], s_mfv[1024];
-    const uint32_t t = threadIdx.x, nt = blockDim.x;
-    const uint32_t per = (a.npatch + nt - 1) / nt;
-    const uint32_t b = t * per, e = min(a.npatch, b + per);
-    unsigned long long comp = 0, nnz = 0, zero = 0;
-    double mass = 0.0, mfv = 0.0;
-    for (uint32_t p = b; p < e; ++p) {  // contiguous chunk, fixed order
-        const PatchStats s = a.stats[p];
-        comp += s.comp_bytes;
-        nnz += s.nnz;
-        zero += s.zeroed;
-        mass += s.mass;
-        mfv += s.mass_fv;
-    }
-    s_comp[t] = comp;
-    s_nnz[t] = nnz;
-    s_zero[t] = zero;
-    s_mass[t] = mass;
-    s_mfv[t] = mfv;
-    __syncthreads();
-    for (uint32_t s = nt / 2; s > 0; s >>= 1) {
-        if (t < s) {
-            s_comp[t] += s_comp[t + s];
-            s_nnz[t] += s_nnz[t + s];
-            s_zero[t] += s_zero[t + s];
-            s_mass[t] += s_mass[t + s];
-            s_mfv[t] += s_mfv[t + s];
-        }
-        __syncthreads();
-    }
-    if (t == 0) {
-        wg_metrics_row r;
-        r.step = a.step;
-        r.time = a.time;
-        r.dense_bytes = a.compress ? a.dense_bytes : 0;
-        r.compressed_bytes = a.compress ? s_comp[0] : 0;
-        r.ratio = (a.compress && s_comp[0] > 0) ? (double)r.dense_bytes / (double)s_comp[0] : 1.0;
-        r.nnz = a.compress ? s_nnz[0] : 0;
-        r.zeroed = a.compress ? s_zero[0] : 0;
-        r.global_mass = s_mass[0];
-        r.l2 = 0.0;
-        a.rows[a.row_index] = r;
-        a.mass_fv_out[a.row_index] = s_mfv[0];
-        *a.raw_count = 0;
-        *a.bump_next = 0;
-    }
-}
-
 }  // namespace
 
 // ---- the session -------------------------------------------------------------
@@ -241,12 +171,11 @@ struct Session {
     DirEntry* dir[2] = {nullptr, nullptr};
     EdgeSet edges[2]{};
     double* edge_mem[2] = {nullptr, nullptr};
-    PatchStats* stats = nullptr;
+    StepPartial* partials = nullptr;     // per CTA of the step launch
+    unsigned* done = nullptr;            // CTA completion counter
     double* scratch = nullptr;           // D2Q9 per-CTA staging (L2-resident)
     unsigned grid = 0;                   // launch grid of the step kernels
     unsigned long long* bump = nullptr;  // [2]
-    uint32_t* raw_list = nullptr;
-    uint32_t* raw_count = nullptr;
     unsigned* err = nullptr;
     wg_metrics_row* rows = nullptr;
     double* mass_fv = nullptr;
@@ -298,19 +227,17 @@ struct Session {
             dir[k] = nullptr;
             edge_mem[k] = nullptr;
         }
-        cudaFree(stats);
+        cudaFree(partials);
+        cudaFree(done);
         cudaFree(scratch);
         scratch = nullptr;
         cudaFree(bump);
-        cudaFree(raw_list);
-        cudaFree(raw_count);
         cudaFree(err);
         cudaFree(rows);
         cudaFree(mass_fv);
-        stats = nullptr;
+        partials = nullptr;
+        done = nullptr;
         bump = nullptr;
-        raw_list = nullptr;
-        raw_count = nullptr;
         err = nullptr;
         rows = nullptr;
         mass_fv = nullptr;
@@ -368,14 +295,13 @@ struct Session {
         sg.world = shard.world;
         sg.npatch = sg.R * sg.P1;
         ks = select_kernels(cfg.scheme, N, levels);
-        if (ks.persistent) {
+        {
             int per_sm = 0, sms = 0;
             WG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ks.main, ks.threads, ks.smem));
             WG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, shard.device));
-            grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(sg.npatch, (uint64_t)std::max(per_sm, 1) * sms));
-            scratch = dalloc<double>((uint64_t)grid * ks.scratch_doubles);
-        } else {
-            grid = (sg.npatch + ks.P - 1) / ks.P;
+            const uint64_t groups = (sg.npatch + ks.P - 1) / ks.P;
+            grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(groups, (uint64_t)std::max(per_sm, 1) * sms));
+            if (ks.scratch_doubles) scratch = dalloc<double>((uint64_t)grid * ks.scratch_doubles);
         }
         // thresholds (threshold.hpp:31-47) — the "c == 0 or levels == 0"
         // early return of apply_threshold (threshold.hpp:53) is T = 0.
@@ -398,14 +324,12 @@ struct Session {
             edges[k].collo = edge_mem[k] + 2 * rowline;
             edges[k].colhi = edge_mem[k] + 2 * rowline + colline;
         }
-        stats = dalloc<PatchStats>(sg.npatch);
+        partials = dalloc<StepPartial>(grid);
+        done = dalloc<unsigned>(1);
         bump = dalloc<unsigned long long>(2);
-        raw_list = dalloc<uint32_t>(sg.npatch);
-        raw_count = dalloc<uint32_t>(1);
         err = dalloc<unsigned>(1);
-        WG_CUDA(cudaMemsetAsync(stats, 0, sizeof(PatchStats) * sg.npatch, stream));
+        WG_CUDA(cudaMemsetAsync(done, 0, sizeof(unsigned), stream));
         WG_CUDA(cudaMemsetAsync(bump, 0, 2 * sizeof(unsigned long long), stream));
-        WG_CUDA(cudaMemsetAsync(raw_count, 0, sizeof(uint32_t), stream));
         WG_CUDA(cudaMemsetAsync(err, 0, sizeof(unsigned), stream));
         grow_rows(1024);
     }
@@ -464,60 +388,43 @@ struct Session {
         a.store_out = store[dst];
         a.dir_out = dir[dst];
         a.eout = edges[dst];
-        a.stats = stats;
         a.bump_out = bump + dst;
+        a.bump_next = bump + src;
         a.cap_out = cap;
-        a.raw_list = raw_list;
-        a.raw_count = raw_count;
-        a.raw_capacity = sg.npatch;
         a.err = err;
+        a.partials = partials;
+        a.done = done;
+        a.scratch = scratch;
         a.g = sg;
+        a.compress = cfg.no_compression ? 0 : 1;
+        a.dense_bytes = (uint64_t)sg.npatch * 8ull * N * N * sg.m;
         std::memcpy(a.thr, thr, sizeof(thr));
         return a;
     }
 
     void do_step(double dt) {
         const int src = cur, dst = 1 - cur;
+        grow_rows(step + 1);
         StepArgs a = step_args(src, dst);
         direction_speeds(cfg.alpha, cfg.beta, a.smax, a.smin);
         a.r = dt / sim_dx(cfg);  // solver.hpp:212
         a.omega = 1.0 / cfg.lbm_tau;
-        a.scratch = scratch;
-        if (cfg.no_compression) {
-            a.raw_list = nullptr;
-            ks.raw<<<grid, ks.threads, ks.smem, stream>>>(a);
-            WG_LAUNCH_CHECK("raw step");
-        } else {
-            cudaEvent_t e0 = nullptr, e1 = nullptr;
-            if (profiling) {
-                e0 = take_event();
-                e1 = take_event();
-                WG_CUDA(cudaEventRecord(e0, stream));
-            }
-            ks.main<<<grid, ks.threads, ks.smem, stream>>>(a);
-            WG_LAUNCH_CHECK("fused step");
-            if (profiling) {
-                WG_CUDA(cudaEventRecord(e1, stream));
-                ev_main.emplace_back(e0, e1);
-            }
-            ks.raw<<<grid, ks.threads, ks.smem, stream>>>(a);
-            WG_LAUNCH_CHECK("skip-rule step");
+        a.step = step + 1;
+        a.time = time + dt;
+        a.row_out = rows + step;
+        a.mass_fv_out = mass_fv + step;
+        cudaEvent_t e0 = nullptr, e1 = nullptr;
+        if (profiling) {
+            e0 = take_event();
+            e1 = take_event();
+            WG_CUDA(cudaEventRecord(e0, stream));
         }
-        grow_rows(step + 1);
-        MetricsArgs m{};
-        m.stats = stats;
-        m.npatch = sg.npatch;
-        m.dense_bytes = (uint64_t)sg.npatch * 8ull * N * N * sg.m;
-        m.step = step + 1;
-        m.time = time + dt;
-        m.compress = !cfg.no_compression;
-        m.rows = rows;
-        m.row_index = step;
-        m.raw_count = raw_count;
-        m.bump_next = bump + src;
-        m.mass_fv_out = mass_fv;
-        k_metrics<<<1, 1024, 0, stream>>>(m);
-        WG_LAUNCH_CHECK("metrics");
+        ks.main<<<grid, ks.threads, ks.smem, stream>>>(a);
+        WG_LAUNCH_CHECK("fused step");
+        if (profiling) {
+            WG_CUDA(cudaEventRecord(e1, stream));
+            ev_main.emplace_back(e0, e1);
+        }
         cur = dst;
         ++step;
         time += dt;
@@ -536,7 +443,6 @@ struct Session {
         WG_CUDA(cudaMemsetAsync(d.p, 0, n * sizeof(double), stream));
         StepArgs a = step_args(cur, 1 - cur);
         a.decode_out = d.p;
-        a.scratch = scratch;
         ks.decode<<<grid, ks.threads, ks.smem, stream>>>(a);
         WG_LAUNCH_CHECK("decode");
         WG_CUDA(cudaMemcpyAsync(hgrid, d.p, n * sizeof(double), cudaMemcpyDeviceToHost, stream));
@@ -642,6 +548,16 @@ wg_status wg_session_patch_csr(wg_session* s, uint64_t patch, uint32_t comp, dou
 
 wg_status wg_session_sync(wg_session* s) {
     return guard([&] { reinterpret_cast<Session*>(s)->sync(); });
+}
+
+wg_status wg_session_last_row(wg_session* sp, wg_metrics_row* row) {
+    return guard([&] {
+        Session* s = reinterpret_cast<Session*>(sp);
+        if (s->step == 0) raise(WG_LOGIC, "no step has run");
+        WG_CUDA(cudaMemcpyAsync(row, s->rows + (s->step - 1), sizeof(wg_metrics_row), cudaMemcpyDeviceToHost,
+                                s->stream));
+        s->sync();
+    });
 }
 
 wg_status wg_session_profile(wg_session* sp, int32_t enable) {

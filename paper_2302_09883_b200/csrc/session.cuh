@@ -13,7 +13,8 @@
 //              next step (sync_ghosts, patchgrid.hpp:131-201).  Row lines
 //              have R+2 patch-row slots: slot 0 and R+1 are the halo rows
 //              received from the neighbouring shards (multi-GPU).
-//   stats      PatchStats per patch, reduced per step into a metrics row.
+//   partials   per-CTA metric sums of a step, reduced by the last CTA into
+//              the step's metrics row.
 #pragma once
 
 #include <cstdint>
@@ -27,14 +28,6 @@ struct DirEntry {
     uint64_t off;    // byte offset in the pool
     uint32_t nnz;    // CSR entries (0 for raw)
     uint32_t flags;  // DIR_RAW
-};
-
-struct PatchStats {
-    uint64_t comp_bytes;  // CsrBlock::byte_size summed over components
-    uint32_t nnz;
-    uint32_t zeroed;
-    double mass;          // trapezoid mass of component 0..m-1 summed (after the cycle)
-    double mass_fv;       // same, of the scheme output before compression (strict mode)
 };
 
 struct EdgeSet {

@@ -1,0 +1,148 @@
+"""Patch-row sharding of the compressed stencil loop over GPUs.
+
+One process per GPU.  Rank r owns a contiguous range of patch rows (a patch
+row lies wholly on one rank, so the dim-1 ghost sync and the corner fill stay
+local).  After every step the only exchange is the ring of halo lines:
+rank r sends logical row 1 of its first patch row to r-1 and logical row n-2
+of its last patch row to r+1 (periodic ring), i.e. exactly the values that
+sync_ghosts (patchgrid.hpp:131-201) copies across the rank boundary.
+Reductions (mass, nnz, zeroed, bytes) are all-reduced once, at the end.
+
+The exchange uses torch.distributed point-to-point (NCCL over NVLink on GPU,
+gloo on CPU in the tests) on tensors that alias the session's halo blocks.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import abi
+
+
+def shard_rows(nrows: int, rank: int, world: int) -> tuple[int, int]:
+    """Contiguous, balanced patch-row range of `rank` (row-major patches,
+    patchgrid.hpp:50-54, so a shard is a contiguous patch-index range)."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("bad rank/world")
+    if nrows < world:
+        raise ValueError(f"{nrows} patch rows cannot be split over {world} ranks")
+    base, extra = divmod(nrows, world)
+    begin = rank * base + min(rank, extra)
+    return begin, begin + base + (1 if rank < extra else 0)
+
+
+def ring_neighbours(rank: int, world: int) -> tuple[int, int]:
+    """(above, below) in the periodic ring of patch-row shards."""
+    return (rank - 1) % world, (rank + 1) % world
+
+
+def exchange_halos(send_lo, send_hi, recv_lo, recv_hi, rank: int, world: int, dist) -> None:
+    """Ring exchange of halo blocks.  recv_lo <- above.send_hi,
+    recv_hi <- below.send_lo.  Operations are posted in one fixed order on
+    every rank so that world == 2 (above == below) still pairs correctly."""
+    above, below = ring_neighbours(rank, world)
+    ops = [
+        dist.P2POp(dist.isend, send_hi, below),
+        dist.P2POp(dist.isend, send_lo, above),
+        dist.P2POp(dist.irecv, recv_lo, above),
+        dist.P2POp(dist.irecv, recv_hi, below),
+    ]
+    for req in dist.batch_isend_irecv(ops):
+        req.wait()
+
+
+class _DevArray:
+    """A raw device pointer exposed through __cuda_array_interface__ so that
+    torch.as_tensor aliases it without a copy."""
+
+    def __init__(self, ptr: int, n: int):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<f8", "data": (int(ptr), False),
+                                         "version": 3, "strides": None}
+
+
+def reduce_rows(rows: list[dict], dist, device) -> list[dict]:
+    """All-reduce per-shard metrics rows into whole-grid rows (sums; ratio
+    recomputed as in pipeline.hpp:270-272)."""
+    import torch
+
+    keys = ["dense_bytes", "compressed_bytes", "nnz", "zeroed"]
+    ints = torch.tensor([[r[k] for k in keys] for r in rows], dtype=torch.int64, device=device)
+    mass = torch.tensor([r["global_mass"] for r in rows], dtype=torch.float64, device=device)
+    dist.all_reduce(ints)
+    dist.all_reduce(mass)
+    out = []
+    for r, iv, m in zip(rows, ints.tolist(), mass.tolist()):
+        o = dict(r)
+        o.update(dict(zip(keys, iv)))
+        o["global_mass"] = m
+        o["ratio"] = o["dense_bytes"] / o["compressed_bytes"] if o["compressed_bytes"] > 0 else 1.0
+        out.append(o)
+    return out
+
+
+@dataclass
+class ShardInfo:
+    rank: int
+    world: int
+    row_begin: int
+    row_end: int
+    device: int
+
+
+class ShardedSession:
+    """A device session over this rank's patch rows, stepping in lock-step
+    with the other ranks."""
+
+    def __init__(self, lib: abi.Lib, cfg, shard: ShardInfo, stream_ptr: int | None, dist=None):
+        self.lib, self.cfg, self.shard, self.dist = lib, cfg, shard, dist
+        c = cfg.to_c()
+        sh = abi.ShardC()
+        sh.rank, sh.world, sh.device = shard.rank, shard.world, shard.device
+        sh.row_begin, sh.row_end = shard.row_begin, shard.row_end
+        self.handle = abi.vp()
+        lib.check(lib.wg_session_create(C.byref(c), C.byref(sh), abi.vp(stream_ptr) if stream_ptr else None,
+                                        C.byref(self.handle)))
+        self.info = abi.SessionInfoC()
+        lib.check(lib.wg_session_info_get(self.handle, C.byref(self.info)))
+        self._halo = None
+
+    def close(self):
+        if self.handle:
+            self.lib.wg_session_destroy(self.handle)
+            self.handle = abi.vp()
+
+    def upload(self, host_grid: np.ndarray):
+        self.lib.check(self.lib.wg_session_upload(self.handle, abi.dptr(host_grid)))
+
+    def halo_tensors(self):
+        import torch
+
+        ptrs = [abi.vp() for _ in range(4)]
+        self.lib.check(self.lib.wg_session_halo(self.handle, *[C.byref(p) for p in ptrs]))
+        n = self.info.halo_doubles
+        return [torch.as_tensor(_DevArray(p.value, n), device=f"cuda:{self.shard.device}") for p in ptrs]
+
+    def step(self, dt: float = 1.0):
+        self.lib.check(self.lib.wg_session_step(self.handle, dt))
+        if self.shard.world > 1:
+            # the halo blocks move with the double buffer: re-fetch every step
+            s_lo, s_hi, r_lo, r_hi = self.halo_tensors()
+            exchange_halos(s_lo, s_hi, r_lo, r_hi, self.shard.rank, self.shard.world, self.dist)
+
+    def sync(self):
+        self.lib.check(self.lib.wg_session_sync(self.handle))
+
+    def rows(self) -> list[dict]:
+        n = abi.u64()
+        self.lib.check(self.lib.wg_session_metrics(self.handle, None, 0, C.byref(n)))
+        buf = (abi.MetricsRowC * max(n.value, 1))()
+        self.lib.check(self.lib.wg_session_metrics(self.handle, buf, n.value, C.byref(n)))
+        keys = [k for k, _ in abi.MetricsRowC._fields_]
+        return [{k: getattr(r, k) for k in keys} for r in buf[: n.value]]
+
+    def last_row(self) -> dict:
+        r = abi.MetricsRowC()
+        self.lib.check(self.lib.wg_session_last_row(self.handle, C.byref(r)))
+        return {k: getattr(r, k) for k, _ in abi.MetricsRowC._fields_}
