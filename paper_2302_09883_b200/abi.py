@@ -262,7 +262,11 @@ class Lib:
 
 
 def load_product() -> Lib:
-    """Load the sm_100a product library; there is no CPU fallback."""
+    """Load the sm_100a product library; there is no CPU fallback.
+    (WG_PRODUCT_LIB may point at an in-tree build variant for tuning runs.)"""
+    alt = os.environ.get("WG_PRODUCT_LIB")
+    if alt:
+        return Lib(alt)
     if not PRODUCT_LIB.exists():
         raise ImportError(
             f"{PRODUCT_LIB} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`"

@@ -39,12 +39,12 @@ def _sources():
     return sorted(CSRC.glob("*.cu"))
 
 
-def _compile(src: Path, verbose_ptxas: bool) -> Path:
-    obj = BUILD / (src.stem + ".o")
+def _compile(src: Path, verbose_ptxas: bool, defines=(), tag: str = "") -> Path:
+    obj = BUILD / (src.stem + tag + ".o")
     deps = [src] + list(CSRC.glob("*.cuh")) + list(CSRC.glob("*.h")) + [REPO / "include" / "wavegrid_b200.h"]
     if obj.exists() and all(obj.stat().st_mtime >= d.stat().st_mtime for d in deps):
         return obj
-    cmd = [NVCC, *NVFLAGS, "-c", str(src), "-o", str(obj)]
+    cmd = [NVCC, *NVFLAGS, *[f"-D{d}" for d in defines], "-c", str(src), "-o", str(obj)]
     if verbose_ptxas:
         cmd[1:1] = ["-Xptxas", "-v"]
     res = subprocess.run(cmd, capture_output=True, text=True)
@@ -55,20 +55,23 @@ def _compile(src: Path, verbose_ptxas: bool) -> Path:
     return obj
 
 
-def build_product(verbose_ptxas: bool = False, jobs: int | None = None) -> Path:
+def build_product(verbose_ptxas: bool = False, jobs: int | None = None, defines=(), variant: str = "") -> Path:
+    """variant/defines build a tuning variant libwavegrid_b200_<variant>.so."""
     BUILD.mkdir(parents=True, exist_ok=True)
     srcs = _sources()
+    tag = f"_{variant}" if variant else ""
+    lib = PKG / f"libwavegrid_b200{tag}.so"
     with cf.ThreadPoolExecutor(max_workers=jobs or min(8, os.cpu_count() or 4)) as ex:
-        objs = list(ex.map(lambda s: _compile(s, verbose_ptxas), srcs))
-    if LIB.exists() and all(LIB.stat().st_mtime >= o.stat().st_mtime for o in objs):
-        return LIB
-    tmp = LIB.with_suffix(".so.tmp")
+        objs = list(ex.map(lambda s: _compile(s, verbose_ptxas, defines, tag), srcs))
+    if lib.exists() and all(lib.stat().st_mtime >= o.stat().st_mtime for o in objs):
+        return lib
+    tmp = lib.with_suffix(".so.tmp")
     cmd = [NVCC, *ARCH, "-shared", "-o", str(tmp), *map(str, objs), "-lcudart"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError(f"link failed:\n{res.stdout}\n{res.stderr}")
-    tmp.replace(LIB)
-    return LIB
+    tmp.replace(lib)
+    return lib
 
 
 def build_oracles(reference: bool = True) -> None:
@@ -81,5 +84,8 @@ def build_oracles(reference: bool = True) -> None:
 
 if __name__ == "__main__":
     v = "-v" in sys.argv
-    print(build_product(verbose_ptxas=v))
-    build_oracles()
+    defs = [a[2:] for a in sys.argv[1:] if a.startswith("-D")]
+    var = next((a.split("=", 1)[1] for a in sys.argv[1:] if a.startswith("--variant=")), "")
+    print(build_product(verbose_ptxas=v, defines=defs, variant=var))
+    if not var:
+        build_oracles()

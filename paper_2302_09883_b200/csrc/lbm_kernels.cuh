@@ -56,6 +56,7 @@ __device__ __forceinline__ double decode_stream_collide(const StepArgs& a, doubl
             store_col<N>(T, li, v);
         }
         __syncthreads();
+        WG_PHASE_MARK(rd == 0 ? 0 : 12);
         if (lane_ok) {  // pull streaming f_q(x) <- f_q(x - c_q), ghost ring included
             const int cx = lbm_cx(q), cy = lbm_cy(q);
             double* Sq = S + (size_t)q * NN;
@@ -64,22 +65,36 @@ __device__ __forceinline__ double decode_stream_collide(const StepArgs& a, doubl
             for (int i = 0; i < N; ++i) Sq[i * N + j] = T[(i + 1 - cx) * TP + (j + 1 - cy)];
         }
         __syncthreads();
+        WG_PHASE_MARK(1);
     }
     double mfv = 0.0;
-    for (int c = threadIdx.x; c < NN; c += NT) {
-        double f[9];
-#pragma unroll
-        for (int q = 0; q < 9; ++q) f[q] = S[(size_t)q * NN + c];
-        lbm_collide(f, a.omega);
-        const int i = c / N, j = c - (c / N) * N;
-        const double w = ((i == 0 || i == N - 1) ? 0.5 : 1.0) * ((j == 0 || j == N - 1) ? 0.5 : 1.0);
+    // two cells per iteration: 18 independent scratch loads in flight
+    for (int c0 = threadIdx.x; c0 < NN; c0 += 2 * NT) {
+        const int c1 = c0 + NT;
+        const bool two = c1 < NN;
+        double f0[9], f1[9];
 #pragma unroll
         for (int q = 0; q < 9; ++q) {
-            S[(size_t)q * NN + c] = f[q];
-            mfv += w * f[q];
+            f0[q] = S[(size_t)q * NN + c0];
+            f1[q] = two ? S[(size_t)q * NN + c1] : 1.0;
+        }
+        lbm_collide(f0, a.omega);
+        lbm_collide(f1, a.omega);
+        const int i0 = c0 / N, j0 = c0 - i0 * N, i1 = c1 / N, j1 = c1 - i1 * N;
+        const double w0 = ((i0 == 0 || i0 == N - 1) ? 0.5 : 1.0) * ((j0 == 0 || j0 == N - 1) ? 0.5 : 1.0);
+        const double w1 = ((i1 == 0 || i1 == N - 1) ? 0.5 : 1.0) * ((j1 == 0 || j1 == N - 1) ? 0.5 : 1.0);
+#pragma unroll
+        for (int q = 0; q < 9; ++q) {
+            S[(size_t)q * NN + c0] = f0[q];
+            mfv += w0 * f0[q];
+            if (two) {
+                S[(size_t)q * NN + c1] = f1[q];
+                mfv += w1 * f1[q];
+            }
         }
     }
     __syncthreads();
+    WG_PHASE_MARK(2);
     return mfv;
 }
 
@@ -94,6 +109,8 @@ __global__ void __launch_bounds__(LbmLayout<N>::NT) k_lbm_step(const __grid_cons
     unsigned long long* inc = reinterpret_cast<unsigned long long*>(red_fv + NT);
     __shared__ uint64_t slot_off[3];
     __shared__ int slot_ok[3];
+    __shared__ ChunkState cs;
+    __shared__ DirEntry next_dir[9];
     __shared__ unsigned long long patch_bytes, patch_nnz, patch_zero;
     __shared__ uint32_t comp_nnz[9];
     __shared__ uint32_t row_k[3 * NT];  // CSR entry offset of each row, per round
@@ -127,9 +144,15 @@ __global__ void __launch_bounds__(LbmLayout<N>::NT) k_lbm_step(const __grid_cons
     }
 
     StepPartial part{0, 0, 0, 0.0, 0.0};
+    WG_PHASE_MARK(-1);
+    if (t == 0) cs.cur = cs.end = 0;
     for (uint32_t p = blockIdx.x; p < g.npatch; p += gridDim.x) {
         const PatchPos pp = patch_pos(p, g);
+        const uint32_t pn = p + gridDim.x;  // this CTA's next patch
+        if (t < 9) next_dir[t] = pn < g.npatch ? a.dir_in[(size_t)pn * 9 + t] : DirEntry{0, 0u, DIR_DEAD};
         red_fv[t] = decode_stream_collide<N, L>(a, T, S, p, pp, s, li, lane_ok);
+        if (pn < g.npatch && lane_ok)  // warm L2 with the next patch's blocks and ghost sources
+            for (int q = s; q < 9; q += 3) prefetch_patch<N>(a, pn, next_dir[q], q, li, N);
         double m = 0.0;
         bool store_raw = !a.compress;
         if (a.compress) {
@@ -153,6 +176,7 @@ __global__ void __launch_bounds__(LbmLayout<N>::NT) k_lbm_step(const __grid_cons
                     fwd_col_to_tile<N, L>(T, j, v);
                 }
                 __syncthreads();
+                WG_PHASE_MARK(3);
                 unsigned nz = 0, zr = 0;
                 if (lane_ok) {
                     fwd_row_threshold<N, L>(T, li, a.thr, v, nz, zr);
@@ -172,6 +196,7 @@ __global__ void __launch_bounds__(LbmLayout<N>::NT) k_lbm_step(const __grid_cons
                     }
                 }
                 __syncthreads();
+                WG_PHASE_MARK(4);
             }
             if (t == 0) {
                 part.comp_bytes += patch_bytes;
@@ -182,19 +207,18 @@ __global__ void __launch_bounds__(LbmLayout<N>::NT) k_lbm_step(const __grid_cons
             // ---- pass 2: CSR blocks, reconstruction, edge lines, mass ------
             for (int rd = 0; rd < 3 && !store_raw; ++rd) {
                 const int q = 3 * rd + s;
-                if (lane_ok && li == 0) {
-                    const uint64_t bytes = round16(12ull * comp_nnz[q] + 4ull * (N + 1));
-                    const uint64_t off = atomicAdd(a.bump_out, (unsigned long long)bytes);
-                    slot_ok[s] = off + bytes <= a.cap_out;
-                    if (!slot_ok[s]) {
-                        atomicOr(a.err, ERR_STORE_OVERFLOW);
-                        a.dir_out[(size_t)p * 9 + q] = DirEntry{0, 0u, DIR_DEAD};
-                    } else {
-                        slot_off[s] = off;
-                        a.dir_out[(size_t)p * 9 + q] = DirEntry{off, comp_nnz[q], 0u};
+                if (t == 0) {
+                    for (int sl = 0; sl < 3; ++sl) {
+                        const int qq = 3 * rd + sl;
+                        const uint64_t off = chunk_alloc(a, cs, round16(12ull * comp_nnz[qq] + 4ull * (N + 1)));
+                        slot_ok[sl] = off != ~0ull;
+                        slot_off[sl] = off;
+                        a.dir_out[(size_t)p * 9 + qq] =
+                            slot_ok[sl] ? DirEntry{off, comp_nnz[qq], 0u} : DirEntry{0, 0u, DIR_DEAD};
                     }
                 }
                 __syncthreads();
+                WG_PHASE_MARK(5);
                 const bool ok = lane_ok && slot_ok[s];
                 double v[N];
                 if (ok) {
@@ -207,12 +231,14 @@ __global__ void __launch_bounds__(LbmLayout<N>::NT) k_lbm_step(const __grid_cons
                     inv_row_to_tile<N, L>(T, li, v);
                 }
                 __syncthreads();
+                WG_PHASE_MARK(6);
                 if (ok) {
                     decode_col<N, L>(T, li, false, v);
                     write_edges<N>(a.eout, pp, q, g, li, v);
                     m += col_mass<N>(li, v);
                 }
                 __syncthreads();
+                WG_PHASE_MARK(7);
             }
             // skip rule (pipeline.hpp:243-249): the collided state, bit for
             // bit, is re-derived (pass 1 overwrote the scratch) and stored raw
@@ -221,16 +247,13 @@ __global__ void __launch_bounds__(LbmLayout<N>::NT) k_lbm_step(const __grid_cons
         if (store_raw) {
             for (int rd = 0; rd < 3; ++rd) {
                 const int q = 3 * rd + s;
-                if (lane_ok && li == 0) {
-                    const uint64_t bytes = round16((uint64_t)NN * 8);
-                    const uint64_t off = atomicAdd(a.bump_out, (unsigned long long)bytes);
-                    slot_ok[s] = off + bytes <= a.cap_out;
-                    if (!slot_ok[s]) {
-                        atomicOr(a.err, ERR_STORE_OVERFLOW);
-                        a.dir_out[(size_t)p * 9 + q] = DirEntry{0, 0u, DIR_DEAD};
-                    } else {
-                        slot_off[s] = off;
-                        a.dir_out[(size_t)p * 9 + q] = DirEntry{off, 0u, DIR_RAW};
+                if (t == 0) {
+                    for (int sl = 0; sl < 3; ++sl) {
+                        const int qq = 3 * rd + sl;
+                        const uint64_t off = chunk_alloc(a, cs, round16((uint64_t)NN * 8));
+                        slot_ok[sl] = off != ~0ull;
+                        slot_off[sl] = off;
+                        a.dir_out[(size_t)p * 9 + qq] = slot_ok[sl] ? DirEntry{off, 0u, DIR_RAW} : DirEntry{0, 0u, DIR_DEAD};
                     }
                 }
                 __syncthreads();
@@ -261,8 +284,10 @@ __global__ void __launch_bounds__(LbmLayout<N>::NT) k_lbm_step(const __grid_cons
             }
         }
         __syncthreads();
+        WG_PHASE_MARK(9);
     }
     finalize_step(a, part);
+    WG_PHASE_MARK(11);
 }
 
 }  // namespace wg

@@ -36,21 +36,23 @@ struct Layout {
 // decode (rows + columns), ghost ring, upwind FV: returns the FV output
 // column j in v (natural order) for an active slot.  Contains 2 barriers.
 template <int N, int L>
-__device__ __forceinline__ void decode_and_fv(const StepArgs& a, double* T, bool active, uint32_t p,
+__device__ __forceinline__ void decode_and_fv(const StepArgs& a, double* T, bool active, const DirEntry e,
                                               const PatchPos& pp, int li, double (&v)[N]) {
     constexpr int TP = N + 2;
     bool raw_in = false;
     if (active) {
-        raw_in = decode_row<N, L>(T, li, a.dir_in[p], a.store_in);
+        raw_in = decode_row<N, L>(T, li, e, a.store_in);
         fill_ghosts<N>(T, li, a.ein, pp, 0, a.g);
     }
     __syncthreads();
+    WG_PHASE_MARK(0);
     const int j = li;
     if (active) {
         decode_col<N, L>(T, j, raw_in, v);
         if (!raw_in) store_col<N>(T, j, v);
     }
     __syncthreads();
+    WG_PHASE_MARK(1);
     // upwind FV update of column j (solver.hpp:207-231): directions in the
     // reference order +x, -x, +y, -y (solver.hpp:21-22); x = dim 0 = i.
     // No FMA (-fmad=false): out -= r * Q, Q = wl*max(s,0) + wr*min(s,0).
@@ -74,23 +76,26 @@ __device__ __forceinline__ void decode_and_fv(const StepArgs& a, double* T, bool
     }
 }
 
+#ifndef WG_MIN_BLOCKS
+#define WG_MIN_BLOCKS 2
+#endif
 template <int N, int L, int P, int MODE>
-__global__ void __launch_bounds__(Layout<N, P>::NT, 2)
+__global__ void __launch_bounds__(Layout<N, P>::NT, WG_MIN_BLOCKS)
     k_patch_step(const __grid_constant__ StepArgs a) {
     using Lay = Layout<N, P>;
     constexpr int TP = Lay::TP, TILE = Lay::TILE, NT = Lay::NT;
+    static_assert(P <= 32, "slots are handled by the lanes of warp 0");
     extern __shared__ __align__(16) unsigned char smem_raw[];
     double* tiles = reinterpret_cast<double*>(smem_raw);
-    double* red = tiles + P * TILE;   // per-thread mass partials (after the cycle)
-    double* red_fv = red + NT;        // per-thread mass partials (scheme output)
-    unsigned long long* inc = reinterpret_cast<unsigned long long*>(red_fv + NT);
+    unsigned long long* inc = reinterpret_cast<unsigned long long*>(tiles + P * TILE + 2 * NT);
+    __shared__ DirEntry slot_dir[P], next_dir[P];
     __shared__ uint64_t slot_off[P];
     __shared__ int slot_mode[P];  // 0 compressed, 1 raw (skip rule / no compression), 2 dead
-    __shared__ unsigned long long slot_bytes[P], slot_nnz[P], slot_zero[P];
-    __shared__ double slot_m[P], slot_mf[P];
     __shared__ int any_raw;
+    __shared__ ChunkState cs;
 
     const int t = threadIdx.x;
+    const int lane = t & 31;
     const int ps = t / N;
     const int li = t - ps * N;
     const bool lane_ok = t < P * N;
@@ -98,17 +103,32 @@ __global__ void __launch_bounds__(Layout<N, P>::NT, 2)
     double* T = tiles + (lane_ok ? ps : 0) * TILE;
     const int j = li;
     const uint32_t ngroups = (g.npatch + P - 1) / P;
-    StepPartial part{0, 0, 0, 0.0, 0.0};
+    // running partials: every thread its columns' masses, lane s of warp 0
+    // the byte/nnz/zeroed counts of slot s (fixed order -> deterministic)
+    StepPartial acc{0, 0, 0, 0.0, 0.0};
+    WG_PHASE_MARK(-1);
+
+    if (t == 0) cs.cur = cs.end = 0;
+    if (t < P) {
+        const uint32_t p0 = blockIdx.x * P + t;
+        slot_dir[t] = p0 < g.npatch ? a.dir_in[p0] : DirEntry{0, 0u, DIR_DEAD};
+    }
+    __syncthreads();
 
     // persistent CTAs: patch groups grp, grp + gridDim.x, ... (fixed order)
     for (uint32_t grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
         const uint32_t p = grp * P + ps;
         const bool valid = lane_ok && p < g.npatch;
         const PatchPos pp = patch_pos(p, g);
+        const uint32_t nxt = grp + gridDim.x;
+        if (t < P) {  // the next group's directory entries (latency hidden by this group)
+            const uint32_t pn = nxt * P + t;
+            next_dir[t] = (nxt < ngroups && pn < g.npatch) ? a.dir_in[pn] : DirEntry{0, 0u, DIR_DEAD};
+        }
 
         if (MODE == MODE_DECODE) {
             bool raw_in = false;
-            if (valid) raw_in = decode_row<N, L>(T, li, a.dir_in[p], a.store_in);
+            if (valid) raw_in = decode_row<N, L>(T, li, slot_dir[ps], a.store_in);
             __syncthreads();
             if (valid) {
                 double v[N];
@@ -118,14 +138,12 @@ __global__ void __launch_bounds__(Layout<N, P>::NT, 2)
                 for (int i = 0; i < N; ++i) out[(i + 1) * TP + j + 1] = v[i];
             }
             __syncthreads();
+            if (t < P) slot_dir[t] = next_dir[t];
+            __syncthreads();
             continue;
         }
 
-        if (t < P) {
-            slot_bytes[t] = slot_nnz[t] = slot_zero[t] = 0;
-            slot_mode[t] = a.compress ? 2 : 1;  // no_compression: every patch is stored raw
-        }
-        if (t == 0) any_raw = 0;
+        if (t < P) slot_mode[t] = 2;
         double v[N];
         double m = 0.0;
         // pass 0 runs the cycle for every slot; pass 1 (only if some slot
@@ -134,122 +152,115 @@ __global__ void __launch_bounds__(Layout<N, P>::NT, 2)
         // can be stored raw.
         for (int pass = 0; pass < 2; ++pass) {
             const bool active = valid && (pass == 0 || slot_mode[ps] == 1);
-            decode_and_fv<N, L>(a, T, active, p, pp, li, v);
+            decode_and_fv<N, L>(a, T, active, lane_ok ? slot_dir[ps] : DirEntry{}, pp, li, v);
             if (pass == 1) {
                 if (active) m = col_mass<N>(j, v);
                 break;
             }
-            red_fv[t] = valid ? col_mass<N>(j, v) : 0.0;
-            if (!a.compress) {
-                m = red_fv[t];
-                break;
-            }
-            // ---- forward DWT along dim 0 (columns) in registers -----------
-            __syncthreads();  // everyone done reading the state tile
-            if (valid) fwd_col_to_tile<N, L>(T, j, v);
-            __syncthreads();
+            if (valid) acc.mass_fv += col_mass<N>(j, v);
+            WG_PHASE_MARK(2);
+            // warm L2 with the next group's inputs while this one computes
+            if (nxt < ngroups && lane_ok && nxt * P + ps < g.npatch)
+                prefetch_patch<N>(a, nxt * P + ps, next_dir[ps], 0, li, N);
 
-            // ---- ROW phase: forward DWT along dim 1, threshold, count -----
-            const int i = li;
             unsigned nz = 0, zr = 0;
-            if (valid) fwd_row_threshold<N, L>(T, i, a.thr, v, nz, zr);
-            cta_inclusive_scan<NT>(((unsigned long long)zr << 32) | nz, inc);
-            unsigned long long slot_base = 0, slot_tot = 0;
-            if (lane_ok) {
-                slot_base = ps == 0 ? 0ull : inc[ps * N - 1];
-                slot_tot = inc[ps * N + N - 1] - slot_base;
+            if (a.compress) {
+                // ---- forward DWT along dim 0 (columns) in registers -------
+                __syncthreads();  // everyone done reading the state tile
+                WG_PHASE_MARK(3);
+                if (valid) fwd_col_to_tile<N, L>(T, j, v);
+                __syncthreads();
+                WG_PHASE_MARK(4);
+                // ---- ROW phase: forward DWT along dim 1, threshold, count --
+                if (valid) fwd_row_threshold<N, L>(T, li, a.thr, v, nz, zr);
+                cta_inclusive_scan<NT>(((unsigned long long)zr << 32) | nz, inc);
+                WG_PHASE_MARK(5);
+            } else {
+                __syncthreads();
             }
-            const uint32_t nnz_tot = (uint32_t)(slot_tot & 0xffffffffu);
-            const uint32_t zero_tot = (uint32_t)(slot_tot >> 32);
-            if (valid && li == 0) {
-                slot_bytes[ps] = 12ull * nnz_tot + 4ull * (N + 1);  // CsrBlock::byte_size
-                slot_nnz[ps] = nnz_tot;
-                slot_zero[ps] = zero_tot;
-                if (zero_tot == 0) {  // skip rule: stored raw after pass 1
-                    slot_mode[ps] = 1;
-                    any_raw = 1;
-                } else {
-                    const uint64_t bytes = round16(12ull * nnz_tot + 4ull * (N + 1));
-                    const uint64_t off = atomicAdd(a.bump_out, (unsigned long long)bytes);
-                    if (off + bytes > a.cap_out) {
-                        atomicOr(a.err, ERR_STORE_OVERFLOW);
-                        a.dir_out[p] = DirEntry{0, 0u, DIR_DEAD};
-                        slot_mode[ps] = 2;
-                    } else {
-                        slot_mode[ps] = 0;
-                        slot_off[ps] = off;
-                        a.dir_out[p] = DirEntry{off, nnz_tot, 0u};
+            // ---- warp 0, lane s = slot s: modes, one allocation, directory -
+            if (t < 32) {
+                const uint32_t ps_ = (uint32_t)lane;
+                const bool sv = lane < P && grp * P + ps_ < g.npatch;
+                unsigned long long base = 0, tot = 0;
+                if (sv && a.compress) {
+                    base = ps_ == 0 ? 0ull : inc[ps_ * N - 1];
+                    tot = inc[ps_ * N + N - 1] - base;
+                }
+                const uint32_t snz = (uint32_t)(tot & 0xffffffffu), szr = (uint32_t)(tot >> 32);
+                const int mode = !sv ? 2 : (a.compress && szr != 0 ? 0 : 1);
+                unsigned long long need = mode == 0   ? round16(12ull * snz + 4ull * (N + 1))
+                                          : mode == 1 ? round16((unsigned long long)N * N * 8)
+                                                      : 0ull;
+                unsigned long long ex = need;  // exclusive scan over the lanes
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const unsigned long long y = __shfl_up_sync(0xffffffffu, ex, o);
+                    if (lane >= o) ex += y;
+                }
+                const unsigned long long total = __shfl_sync(0xffffffffu, ex, 31);
+                ex -= need;
+                unsigned long long b0 = 0;
+                if (lane == 0) b0 = chunk_alloc(a, cs, total);
+                b0 = __shfl_sync(0xffffffffu, b0, 0);
+                if (sv) {
+                    const uint32_t pq = grp * P + ps_;
+                    const bool dead = b0 == ~0ull;
+                    slot_mode[ps_] = dead ? 2 : mode;
+                    slot_off[ps_] = b0 + ex;
+                    a.dir_out[pq] = dead ? DirEntry{0, 0u, DIR_DEAD}
+                                         : (mode == 0 ? DirEntry{b0 + ex, snz, 0u} : DirEntry{b0 + ex, 0u, DIR_RAW});
+                    if (a.compress) {
+                        acc.comp_bytes += 12ull * snz + 4ull * (N + 1);  // CsrBlock::byte_size
+                        acc.nnz += snz;
+                        acc.zeroed += szr;
                     }
                 }
+                const unsigned rawmask = __ballot_sync(0xffffffffu, sv && mode == 1 && b0 != ~0ull);
+                if (lane == 0) any_raw = a.compress && rawmask != 0;
             }
             __syncthreads();
+            WG_PHASE_MARK(6);
+            if (!a.compress) break;
             const bool compressed = valid && slot_mode[ps] == 0;
             if (compressed) {
-                const uint32_t k = (uint32_t)((inc[t] - slot_base) & 0xffffffffu) - nz;
-                write_csr_row<N, L>(a.store_out + slot_off[ps], nnz_tot, i, k, nz, v);
-                inv_row_to_tile<N, L>(T, i, v);  // reconstruction, dim 1 inverse
+                const unsigned long long base = ps == 0 ? 0ull : inc[ps * N - 1];
+                const uint32_t k = (uint32_t)((inc[t] - base) & 0xffffffffu) - nz;
+                const uint32_t snz = (uint32_t)((inc[ps * N + N - 1] - base) & 0xffffffffu);
+                write_csr_row<N, L>(a.store_out + slot_off[ps], snz, li, k, nz, v);
+                inv_row_to_tile<N, L>(T, li, v);  // reconstruction, dim 1 inverse
             }
             __syncthreads();
+            WG_PHASE_MARK(7);
             if (compressed) {
                 decode_col<N, L>(T, j, false, v);
                 m = col_mass<N>(j, v);
                 write_edges<N>(a.eout, pp, 0, g, j, v);
             }
+            WG_PHASE_MARK(8);
             if (!any_raw) break;
             __syncthreads();
         }
 
-        // ---- raw slots: dense store of the FV output ----------------------
-        __syncthreads();
-        if (valid && li == 0 && slot_mode[ps] == 1) {
-            const uint64_t bytes = round16((uint64_t)N * N * 8);
-            const uint64_t off = atomicAdd(a.bump_out, (unsigned long long)bytes);
-            if (off + bytes > a.cap_out) {
-                atomicOr(a.err, ERR_STORE_OVERFLOW);
-                a.dir_out[p] = DirEntry{0, 0u, DIR_DEAD};
-                slot_off[ps] = ~0ull;
-            } else {
-                slot_off[ps] = off;
-                a.dir_out[p] = DirEntry{off, 0u, DIR_RAW};
-            }
-        }
-        __syncthreads();
+        // ---- raw slots: dense store of the scheme output ------------------
         if (valid && slot_mode[ps] == 1) {
-            if (slot_off[ps] != ~0ull) {
-                double* d = reinterpret_cast<double*>(a.store_out + slot_off[ps]);
+            double* d = reinterpret_cast<double*>(a.store_out + slot_off[ps]);
 #pragma unroll
-                for (int i = 0; i < N; ++i) d[(size_t)i * N + j] = v[i];
-            }
+            for (int i = 0; i < N; ++i) d[(size_t)i * N + j] = v[i];
             write_edges<N>(a.eout, pp, 0, g, j, v);
+            if (!a.compress) m = col_mass<N>(j, v);
         }
-        red[t] = m;
+        acc.mass += m;
         __syncthreads();
-
-        // ---- per-group partial sums (fixed slot order) ---------------------
-        const int warp = t >> 5;
-        for (int sl = warp; sl < P; sl += NT / 32) {
-            const double mm = warp_sum_range(red, sl * N, N);
-            const double mf = warp_sum_range(red_fv, sl * N, N);
-            if ((t & 31) == 0) {
-                slot_m[sl] = mm;
-                slot_mf[sl] = mf;
-            }
-        }
+        if (t < P) slot_dir[t] = next_dir[t];
         __syncthreads();
-        if (t == 0) {
-            for (int sl = 0; sl < P; ++sl) {
-                if (grp * P + sl >= g.npatch) break;
-                part.comp_bytes += slot_bytes[sl];
-                part.nnz += slot_nnz[sl];
-                part.zeroed += slot_zero[sl];
-                part.mass += slot_m[sl];
-                part.mass_fv += slot_mf[sl];
-            }
-        }
-        __syncthreads();
+        WG_PHASE_MARK(9);
     }
     if (MODE == MODE_DECODE) return;
+    const StepPartial part = cta_reduce_partial<NT>(acc);
+    WG_PHASE_MARK(10);
     finalize_step(a, part);
+    WG_PHASE_MARK(11);
 }
 
 }  // namespace wg

@@ -17,6 +17,27 @@ namespace wg {
 
 constexpr int kMaxLevels = 8;
 
+// ---- optional phase timing (tuning builds only: -DWG_PHASE_TIMING) ---------
+// Thread 0 of every CTA adds the cycles since its previous mark (i.e. the
+// wall time of the phase that just ended at a barrier) to g_phase_cycles[k].
+#ifdef WG_PHASE_TIMING
+__device__ unsigned long long g_phase_cycles[32];
+__device__ __forceinline__ unsigned long long& phase_last() {
+    __shared__ unsigned long long last;
+    return last;
+}
+__device__ __forceinline__ void phase_mark(int k) {
+    if (threadIdx.x == 0) {
+        const unsigned long long t = clock64();
+        if (k >= 0) atomicAdd(&g_phase_cycles[k], t - phase_last());
+        phase_last() = t;
+    }
+}
+#define WG_PHASE_MARK(k) ::wg::phase_mark(k)
+#else
+#define WG_PHASE_MARK(k) ((void)0)
+#endif
+
 // Per-CTA partial sums of the step metrics (fixed order inside the CTA).
 struct StepPartial {
     unsigned long long comp_bytes, nnz, zeroed;
@@ -33,6 +54,7 @@ struct StepArgs {
     unsigned long long* bump_out;
     unsigned long long* bump_next;  // pool written by the next step: reset by the last CTA
     uint64_t cap_out;
+    uint64_t chunk;                 // per-CTA sub-allocation chunk of the output pool (bytes)
     unsigned* err;
     double* decode_out;   // MODE_DECODE: grid buffer (true layout) of this shard
     double* scratch;      // D2Q9: per-CTA L2-resident staging of 9 N*N fields
@@ -290,6 +312,102 @@ __device__ __forceinline__ double warp_sum_range(const double* red, int base, in
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
     return s;
+}
+
+// Sum of every thread's partial over the CTA with a fixed association
+// (xor-shuffle trees inside warps, warps in order): result valid in thread 0.
+template <int NT>
+__device__ __forceinline__ StepPartial cta_reduce_partial(StepPartial x) {
+    __shared__ StepPartial wpart[NT / 32];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        x.comp_bytes += __shfl_xor_sync(0xffffffffu, x.comp_bytes, o);
+        x.nnz += __shfl_xor_sync(0xffffffffu, x.nnz, o);
+        x.zeroed += __shfl_xor_sync(0xffffffffu, x.zeroed, o);
+        x.mass += __shfl_xor_sync(0xffffffffu, x.mass, o);
+        x.mass_fv += __shfl_xor_sync(0xffffffffu, x.mass_fv, o);
+    }
+    if ((threadIdx.x & 31) == 0) wpart[threadIdx.x >> 5] = x;
+    __syncthreads();
+    StepPartial r{0, 0, 0, 0.0, 0.0};
+    if (threadIdx.x == 0) {
+        for (int w = 0; w < NT / 32; ++w) {
+            r.comp_bytes += wpart[w].comp_bytes;
+            r.nnz += wpart[w].nnz;
+            r.zeroed += wpart[w].zeroed;
+            r.mass += wpart[w].mass;
+            r.mass_fv += wpart[w].mass_fv;
+        }
+    }
+    return r;
+}
+
+// Per-CTA sub-allocator of the output pool: the CTA grabs `a.chunk` bytes
+// with one global atomic and carves its blocks out of them, so most groups
+// allocate without a global round trip.  Blocks larger than chunk/8 get an
+// exact allocation, so the unused chunk tails stay below 1/8 of the bytes
+// served from chunks plus one chunk per CTA.  Returns ~0 (and raises the
+// error bit) on overflow.
+struct ChunkState {
+    unsigned long long cur, end;
+};
+
+__device__ __forceinline__ unsigned long long chunk_alloc(const StepArgs& a, ChunkState& cs,
+                                                          unsigned long long bytes) {
+    if (bytes == 0) return cs.cur;
+    if (bytes * 8 > a.chunk) {
+        const unsigned long long off = atomicAdd(a.bump_out, bytes);
+        if (off + bytes > a.cap_out) {
+            atomicOr(a.err, ERR_STORE_OVERFLOW);
+            return ~0ull;
+        }
+        return off;
+    }
+    if (cs.cur + bytes > cs.end) {
+        const unsigned long long c = atomicAdd(a.bump_out, (unsigned long long)a.chunk);
+        if (c + a.chunk > a.cap_out) {
+            atomicOr(a.err, ERR_STORE_OVERFLOW);
+            cs.cur = cs.end = 0;
+            return ~0ull;
+        }
+        cs.cur = c;
+        cs.end = c + a.chunk;
+    }
+    const unsigned long long off = cs.cur;
+    cs.cur += bytes;
+    return off;
+}
+
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
+// Prefetch [p, p + bytes) into L2, lines split over `nthreads` threads.
+__device__ __forceinline__ void prefetch_range(const unsigned char* p, unsigned long long bytes, int tid,
+                                               int nthreads) {
+    for (unsigned long long o = (unsigned long long)tid * 128; o < bytes; o += (unsigned long long)nthreads * 128)
+        prefetch_l2(p + o);
+}
+
+// L2 prefetch of everything the decode of patch p will read: its stored
+// block and the neighbours' edge lines (the ghost-ring sources).
+template <int N>
+__device__ __forceinline__ void prefetch_patch(const StepArgs& a, uint32_t p, const DirEntry e, uint32_t q,
+                                               int tid, int nthreads) {
+    const unsigned long long bytes = (e.flags & DIR_RAW) ? (unsigned long long)N * N * 8
+                                                          : 12ull * e.nnz + 4ull * (N + 1);
+    if (!(e.flags & DIR_DEAD)) prefetch_range(a.store_in + e.off, bytes, tid, nthreads);
+    const PatchPos pp = patch_pos(p, a.g);
+    const int lines = (N * 8 + 127) / 128;
+    const double* srcs[7] = {a.ein.colhi + edge_ix(pp.ar, pp.bl, q, a.g, N),
+                             a.ein.collo + edge_ix(pp.ar, pp.br, q, a.g, N),
+                             a.ein.rowhi + edge_ix(pp.su, pp.b, q, a.g, N),
+                             a.ein.rowlo + edge_ix(pp.sd, pp.b, q, a.g, N),
+                             a.ein.rowhi + edge_ix(pp.su, pp.bl, q, a.g, N),
+                             a.ein.rowlo + edge_ix(pp.sd, pp.br, q, a.g, N),
+                             a.ein.rowhi + edge_ix(pp.su, pp.br, q, a.g, N)};
+    for (int k = tid; k < 7 * lines; k += nthreads)
+        prefetch_l2(reinterpret_cast<const unsigned char*>(srcs[k / lines]) + (k % lines) * 128);
 }
 
 // End of a step, called by every CTA with its partial sums: the last CTA to

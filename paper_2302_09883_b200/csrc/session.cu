@@ -10,6 +10,7 @@
 // synchronises with the host inside the step loop.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <vector>
@@ -181,6 +182,7 @@ struct Session {
     double* mass_fv = nullptr;
     uint64_t row_cap = 0;
     uint64_t cap = 0;  // bytes per pool
+    uint64_t chunk = 0;  // per-CTA sub-allocation chunk
     uint64_t device_bytes = 0;
 
     int cur = 0;  // pool/edges holding the current state
@@ -300,7 +302,10 @@ struct Session {
             WG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ks.main, ks.threads, ks.smem));
             WG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, shard.device));
             const uint64_t groups = (sg.npatch + ks.P - 1) / ks.P;
-            grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(groups, (uint64_t)std::max(per_sm, 1) * sms));
+            uint64_t resident = (uint64_t)std::max(per_sm, 1) * sms;
+            if (const char* f = std::getenv("WG_GRID_WAVES"))  // tuning knob: CTAs = waves x resident
+                resident = (uint64_t)std::max(1.0, std::atof(f) * (double)resident);
+            grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(groups, resident));
             if (ks.scratch_doubles) scratch = dalloc<double>((uint64_t)grid * ks.scratch_doubles);
         }
         // thresholds (threshold.hpp:31-47) — the "c == 0 or levels == 0"
@@ -310,7 +315,12 @@ struct Session {
 
         const uint64_t raw_block = round16((uint64_t)N * N * 8);
         const uint64_t blocks = (uint64_t)sg.npatch * sg.m;
-        cap = cfg.store_budget_bytes ? cfg.store_budget_bytes / 2 : blocks * raw_block;
+        // per-CTA sub-allocation chunk: big enough to amortise the global
+        // atomic, small enough that the unused tails (<= one chunk per CTA)
+        // stay a small fraction of the pool
+        chunk = std::clamp<uint64_t>(round16(blocks * raw_block / (8ull * grid)), 4096, 256 * 1024);
+        cap = cfg.store_budget_bytes ? cfg.store_budget_bytes / 2
+                                     : blocks * raw_block + blocks * raw_block / 8 + (uint64_t)grid * chunk;
         cap = std::max<uint64_t>(cap, 16) & ~uint64_t(15);
         for (int k = 0; k < 2; ++k) {
             store[k] = dalloc<unsigned char>(cap);
@@ -391,6 +401,7 @@ struct Session {
         a.bump_out = bump + dst;
         a.bump_next = bump + src;
         a.cap_out = cap;
+        a.chunk = chunk;
         a.err = err;
         a.partials = partials;
         a.done = done;
@@ -557,6 +568,25 @@ wg_status wg_session_last_row(wg_session* sp, wg_metrics_row* row) {
         WG_CUDA(cudaMemcpyAsync(row, s->rows + (s->step - 1), sizeof(wg_metrics_row), cudaMemcpyDeviceToHost,
                                 s->stream));
         s->sync();
+    });
+}
+
+// Tuning builds (-DWG_PHASE_TIMING) only: summed per-phase cycles of thread 0
+// of every CTA; `reset` zeroes them.  Not part of the product ABI.
+wg_status wg_debug_phase_cycles(uint64_t* out, int32_t n, int32_t reset) {
+    return guard([&] {
+#ifdef WG_PHASE_TIMING
+        unsigned long long h[32];
+        WG_CUDA(cudaMemcpyFromSymbol(h, g_phase_cycles, sizeof h));
+        for (int k = 0; k < n && k < 32; ++k) out[k] = h[k];
+        if (reset) {
+            std::memset(h, 0, sizeof h);
+            WG_CUDA(cudaMemcpyToSymbol(g_phase_cycles, h, sizeof h));
+        }
+#else
+        (void)out; (void)n; (void)reset;
+        raise(WG_LOGIC, "built without WG_PHASE_TIMING");
+#endif
     });
 }
 
