@@ -280,7 +280,7 @@ class RunResult:  # pipeline.hpp:65-70
     t_final: float
 
 
-def run(cfg: RunConfig, lib=None, max_rows: int = 1 << 20) -> RunResult:
+def run(cfg: RunConfig, lib=None, max_rows: int = 1 << 17) -> RunResult:
     """run(RunConfig) (pipeline.hpp:129-305)."""
     L = _lib(lib)
     c = cfg.to_c()

@@ -105,7 +105,7 @@ def main():
         "demo": {
             "n": 129, "levels": 6, "threshold": 0.2, "nonzeros": nnz, "zeroed": z,
             "field_sha256": hashlib.sha256(f.tobytes()).hexdigest(),
-            "coeff_sha256": hashlib.sha256(cs.tobytes()).hexdigest(),
+            "coeff_sha256": hashlib.sha256(cs.tobytes()).hexdigest(),  # after thresholding
             "recon_sha256": hashlib.sha256(rec.tobytes()).hexdigest(),
             "csr_v_sha256": hashlib.sha256(blk.v.tobytes()).hexdigest(),
             "csr_col_sha256": hashlib.sha256(blk.col.tobytes()).hexdigest(),

@@ -195,3 +195,43 @@ def test_lbm_step_bit_exact(product, oracle):
     api.lbm_step(cur, n1, 0.6, lib=product)
     api.lbm_step(cur, n2, 0.6, lib=oracle)
     assert np.array_equal(bits(n1.data), bits(n2.data))
+
+
+def test_demo_discontinuous_golden(product):
+    """pipeline.hpp:417-460 / PAPER.md:481 on the device, against the
+    reference-generated golden hashes (tests/golden/kat.json)."""
+    import hashlib
+    import json
+
+    from tests.conftest import GOLDEN
+    from tests.golden.make_golden import demo_field
+
+    sha = lambda a: hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()  # noqa: E731
+    kat = json.loads((GOLDEN / "kat.json").read_text())["demo"]
+    f = demo_field()
+    cs = api.dwt_nd(f, 6, lib=product)
+    assert api.apply_threshold(cs, 6, api.ThresholdSpec("constant", 0.2), lib=product) == kat["zeroed"]
+    assert sha(cs) == kat["coeff_sha256"] and int(np.count_nonzero(cs)) == 481
+    assert sha(api.idwt_nd(cs, 6, lib=product)) == kat["recon_sha256"]
+    blk = api.csr_encode(cs, 129, 129, lib=product)
+    assert sha(blk.v) == kat["csr_v_sha256"] and sha(blk.col) == kat["csr_col_sha256"]
+    assert sha(blk.row) == kat["csr_row_sha256"]
+
+
+@pytest.mark.parametrize("name", ["small_transport", "small_lbm"])
+def test_run_goldens_on_device(product, name):
+    import hashlib
+    import json
+
+    from tests.conftest import GOLDEN
+
+    gold = json.loads((GOLDEN / f"{name}.json").read_text())
+    c = gold["config"]
+    cfg = api.RunConfig(scheme=c["scheme"], nx=c["nx"], splits=tuple(c["splits"]), levels=c["levels"],
+                        t_end=c["t_end"], lbm_steps=c["lbm_steps"], compute_l2=False,
+                        spec=api.ThresholdSpec(c["spec"]["mode"], c["spec"]["c"], c["spec"]["alpha"]))
+    r = api.run(cfg, lib=product)
+    assert len(r.rows) == gold["steps"]
+    for row, g in zip(r.rows, gold["rows"]):
+        assert (row["nnz"], row["zeroed"], row["compressed_bytes"]) == (g["nnz"], g["zeroed"], g["compressed_bytes"])
+    assert hashlib.sha256(np.ascontiguousarray(r.grid.logical_view()).tobytes()).hexdigest() == gold["state_sha256"]
