@@ -238,7 +238,7 @@ def bench_b200(args, w: dict):
             # reported are those of the loaded GPU around the timed region
             t_w = time.perf_counter()
             done = 0
-            while done < args.warmup or (world == 1 and clocks.count() < 3 and time.perf_counter() - t_w < 5.0):
+            while done < args.warmup or (world == 1 and clocks.count() < 3 and time.perf_counter() - t_w < 3.0):
                 sess.step(dt)
                 done += 1
                 if done % 8 == 0:
@@ -301,12 +301,14 @@ def bench_b200(args, w: dict):
                      "avg_launch_ms": launch_ms, "peak_source": pk["source"],
                      "step_share": main_max / tot_ms if tot_ms else None},
         "e2e": e2e,
-        "gpu_launches": 3 * args.steps,
+        "gpu_launches": args.steps,  # one fused kernel launch per step (k_*_step<STEP>)
         "clocks": clocks.summary(),
         "device_bytes": info.device_bytes,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu_steps = args.cpu_steps
+        # bounded sample: calibrate on a few steps, then about 12 s of CPU work
+        _, s0, _, _, _ = cpu_run(w, 3, os.cpu_count() or 1)
+        cpu_steps = args.cpu_steps or int(max(3, min(2000, 12.0 / max(s0 / 3, 1e-6))))
         mlups, secs, kind, cores, _ = cpu_run(w, cpu_steps, os.cpu_count() or 1)
         line["cpu_baseline"] = {"value": mlups, "unit": "MLUPS", "cores": cores, "kind": kind,
                                 "sample": f"{cpu_steps} steps of the full {w['nx'] - 1}^2 workload ({secs:.1f} s)"}
@@ -365,7 +367,7 @@ def main():
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="lbm_c2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-steps", type=int, default=10)
+    ap.add_argument("--cpu-steps", type=int, default=0, help="CPU baseline steps (0: ~12 s of work)")
     args = ap.parse_args()
     if args.impl == "b200":
         args.warmup = max(args.warmup, 3)  # timing rule: at least 3 untimed warm-up steps
