@@ -112,8 +112,7 @@ __global__ void __launch_bounds__(LbmLayout<N>::NT) k_lbm_step(const __grid_cons
     __shared__ ChunkState cs;
     __shared__ DirEntry next_dir[9];
     __shared__ unsigned long long patch_bytes, patch_nnz, patch_zero;
-    __shared__ uint32_t comp_nnz[9];
-    __shared__ uint32_t row_k[3 * NT];  // CSR entry offset of each row, per round
+    __shared__ uint32_t comp_nnz[3];
 
     const int t = threadIdx.x;
     const int s = t / N;
@@ -155,17 +154,22 @@ __global__ void __launch_bounds__(LbmLayout<N>::NT) k_lbm_step(const __grid_cons
             for (int q = s; q < 9; q += 3) prefetch_patch<N>(a, pn, next_dir[q], q, li, N);
         double m = 0.0;
         bool store_raw = !a.compress;
+        // nothing can be zeroed with c == 0 or no transform (threshold.hpp:53):
+        // every patch is raw by the skip rule, so no CSR block is written
+        // (the coefficients are still transformed and counted for the
+        // metrics, pipeline.hpp:234-242)
+        const bool cycle = a.thr_any != 0;
         if (a.compress) {
             if (t == 0) {
                 patch_bytes = 0;
                 patch_nnz = 0;
                 patch_zero = 0;
             }
-            // ---- pass 1: forward DWT + threshold of every population; the
-            // kept coefficients go back to the scratch (transposed: column-
-            // major, so both passes access it coalesced).  The skip rule
-            // needs the patch total of zeroed coefficients before anything
-            // is written to the store.
+            // ---- per round: forward DWT, threshold, CSR, reconstruction ----
+            // written speculatively as compressed: a patch whose cycle zeroed
+            // nothing (rare for c > 0) is re-derived and stored raw below,
+            // overwriting its directory entries (its CSR blocks are left as
+            // unused pool space).
             for (int rd = 0; rd < 3; ++rd) {
                 const int q = 3 * rd + s;
                 double v[N];
@@ -178,56 +182,35 @@ __global__ void __launch_bounds__(LbmLayout<N>::NT) k_lbm_step(const __grid_cons
                 __syncthreads();
                 WG_PHASE_MARK(3);
                 unsigned nz = 0, zr = 0;
-                if (lane_ok) {
-                    fwd_row_threshold<N, L>(T, li, a.thr, v, nz, zr);
-#pragma unroll
-                    for (int pc = 0; pc < N; ++pc) S[(size_t)q * NN + pc * N + li] = v[interleaved_of<N, L>(pc)];
-                }
+                if (lane_ok) fwd_row_threshold<N, L>(T, li, a.thr, v, nz, zr);
                 cta_inclusive_scan<NT>(((unsigned long long)zr << 32) | nz, inc);
-                if (lane_ok) {
-                    const unsigned long long base = s == 0 ? 0ull : inc[s * N - 1];
-                    row_k[rd * NT + t] = (uint32_t)((inc[t] - base) & 0xffffffffu) - nz;
-                    if (li == 0) {
-                        const unsigned long long tot = inc[s * N + N - 1] - base;
-                        comp_nnz[q] = (uint32_t)(tot & 0xffffffffu);
-                        atomicAdd(&patch_bytes, 12ull * (tot & 0xffffffffu) + 4ull * (N + 1));
-                        atomicAdd(&patch_nnz, tot & 0xffffffffu);
-                        atomicAdd(&patch_zero, tot >> 32);
-                    }
-                }
-                __syncthreads();
-                WG_PHASE_MARK(4);
-            }
-            if (t == 0) {
-                part.comp_bytes += patch_bytes;
-                part.nnz += patch_nnz;
-                part.zeroed += patch_zero;
-            }
-            store_raw = patch_zero == 0;
-            // ---- pass 2: CSR blocks, reconstruction, edge lines, mass ------
-            for (int rd = 0; rd < 3 && !store_raw; ++rd) {
-                const int q = 3 * rd + s;
                 if (t == 0) {
                     for (int sl = 0; sl < 3; ++sl) {
                         const int qq = 3 * rd + sl;
-                        const uint64_t off = chunk_alloc(a, cs, round16(12ull * comp_nnz[qq] + 4ull * (N + 1)));
+                        const unsigned long long base = sl == 0 ? 0ull : inc[sl * N - 1];
+                        const unsigned long long tot = inc[sl * N + N - 1] - base;
+                        const uint32_t snz = (uint32_t)(tot & 0xffffffffu);
+                        comp_nnz[sl] = snz;
+                        patch_bytes += 12ull * snz + 4ull * (N + 1);
+                        patch_nnz += snz;
+                        patch_zero += tot >> 32;
+                        if (!cycle) {
+                            slot_ok[sl] = 0;
+                            continue;
+                        }
+                        const uint64_t off = chunk_alloc(a, cs, round16(12ull * snz + 4ull * (N + 1)));
                         slot_ok[sl] = off != ~0ull;
                         slot_off[sl] = off;
-                        a.dir_out[(size_t)p * 9 + qq] =
-                            slot_ok[sl] ? DirEntry{off, comp_nnz[qq], 0u} : DirEntry{0, 0u, DIR_DEAD};
+                        a.dir_out[(size_t)p * 9 + qq] = slot_ok[sl] ? DirEntry{off, snz, 0u} : DirEntry{0, 0u, DIR_DEAD};
                     }
                 }
                 __syncthreads();
                 WG_PHASE_MARK(5);
                 const bool ok = lane_ok && slot_ok[s];
-                double v[N];
                 if (ok) {
-#pragma unroll
-                    for (int pc = 0; pc < N; ++pc) v[interleaved_of<N, L>(pc)] = S[(size_t)q * NN + pc * N + li];
-                    unsigned nz = 0;
-#pragma unroll
-                    for (int r = 0; r < N; ++r) nz += v[r] != 0.0 ? 1u : 0u;
-                    write_csr_row<N, L>(a.store_out + slot_off[s], comp_nnz[q], li, row_k[rd * NT + t], nz, v);
+                    const unsigned long long base = s == 0 ? 0ull : inc[s * N - 1];
+                    const uint32_t k = (uint32_t)((inc[t] - base) & 0xffffffffu) - nz;
+                    write_csr_row<N, L>(a.store_out + slot_off[s], comp_nnz[s], li, k, nz, v);
                     inv_row_to_tile<N, L>(T, li, v);
                 }
                 __syncthreads();
@@ -240,9 +223,16 @@ __global__ void __launch_bounds__(LbmLayout<N>::NT) k_lbm_step(const __grid_cons
                 __syncthreads();
                 WG_PHASE_MARK(7);
             }
-            // skip rule (pipeline.hpp:243-249): the collided state, bit for
-            // bit, is re-derived (pass 1 overwrote the scratch) and stored raw
-            if (store_raw) decode_stream_collide<N, L>(a, T, S, p, pp, s, li, lane_ok);
+            if (t == 0) {
+                part.comp_bytes += patch_bytes;
+                part.nnz += patch_nnz;
+                part.zeroed += patch_zero;
+            }
+            // skip rule (pipeline.hpp:243-249): the scratch still holds the
+            // collided state bit for bit; the raw store below overwrites the
+            // directory entries written by the rounds
+            store_raw = patch_zero == 0;
+            if (store_raw) m = 0.0;
         }
         if (store_raw) {
             for (int rd = 0; rd < 3; ++rd) {

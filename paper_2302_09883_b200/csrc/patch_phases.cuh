@@ -64,6 +64,7 @@ struct StepArgs {
     double* mass_fv_out;      // this step's scheme-output mass (strict mode)
     ShardGeom g;
     int compress;             // 0: RunConfig::no_compression
+    int thr_any;              // 0: c == 0 or levels == 0 (nothing can be zeroed)
     uint64_t step;
     double time;
     uint64_t dense_bytes;     // CompressedPatch::dense_bytes summed over the shard

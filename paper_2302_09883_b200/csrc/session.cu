@@ -408,6 +408,7 @@ struct Session {
         a.scratch = scratch;
         a.g = sg;
         a.compress = cfg.no_compression ? 0 : 1;
+        a.thr_any = (cfg.c > 0.0 && levels > 0) ? 1 : 0;
         a.dense_bytes = (uint64_t)sg.npatch * 8ull * N * N * sg.m;
         std::memcpy(a.thr, thr, sizeof(thr));
         return a;
