@@ -17,6 +17,7 @@
 
 #include "common.cuh"
 #include "host_model.h"
+#include "half_kernels.cuh"
 #include "lbm_kernels.cuh"
 #include "patch_kernels.cuh"
 
@@ -52,6 +53,52 @@ KernelSet make_lbm_set() {
         WG_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k.smem));
     }
     return k;
+}
+
+// 65-point patches: half-line ownership (half_kernels.cuh)
+template <int N, int L, int P>
+KernelSet make_set_h() {
+    using Lay = HLayout<N, P>;
+    KernelSet k;
+    k.main = k_patch_step_h<N, L, P, MODE_STEP>;
+    k.decode = k_patch_step_h<N, L, P, MODE_DECODE>;
+    k.P = P;
+    k.threads = Lay::NT;
+    k.smem = Lay::smem_bytes();
+    k.persistent = false;
+    k.scratch_doubles = 0;
+    for (auto f : {k.main, k.decode})
+        WG_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k.smem));
+    return k;
+}
+
+template <int N, int L>
+KernelSet make_lbm_set_h() {
+    using Lay = HLayout<N, 3>;
+    KernelSet k;
+    k.main = k_lbm_step_h<N, L, MODE_STEP>;
+    k.decode = k_lbm_step_h<N, L, MODE_DECODE>;
+    k.P = 1;
+    k.threads = Lay::NT;
+    k.smem = Lay::smem_bytes();
+    k.persistent = true;
+    k.scratch_doubles = LbmLayout<N>::scratch_doubles();
+    for (auto f : {k.main, k.decode})
+        WG_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k.smem));
+    return k;
+}
+
+template <int N, int L = 0>
+bool pick_h_levels(int levels, bool lbm, KernelSet& out) {
+    if constexpr ((1 << L) <= N - 1 && L <= 6) {
+        if (levels == L) {
+            out = lbm ? make_lbm_set_h<N, L>() : make_set_h<N, L, 2>();
+            return true;
+        }
+        return pick_h_levels<N, L + 1>(levels, lbm, out);
+    } else {
+        return false;
+    }
 }
 
 template <int N, int L = 0>
@@ -104,7 +151,8 @@ KernelSet select_kernels(int scheme, uint64_t n, int levels) {
         switch (n) {
             case 17: ok = pick_lbm_levels<17>(levels, k); break;
             case 33: ok = pick_lbm_levels<33>(levels, k); break;
-            case 65: ok = pick_lbm_levels<65>(levels, k); break;
+            case 65: ok = std::getenv("WG_HALF_LINES") ? pick_h_levels<65>(levels, true, k)
+                                                       : pick_lbm_levels<65>(levels, k); break;
             default: break;
         }
         if (!ok)
@@ -116,7 +164,8 @@ KernelSet select_kernels(int scheme, uint64_t n, int levels) {
         case 9: ok = pick_levels<9, 7>(levels, k); break;
         case 17: ok = pick_levels<17, 15>(levels, k); break;
         case 33: ok = pick_levels<33, 8>(levels, k); break;
-        case 65: ok = pick_levels<65, 2>(levels, k); break;
+        case 65: ok = std::getenv("WG_HALF_LINES") ? pick_h_levels<65>(levels, false, k)
+                                                   : pick_levels<65, 2>(levels, k); break;
         default: break;
     }
     if (!ok)
