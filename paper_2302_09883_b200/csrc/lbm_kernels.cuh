@@ -47,7 +47,7 @@ __device__ __forceinline__ double decode_stream_collide(const StepArgs& a, doubl
         bool raw_in = false;
         if (lane_ok) {
             raw_in = decode_row<N, L>(T, li, a.dir_in[(size_t)p * 9 + q], a.store_in);
-            fill_ghosts<N>(T, li, a.ein, pp, q, a.g);
+            fill_ghosts_lbm<N>(T, li, a.ein, pp, q, a.g);
         }
         __syncthreads();
         if (lane_ok && !raw_in) {
@@ -150,8 +150,10 @@ __global__ void __launch_bounds__(LbmLayout<N>::NT) k_lbm_step(const __grid_cons
         const uint32_t pn = p + gridDim.x;  // this CTA's next patch
         if (t < 9) next_dir[t] = pn < g.npatch ? a.dir_in[(size_t)pn * 9 + t] : DirEntry{0, 0u, DIR_DEAD};
         red_fv[t] = decode_stream_collide<N, L>(a, T, S, p, pp, s, li, lane_ok);
-        if (pn < g.npatch && lane_ok)  // warm L2 with the next patch's blocks and ghost sources
-            for (int q = s; q < 9; q += 3) prefetch_patch<N>(a, pn, next_dir[q], q, li, N);
+        if (pn < g.npatch && lane_ok) {  // warm L2 with the next patch's blocks and ghost sources
+            for (int q = s; q < 9; q += 3) prefetch_block<N>(a, next_dir[q], li, N);
+            prefetch_edges<N>(a, pn, t, Lay::SLOTS * N);
+        }
         double m = 0.0;
         bool store_raw = !a.compress;
         // nothing can be zeroed with c == 0 or no transform (threshold.hpp:53):
@@ -217,7 +219,7 @@ __global__ void __launch_bounds__(LbmLayout<N>::NT) k_lbm_step(const __grid_cons
                 WG_PHASE_MARK(6);
                 if (ok) {
                     decode_col<N, L>(T, li, false, v);
-                    write_edges<N>(a.eout, pp, q, g, li, v);
+                    write_edges_lbm<N>(a.eout, pp, q, g, li, v);
                     m += col_mass<N>(li, v);
                 }
                 __syncthreads();
@@ -257,7 +259,7 @@ __global__ void __launch_bounds__(LbmLayout<N>::NT) k_lbm_step(const __grid_cons
 #pragma unroll
                         for (int i = 0; i < N; ++i) d[i * N + j] = v[i];
                     }
-                    write_edges<N>(a.eout, pp, q, g, j, v);
+                    write_edges_lbm<N>(a.eout, pp, q, g, j, v);
                     m += col_mass<N>(j, v);
                 }
                 __syncthreads();

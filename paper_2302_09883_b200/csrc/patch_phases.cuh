@@ -93,10 +93,10 @@ __device__ __forceinline__ PatchPos patch_pos(uint32_t p, const ShardGeom& g) {
     return pp;
 }
 
-// Index of an edge line element: line arrays are [slot][P1][m][N].
+// Index of an edge line element: line arrays are [slot][P1][me][N].
 __device__ __forceinline__ size_t edge_ix(uint32_t slot, uint32_t b, uint32_t q, const ShardGeom& g,
                                           int N) {
-    return (((size_t)slot * g.P1 + b) * g.m + q) * (size_t)N;
+    return (((size_t)slot * g.P1 + b) * g.me + q) * (size_t)N;
 }
 
 // ROW phase of the decode: row li of component (p, q) from the store into
@@ -267,6 +267,42 @@ __device__ __forceinline__ void write_edges(const EdgeSet& e, const PatchPos& pp
     }
 }
 
+// D2Q9 variants: only the populations that cross a side (session.cuh).
+template <int N>
+__device__ __forceinline__ void fill_ghosts_lbm(double* T, int li, const EdgeSet& e, const PatchPos& pp, int q,
+                                                const ShardGeom& g) {
+    constexpr int TP = N + 2;
+    const int cxq = lbm_cx(q), cyq = lbm_cy(q);
+    if (cxq == 1) T[li + 1] = e.rowhi[edge_ix(pp.su, pp.b, lbm_slot_rowhi(q), g, N) + li];
+    if (cxq == -1) T[(N + 1) * TP + li + 1] = e.rowlo[edge_ix(pp.sd, pp.b, lbm_slot_rowlo(q), g, N) + li];
+    if (cyq == 1) T[(li + 1) * TP] = e.colhi[edge_ix(pp.ar, pp.bl, lbm_slot_colhi(q), g, N) + li];
+    if (cyq == -1) T[(li + 1) * TP + N + 1] = e.collo[edge_ix(pp.ar, pp.br, lbm_slot_collo(q), g, N) + li];
+    if (li == 0) {
+        if (q == 5) T[0] = e.rowhi[edge_ix(pp.su, pp.bl, lbm_slot_rowhi(5), g, N) + N - 2];
+        if (q == 7) T[N + 1] = e.rowhi[edge_ix(pp.su, pp.br, lbm_slot_rowhi(7), g, N) + 1];
+        if (q == 8) T[(N + 1) * TP] = e.rowlo[edge_ix(pp.sd, pp.bl, lbm_slot_rowlo(8), g, N) + N - 2];
+        if (q == 6) T[(N + 1) * TP + N + 1] = e.rowlo[edge_ix(pp.sd, pp.br, lbm_slot_rowlo(6), g, N) + 1];
+    }
+}
+
+template <int N>
+__device__ __forceinline__ void write_edges_lbm(const EdgeSet& e, const PatchPos& pp, int q, const ShardGeom& g,
+                                                int j, const double (&v)[N]) {
+    const int cxq = lbm_cx(q), cyq = lbm_cy(q);
+    if (cxq == -1) e.rowlo[edge_ix((uint32_t)(pp.ar + 1), pp.b, lbm_slot_rowlo(q), g, N) + j] = v[1];
+    if (cxq == 1) e.rowhi[edge_ix((uint32_t)(pp.ar + 1), pp.b, lbm_slot_rowhi(q), g, N) + j] = v[N - 2];
+    if (cyq == -1 && j == 1) {
+        double* d = e.collo + edge_ix((uint32_t)pp.ar, pp.b, lbm_slot_collo(q), g, N);
+#pragma unroll
+        for (int i = 0; i < N; ++i) d[i] = v[i];
+    }
+    if (cyq == 1 && j == N - 2) {
+        double* d = e.colhi + edge_ix((uint32_t)pp.ar, pp.b, lbm_slot_colhi(q), g, N);
+#pragma unroll
+        for (int i = 0; i < N; ++i) d[i] = v[i];
+    }
+}
+
 // Trapezoid-weighted column sum (global_mass weights, patchgrid.hpp:244-266),
 // with four interleaved partial sums (fixed association: deterministic; the
 // mass is a tolerance-checked diagnostic).
@@ -393,22 +429,36 @@ __device__ __forceinline__ void prefetch_range(const unsigned char* p, unsigned 
 // L2 prefetch of everything the decode of patch p will read: its stored
 // block and the neighbours' edge lines (the ghost-ring sources).
 template <int N>
-__device__ __forceinline__ void prefetch_patch(const StepArgs& a, uint32_t p, const DirEntry e, uint32_t q,
-                                               int tid, int nthreads) {
+__device__ __forceinline__ void prefetch_block(const StepArgs& a, const DirEntry e, int tid, int nthreads) {
     const unsigned long long bytes = (e.flags & DIR_RAW) ? (unsigned long long)N * N * 8
                                                           : 12ull * e.nnz + 4ull * (N + 1);
     if (!(e.flags & DIR_DEAD)) prefetch_range(a.store_in + e.off, bytes, tid, nthreads);
+}
+
+// L2 prefetch of the neighbours' edge lines (all stored components) that
+// the ghost ring of patch p will read.
+template <int N>
+__device__ __forceinline__ void prefetch_edges(const StepArgs& a, uint32_t p, int tid, int nthreads) {
     const PatchPos pp = patch_pos(p, a.g);
-    const int lines = (N * 8 + 127) / 128;
-    const double* srcs[7] = {a.ein.colhi + edge_ix(pp.ar, pp.bl, q, a.g, N),
-                             a.ein.collo + edge_ix(pp.ar, pp.br, q, a.g, N),
-                             a.ein.rowhi + edge_ix(pp.su, pp.b, q, a.g, N),
-                             a.ein.rowlo + edge_ix(pp.sd, pp.b, q, a.g, N),
-                             a.ein.rowhi + edge_ix(pp.su, pp.bl, q, a.g, N),
-                             a.ein.rowlo + edge_ix(pp.sd, pp.br, q, a.g, N),
-                             a.ein.rowhi + edge_ix(pp.su, pp.br, q, a.g, N)};
+    const int lines = (int)((a.g.me * N * 8 + 127) / 128);
+    const double* srcs[7] = {a.ein.colhi + edge_ix(pp.ar, pp.bl, 0, a.g, N),
+                             a.ein.collo + edge_ix(pp.ar, pp.br, 0, a.g, N),
+                             a.ein.rowhi + edge_ix(pp.su, pp.b, 0, a.g, N),
+                             a.ein.rowlo + edge_ix(pp.sd, pp.b, 0, a.g, N),
+                             a.ein.rowhi + edge_ix(pp.su, pp.bl, 0, a.g, N),
+                             a.ein.rowlo + edge_ix(pp.sd, pp.br, 0, a.g, N),
+                             a.ein.rowhi + edge_ix(pp.su, pp.br, 0, a.g, N)};
     for (int k = tid; k < 7 * lines; k += nthreads)
         prefetch_l2(reinterpret_cast<const unsigned char*>(srcs[k / lines]) + (k % lines) * 128);
+}
+
+// L2 prefetch of everything the decode of patch p (single component) reads.
+template <int N>
+__device__ __forceinline__ void prefetch_patch(const StepArgs& a, uint32_t p, const DirEntry e, uint32_t q,
+                                               int tid, int nthreads) {
+    (void)q;
+    prefetch_block<N>(a, e, tid, nthreads);
+    prefetch_edges<N>(a, p, tid, nthreads);
 }
 
 // End of a step, called by every CTA with its partial sums: the last CTA to

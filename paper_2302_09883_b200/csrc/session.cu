@@ -36,6 +36,7 @@ struct KernelSet {
     size_t smem;
     bool persistent;     // D2Q9: grid-stride over patches with per-CTA scratch
     size_t scratch_doubles;  // per CTA
+    bool edges3;         // D2Q9 edge lines hold only the 3 crossing populations
 };
 
 template <int N, int L>
@@ -49,6 +50,7 @@ KernelSet make_lbm_set() {
     k.smem = Lay::smem_bytes();
     k.persistent = true;
     k.scratch_doubles = Lay::scratch_doubles();
+    k.edges3 = true;
     for (auto f : {k.main, k.decode}) {
         WG_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k.smem));
     }
@@ -67,6 +69,7 @@ KernelSet make_set_h() {
     k.smem = Lay::smem_bytes();
     k.persistent = false;
     k.scratch_doubles = 0;
+    k.edges3 = false;
     for (auto f : {k.main, k.decode})
         WG_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k.smem));
     return k;
@@ -83,6 +86,7 @@ KernelSet make_lbm_set_h() {
     k.smem = Lay::smem_bytes();
     k.persistent = true;
     k.scratch_doubles = LbmLayout<N>::scratch_doubles();
+    k.edges3 = false;
     for (auto f : {k.main, k.decode})
         WG_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k.smem));
     return k;
@@ -125,6 +129,7 @@ KernelSet make_set() {
     k.smem = Lay::smem_bytes();
     k.persistent = false;
     k.scratch_doubles = 0;
+    k.edges3 = false;
     for (auto f : {k.main, k.decode}) {
         WG_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k.smem));
     }
@@ -192,14 +197,16 @@ __global__ void k_upload(const double* grid, uint32_t N, ShardGeom g, unsigned c
     for (uint32_t j = 0; j < N; ++j) dst[j] = src[j];
     if (i == 0) dir[(uint64_t)p * g.m + q] = DirEntry{off, 0u, DIR_RAW};
     const uint32_t ar = p / g.P1, b = p % g.P1;
-    const uint64_t own = (((uint64_t)(ar + 1) * g.P1 + b) * g.m + q) * N;
-    const uint64_t oc = (((uint64_t)ar * g.P1 + b) * g.m + q) * N;
-    if (i == 1)
-        for (uint32_t j = 0; j < N; ++j) e.rowlo[own + j] = src[j];
-    if (i == N - 2)
-        for (uint32_t j = 0; j < N; ++j) e.rowhi[own + j] = src[j];
-    e.collo[oc + i] = src[1];
-    e.colhi[oc + i] = src[N - 2];
+    const bool lbm3 = g.me != g.m;  // D2Q9 edges with the 3 crossing populations
+    const int s_rl = lbm3 ? lbm_slot_rowlo((int)q) : (int)q, s_rh = lbm3 ? lbm_slot_rowhi((int)q) : (int)q;
+    const int s_cl = lbm3 ? lbm_slot_collo((int)q) : (int)q, s_ch = lbm3 ? lbm_slot_colhi((int)q) : (int)q;
+    auto ix = [&](uint32_t slot, int c) { return (((uint64_t)slot * g.P1 + b) * g.me + c) * N; };
+    if (i == 1 && s_rl >= 0)
+        for (uint32_t j = 0; j < N; ++j) e.rowlo[ix(ar + 1, s_rl) + j] = src[j];
+    if (i == N - 2 && s_rh >= 0)
+        for (uint32_t j = 0; j < N; ++j) e.rowhi[ix(ar + 1, s_rh) + j] = src[j];
+    if (s_cl >= 0) e.collo[ix(ar, s_cl) + i] = src[1];
+    if (s_ch >= 0) e.colhi[ix(ar, s_ch) + i] = src[N - 2];
 }
 
 }  // namespace
@@ -306,7 +313,7 @@ struct Session {
         return p;
     }
 
-    uint64_t halo_doubles() const { return (uint64_t)sg.P1 * sg.m * N; }
+    uint64_t halo_doubles() const { return (uint64_t)sg.P1 * sg.me * N; }
 
     void create(const wg_run_config& c, const wg_shard* sh, void* strm) {
         cfg = c;
@@ -346,6 +353,7 @@ struct Session {
         sg.world = shard.world;
         sg.npatch = sg.R * sg.P1;
         ks = select_kernels(cfg.scheme, N, levels);
+        sg.me = ks.edges3 ? 3u : sg.m;
         {
             int per_sm = 0, sms = 0;
             WG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ks.main, ks.threads, ks.smem));
@@ -374,8 +382,8 @@ struct Session {
         for (int k = 0; k < 2; ++k) {
             store[k] = dalloc<unsigned char>(cap);
             dir[k] = dalloc<DirEntry>(blocks);
-            const uint64_t rowline = (uint64_t)(sg.R + 2) * sg.P1 * sg.m * N;
-            const uint64_t colline = (uint64_t)sg.R * sg.P1 * sg.m * N;
+            const uint64_t rowline = (uint64_t)(sg.R + 2) * sg.P1 * sg.me * N;
+            const uint64_t colline = (uint64_t)sg.R * sg.P1 * sg.me * N;
             edge_mem[k] = dalloc<double>(2 * rowline + 2 * colline);
             WG_CUDA(cudaMemsetAsync(edge_mem[k], 0, (2 * rowline + 2 * colline) * sizeof(double), stream));
             edges[k].rowlo = edge_mem[k];

@@ -43,7 +43,21 @@ struct ShardGeom {
     uint32_t m;       // components
     int world;        // 1: periodic wrap is local
     uint32_t npatch;  // R * P1
+    uint32_t me;      // components stored per edge line (D2Q9: the 3 crossing that side)
 };
+
+// D2Q9 edge lines carry only the populations a neighbour pulls across that
+// side (pull streaming f_q(x) <- f_q(x - c_q) reads ghost row 0 only for
+// c_x = +1, row N+1 for c_x = -1, column 0 for c_y = +1, column N+1 for
+// c_y = -1).  Slot of population q in each line, -1 if not stored.
+//   rowlo (logical row 1, read as the upper neighbour's ghost row N+1): q in {2,6,8}
+//   rowhi (logical row n-2, the lower neighbour's ghost row 0):         q in {1,5,7}
+//   collo (logical column 1, the left neighbour's ghost column N+1):    q in {4,6,7}
+//   colhi (logical column n-2, the right neighbour's ghost column 0):   q in {3,5,8}
+__host__ __device__ constexpr int lbm_slot_rowlo(int q) { return q == 2 ? 0 : q == 6 ? 1 : q == 8 ? 2 : -1; }
+__host__ __device__ constexpr int lbm_slot_rowhi(int q) { return q == 1 ? 0 : q == 5 ? 1 : q == 7 ? 2 : -1; }
+__host__ __device__ constexpr int lbm_slot_collo(int q) { return q == 4 ? 0 : q == 6 ? 1 : q == 7 ? 2 : -1; }
+__host__ __device__ constexpr int lbm_slot_colhi(int q) { return q == 3 ? 0 : q == 5 ? 1 : q == 8 ? 2 : -1; }
 
 __host__ __device__ inline uint64_t round16(uint64_t b) { return (b + 15) & ~uint64_t(15); }
 
