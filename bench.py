@@ -42,13 +42,22 @@ METRIC = "MLUPS (cell-updates/s) w/ compression @1/2/4/8 B200; HBM roofline %; c
 
 WORKLOADS = {
     # BASELINE.json configs[1] (C2)
-    "lbm_c2": dict(scheme="lbm", nx=1025, splits=(16, 16), levels=4, c=1e-3, mode="capped"),
+    "lbm_c2": dict(scheme="lbm", components=9, nx=1025, splits=(16, 16), levels=4, c=1e-3, mode="capped"),
     # BASELINE.json configs[0] (C1): the reference's own CPU-runnable case
-    "transport_c1": dict(scheme="transport", nx=257, splits=(8, 8), levels=4, c=1e-3, mode="capped"),
+    "transport_c1": dict(scheme="transport", components=1, nx=257, splits=(8, 8), levels=4, c=1e-3, mode="capped"),
+    # BASELINE.json configs[3] (C4): 16384^2 D2Q9 on one GPU; the raw f-field
+    # (19.9 GB) exceeds the 8 GiB store budget, so the initial state is
+    # generated and compressed on the device
+    "lbm_c4": dict(scheme="lbm", components=9, nx=16385, splits=(256, 256), levels=4, c=1e-3, mode="capped",
+                   budget=8 << 30, device_init=True),
+    # BASELINE.json configs[4] (C5): 65536^2 D2Q9 (319 GB raw), sharded by patch
+    # rows over the ranks; fits ONE B200 compressed
+    "lbm_c5": dict(scheme="lbm", components=9, nx=65537, splits=(1024, 1024), levels=4, c=1e-3, mode="capped",
+                   budget=24 << 30, device_init=True),
     # C3-sized transport grid in 32^2-cell patches (C1 patch shape)
-    "transport_4k_p33": dict(scheme="transport", nx=4097, splits=(128, 128), levels=4, c=1e-3, mode="capped"),
+    "transport_4k_p33": dict(scheme="transport", components=1, nx=4097, splits=(128, 128), levels=4, c=1e-3, mode="capped"),
     # C3-sized transport grid (4096^2 cells, 64^2-cell patches)
-    "transport_4k": dict(scheme="transport", nx=4097, splits=(64, 64), levels=4, c=1e-3, mode="capped"),
+    "transport_4k": dict(scheme="transport", components=1, nx=4097, splits=(64, 64), levels=4, c=1e-3, mode="capped"),
 }
 
 B_ALG = {"transport": 16, "swe": 48, "lbm": 144}  # bytes per cell-update, SURVEY §8d
@@ -59,6 +68,7 @@ def run_config(w: dict, steps: int) -> api.RunConfig:
                         spec=api.ThresholdSpec(w["mode"], w["c"]), compute_l2=False, lbm_steps=steps)
     if w["scheme"] == "transport":
         cfg.t_end = steps * cfg.cfl * (1.0 / (w["nx"] - 1)) / max(cfg.alpha, cfg.beta)
+    cfg.store_budget_bytes = w.get("budget", 0)
     return cfg
 
 
@@ -150,7 +160,11 @@ def cpu_lib():
 
 def cpu_run(w: dict, steps: int, threads: int):
     """Time the CPU implementation on `steps` steps of the workload; returns
-    (MLUPS, seconds, kind, cores, rows)."""
+    (MLUPS, seconds, kind, cores, rows).  C4/C5 do not fit the host (their raw
+    state is 20 / 319 GB): their CPU rate is measured on the C2 grid
+    ("report the CPU MLUPS at C2/C3 sizes as the rate")."""
+    if w.get("device_init"):
+        w = WORKLOADS["lbm_c2"]
     lib, kind = cpu_lib()
     cfg = run_config(w, steps)
     cfg.threads = threads if kind == "reference" else 1
@@ -219,18 +233,25 @@ def bench_b200(args, w: dict):
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
 
-    # initial state on the host (glibc libm, bit-identical to the reference IC)
-    full = api.initial_state(cfg, lib=lib)
-    own = np.ascontiguousarray(full.data[rb * w["splits"][1]: re_ * w["splits"][1]])
-    pinned = torch.empty(own.size, dtype=torch.float64, pin_memory=True)
-    host = pinned.numpy()
-    host[:] = own.reshape(-1)
-    del full
+    device_init = w.get("device_init", False)
+    if device_init:
+        host = None  # raw state larger than the budget: generated + compressed on the device
+    else:
+        # initial state on the host (glibc libm, bit-identical to the reference IC)
+        full = api.initial_state(cfg, lib=lib)
+        own = np.ascontiguousarray(full.data[rb * w["splits"][1]: re_ * w["splits"][1]])
+        pinned = torch.empty(own.size, dtype=torch.float64, pin_memory=True)
+        host = pinned.numpy()
+        host[:] = own.reshape(-1)
+        del full
 
     sess = ShardedSession(lib, cfg, shard, stream.cuda_stream, dist if world > 1 else None)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{local}")
     try:
-        sess.upload(host)
+        if device_init:
+            sess.init_device()
+        else:
+            sess.upload(host)
         evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
         with ClockSampler(local) as clocks:
             # warm-up: at least W steps, continued until the clock sampler is
@@ -264,6 +285,8 @@ def bench_b200(args, w: dict):
         lib.check(lib.wg_session_profile(sess.handle, 0))
         rows = sess.rows()
         info = sess.info
+        free_b, total_b = torch.cuda.mem_get_info(local)
+        mem_used = total_b - free_b
         if world > 1:
             t = torch.tensor([tot_ms, main_ms.value], dtype=torch.float64, device=f"cuda:{local}")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -304,6 +327,8 @@ def bench_b200(args, w: dict):
         "gpu_launches": args.steps,  # one fused kernel launch per step (k_*_step<STEP>)
         "clocks": clocks.summary(),
         "device_bytes": info.device_bytes,
+        "device_mem_used_bytes": mem_used,
+        "raw_state_bytes": 8 * w["components"] * (w["nx"] - 1) ** 2 if "components" in w else None,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         # bounded sample: calibrate on a few steps, then about 12 s of CPU work
@@ -332,7 +357,10 @@ def e2e_run(lib, cfg, shard, stream, host, args, dt, dist):
             dist.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        sess.upload(host)
+        if host is None:
+            sess.init_device()
+        else:
+            sess.upload(host)
         for _ in range(args.steps):
             sess.step(dt)
             sess.last_row()
@@ -345,6 +373,11 @@ def e2e_run(lib, cfg, shard, stream, host, args, dt, dist):
     finally:
         sess.close()
     cells = (cfg.nx - 1) ** 2
+    if host is None:
+        return {"value": cells * args.steps / secs / 1e6, "unit": "MLUPS", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": C.sizeof(abi.MetricsRowC),
+                "note": "initial state generated and compressed on the device inside the timed region; "
+                        "one metrics row read back per step"}
     return {"value": cells * args.steps / secs / 1e6, "unit": "MLUPS",
             "h2d_bytes_per_step": host.nbytes / args.steps, "d2h_bytes_per_step": C.sizeof(abi.MetricsRowC),
             "note": "initial state uploaded once inside the timed region (bytes amortised per step); "

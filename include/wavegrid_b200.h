@@ -246,6 +246,13 @@ wg_status wg_session_upload(wg_session* s, const double* host_grid);
 /* Same from a device grid buffer (async on the session stream). */
 wg_status wg_dev_session_upload(wg_session* s, const double* dev_grid);
 
+/* Generate the initial state of cfg ON THE DEVICE and store it through the
+ * compression cycle (for grids whose raw state does not fit the store
+ * budget, C4/C5).  Unlike wg_session_upload the first step then starts from
+ * the compressed initial state, and the device libm (tanh/sin) is not
+ * bit-identical to the host's: results are not pinned to run().  D2Q9. */
+wg_status wg_session_init_device(wg_session* s);
+
 /* Advance one step with time step dt (ignored for LBM).  After it returns
  * (asynchronously), the halo send blocks of the next step are ready. */
 wg_status wg_session_step(wg_session* s, double dt);

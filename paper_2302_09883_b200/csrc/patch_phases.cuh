@@ -70,10 +70,11 @@ struct StepArgs {
     uint64_t dense_bytes;     // CompressedPatch::dense_bytes summed over the shard
     double smax[4], smin[4], r;                          // transport faces, dt/dx
     double omega;                                        // D2Q9: 1/tau
+    double ic_u0, ic_kappa, ic_delta, ic_inv;            // MODE_INIT: shear layer, 1/(nx-1)
     double thr[(kMaxLevels + 1) * (kMaxLevels + 1)];     // T[band_i][band_j]
 };
 
-enum { MODE_STEP = 0, MODE_DECODE = 2 };
+enum { MODE_STEP = 0, MODE_INIT = 1, MODE_DECODE = 2 };
 
 struct PatchPos {
     int ar;       // local patch row

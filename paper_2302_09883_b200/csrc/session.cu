@@ -31,6 +31,7 @@ namespace {
 struct KernelSet {
     void (*main)(StepArgs);
     void (*decode)(StepArgs);
+    void (*init)(StepArgs);  // device-generated, compressed initial state (D2Q9); may be null
     int P;               // patches per CTA (non-persistent kernels)
     int threads;
     size_t smem;
@@ -45,13 +46,14 @@ KernelSet make_lbm_set() {
     KernelSet k;
     k.main = k_lbm_step<N, L, MODE_STEP>;
     k.decode = k_lbm_step<N, L, MODE_DECODE>;
+    k.init = k_lbm_step<N, L, MODE_INIT>;
     k.P = 1;
     k.threads = Lay::NT;
     k.smem = Lay::smem_bytes();
     k.persistent = true;
     k.scratch_doubles = Lay::scratch_doubles();
     k.edges3 = true;
-    for (auto f : {k.main, k.decode}) {
+    for (auto f : {k.main, k.decode, k.init}) {
         WG_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k.smem));
     }
     return k;
@@ -64,6 +66,7 @@ KernelSet make_set_h() {
     KernelSet k;
     k.main = k_patch_step_h<N, L, P, MODE_STEP>;
     k.decode = k_patch_step_h<N, L, P, MODE_DECODE>;
+    k.init = nullptr;
     k.P = P;
     k.threads = Lay::NT;
     k.smem = Lay::smem_bytes();
@@ -81,6 +84,7 @@ KernelSet make_lbm_set_h() {
     KernelSet k;
     k.main = k_lbm_step_h<N, L, MODE_STEP>;
     k.decode = k_lbm_step_h<N, L, MODE_DECODE>;
+    k.init = nullptr;
     k.P = 1;
     k.threads = Lay::NT;
     k.smem = Lay::smem_bytes();
@@ -124,6 +128,7 @@ KernelSet make_set() {
     KernelSet k;
     k.main = k_patch_step<N, L, P, MODE_STEP>;
     k.decode = k_patch_step<N, L, P, MODE_DECODE>;
+    k.init = nullptr;
     k.P = P;
     k.threads = Lay::NT;
     k.smem = Lay::smem_bytes();
@@ -352,6 +357,7 @@ struct Session {
         sg.m = geo.m;
         sg.world = shard.world;
         sg.npatch = sg.R * sg.P1;
+        sg.row0 = (uint32_t)shard.row_begin;
         ks = select_kernels(cfg.scheme, N, levels);
         sg.me = ks.edges3 ? 3u : sg.m;
         {
@@ -445,6 +451,29 @@ struct Session {
         DevBuf<double> d(n);
         WG_CUDA(cudaMemcpyAsync(d.p, hgrid, n * sizeof(double), cudaMemcpyHostToDevice, stream));
         upload_dev(d.p);
+    }
+
+    // Initial state generated and compressed on the device (no host grid):
+    // the compression cycle of a step applied to the initial state.
+    void init_device() {
+        if (!ks.init) raise(WG_INVALID_ARGUMENT, "device initial state: D2Q9 full-line kernels only");
+        cur = 1;  // the kernel writes pool 0 (dst = 1 - cur)
+        WG_CUDA(cudaMemsetAsync(bump, 0, 2 * sizeof(unsigned long long), stream));
+        StepArgs a = step_args(1, 0);
+        a.omega = 1.0 / cfg.lbm_tau;
+        a.ic_u0 = cfg.lbm_u0;
+        a.ic_kappa = cfg.lbm_kappa;
+        a.ic_delta = cfg.lbm_delta;
+        a.ic_inv = 1.0 / static_cast<double>(cfg.nx - 1);
+        grow_rows(1);
+        a.row_out = rows;  // the IC's metrics row is scratch (step counter stays 0)
+        a.mass_fv_out = mass_fv;
+        ks.init<<<grid, ks.threads, ks.smem, stream>>>(a);
+        WG_LAUNCH_CHECK("device initial state");
+        cur = 0;
+        step = 0;
+        time = 0.0;
+        sync();
     }
 
     StepArgs step_args(int src, int dst) const {
@@ -583,6 +612,10 @@ wg_status wg_session_upload(wg_session* s, const double* host_grid) {
 
 wg_status wg_dev_session_upload(wg_session* s, const double* dev_grid) {
     return guard([&] { reinterpret_cast<Session*>(s)->upload_dev(dev_grid); });
+}
+
+wg_status wg_session_init_device(wg_session* s) {
+    return guard([&] { reinterpret_cast<Session*>(s)->init_device(); });
 }
 
 wg_status wg_session_step(wg_session* s, double dt) {

@@ -44,6 +44,7 @@ struct ShardGeom {
     int world;        // 1: periodic wrap is local
     uint32_t npatch;  // R * P1
     uint32_t me;      // components stored per edge line (D2Q9: the 3 crossing that side)
+    uint32_t row0;    // global index of the first owned patch row
 };
 
 // D2Q9 edge lines carry only the populations a neighbour pulls across that

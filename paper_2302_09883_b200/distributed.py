@@ -115,6 +115,17 @@ class ShardedSession:
 
     def upload(self, host_grid: np.ndarray):
         self.lib.check(self.lib.wg_session_upload(self.handle, abi.dptr(host_grid)))
+        self._exchange()
+
+    def init_device(self):
+        """Initial state generated and compressed on the device (C4/C5)."""
+        self.lib.check(self.lib.wg_session_init_device(self.handle))
+        self._exchange()
+
+    def _exchange(self):
+        if self.shard.world > 1:
+            s_lo, s_hi, r_lo, r_hi = self.halo_tensors()
+            exchange_halos(s_lo, s_hi, r_lo, r_hi, self.shard.rank, self.shard.world, self.dist)
 
     def halo_tensors(self):
         import torch
@@ -126,10 +137,7 @@ class ShardedSession:
 
     def step(self, dt: float = 1.0):
         self.lib.check(self.lib.wg_session_step(self.handle, dt))
-        if self.shard.world > 1:
-            # the halo blocks move with the double buffer: re-fetch every step
-            s_lo, s_hi, r_lo, r_hi = self.halo_tensors()
-            exchange_halos(s_lo, s_hi, r_lo, r_hi, self.shard.rank, self.shard.world, self.dist)
+        self._exchange()  # the halo blocks move with the double buffer: re-fetched every step
 
     def sync(self):
         self.lib.check(self.lib.wg_session_sync(self.handle))

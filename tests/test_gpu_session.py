@@ -216,3 +216,29 @@ def test_lbm_mass_conserved(product):
     r = api.run(lbm_cfg(129, (2, 2), 4, 1e-3, 30), lib=product)
     m0 = r.rows[0]["global_mass"]
     assert all(abs(x["global_mass"] - m0) <= 1e-12 * abs(m0) for x in r.rows)
+
+
+def test_lbm_device_initial_state(product, oracle):
+    """wg_session_init_device: the shear-layer IC generated and compressed on
+    the device (C4/C5 path) — close to the host IC (compression error and
+    device libm), same mass, and it steps."""
+    cfg = lbm_cfg(129, (4, 4), 4, 1e-4, 3)
+    s = _session(product, cfg)
+    try:
+        product.check(product.wg_session_init_device(s))
+        g = api.PatchGrid((129, 129), (4, 4), 9, True)
+        product.check(product.wg_session_download(s, abi.dptr(g.data)))
+        ic = api.initial_state(cfg, lib=oracle)
+        diff = np.max(np.abs(g.logical_view() - ic.logical_view()))
+        assert diff < 2e-3, diff
+        m_dev = sum(api.global_mass(g, q, lib=oracle) for q in range(9))
+        m_ic = sum(api.global_mass(ic, q, lib=oracle) for q in range(9))
+        assert abs(m_dev - m_ic) <= 1e-12 * m_ic
+        for _ in range(3):
+            product.check(product.wg_session_step(s, 1.0))
+        rows = (abi.MetricsRowC * 3)()
+        n = abi.u64()
+        product.check(product.wg_session_metrics(s, rows, 3, C.byref(n)))
+        assert n.value == 3 and all(abs(r.global_mass - m_ic) <= 1e-11 * m_ic for r in rows)
+    finally:
+        product.wg_session_destroy(s)
