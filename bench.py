@@ -42,18 +42,19 @@ METRIC = "MLUPS (cell-updates/s) w/ compression @1/2/4/8 B200; HBM roofline %; c
 
 WORKLOADS = {
     # BASELINE.json configs[1] (C2)
-    "lbm_c2": dict(scheme="lbm", components=9, nx=1025, splits=(16, 16), levels=4, c=1e-3, mode="capped"),
+    "lbm_c2": dict(scheme="lbm", components=9, nx=1025, splits=(16, 16), levels=4, c=1e-3, mode="capped",
+                   scaling="weak"),
     # BASELINE.json configs[0] (C1): the reference's own CPU-runnable case
     "transport_c1": dict(scheme="transport", components=1, nx=257, splits=(8, 8), levels=4, c=1e-3, mode="capped"),
     # BASELINE.json configs[3] (C4): 16384^2 D2Q9 on one GPU; the raw f-field
     # (19.9 GB) exceeds the 8 GiB store budget, so the initial state is
     # generated and compressed on the device
     "lbm_c4": dict(scheme="lbm", components=9, nx=16385, splits=(256, 256), levels=4, c=1e-3, mode="capped",
-                   budget=8 << 30, device_init=True),
+                   budget=8 << 30, device_init=True, scaling="strong"),
     # BASELINE.json configs[4] (C5): 65536^2 D2Q9 (319 GB raw), sharded by patch
     # rows over the ranks; fits ONE B200 compressed
     "lbm_c5": dict(scheme="lbm", components=9, nx=65537, splits=(1024, 1024), levels=4, c=1e-3, mode="capped",
-                   budget=24 << 30, device_init=True),
+                   budget=24 << 30, device_init=True, scaling="strong"),
     # C3-sized transport grid in 32^2-cell patches (C1 patch shape)
     "transport_4k_p33": dict(scheme="transport", components=1, nx=4097, splits=(128, 128), levels=4, c=1e-3, mode="capped"),
     # C3-sized transport grid (4096^2 cells, 64^2-cell patches)
@@ -204,7 +205,10 @@ def config_json(args, w):
     return {"workload": args.workload, "scheme": w["scheme"], "grid_cells": f"{w['nx'] - 1}x{w['nx'] - 1}",
             "patch_points": f"{n}x{n}", "patches": w["splits"][0] * w["splits"][1], "levels": w["levels"],
             "threshold": f"{w['mode']} c={w['c']}", "codec": "csr",
-            "parallelism": f"patch-row shards x{args.gpus}", "l2": "flushed between timed steps (256 MiB write)"}
+            "parallelism": f"patch-row shards x{args.gpus}"
+                           + (" (weak: one periodic copy of the grid per rank)" if w.get("scaling", "weak") == "weak" else
+                              " (strong: the grid split over the ranks)"),
+            "l2": "flushed between timed steps (256 MiB write)"}
 
 
 # ---- the B200 arm ----------------------------------------------------------------
@@ -225,7 +229,12 @@ def bench_b200(args, w: dict):
     lib = abi.load_product()
     cfg = run_config(w, args.warmup + args.steps)
     dt = transport_dt(cfg) if w["scheme"] == "transport" else 1.0
-    P0 = w["splits"][0]
+    weak = w.get("scaling", "weak") == "weak"
+    if weak:
+        # weak scaling: the square problem replicated periodically along dim 0,
+        # one copy per rank (identical work per rank; the halo exchange is real)
+        cfg.tile_rows = world
+    P0 = w["splits"][0] * (world if weak else 1)
     rb, re_ = shard_rows(P0, rank, world)
     shard = ShardInfo(rank, world, rb, re_, local)
     # a dedicated (non-default) stream: the session launches on it and the
@@ -237,9 +246,14 @@ def bench_b200(args, w: dict):
     if device_init:
         host = None  # raw state larger than the budget: generated + compressed on the device
     else:
-        # initial state on the host (glibc libm, bit-identical to the reference IC)
-        full = api.initial_state(cfg, lib=lib)
-        own = np.ascontiguousarray(full.data[rb * w["splits"][1]: re_ * w["splits"][1]])
+        # initial state on the host (glibc libm, bit-identical to the reference IC);
+        # with weak scaling every rank's rows are one copy of the square grid
+        square = run_config(w, 1)
+        full = api.initial_state(square, lib=lib)
+        if weak:
+            own = full.data
+        else:
+            own = np.ascontiguousarray(full.data[rb * w["splits"][1]: re_ * w["splits"][1]])
         pinned = torch.empty(own.size, dtype=torch.float64, pin_memory=True)
         host = pinned.numpy()
         host[:] = own.reshape(-1)
@@ -297,11 +311,12 @@ def bench_b200(args, w: dict):
         sess.close()
 
         # ---- end to end through the public API with host buffers -------------
-        e2e = e2e_run(lib, cfg, shard, stream, host, args, dt, dist if world > 1 else None)
+        e2e = e2e_run(lib, cfg, shard, stream, host, args, dt, dist if world > 1 else None,
+                      world if weak else 1)
     finally:
         sess.close()
 
-    cells_global = (w["nx"] - 1) ** 2
+    cells_global = (w["nx"] - 1) ** 2 * (world if weak else 1)
     value = cells_global * args.steps / (tot_ms * 1e-3) / 1e6
     pk = peaks()
     cells_local = info.cells_per_step
@@ -311,7 +326,7 @@ def bench_b200(args, w: dict):
     line = {
         "metric": METRIC, "value": value, "unit": "MLUPS", "n_gpus": world, "steps": args.steps,
         "warmup": warm_steps, "ms_per_step": tot_ms / args.steps, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "scaling": "weak" if weak else "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (shear-layer D2Q9 initial state)" if w["scheme"] == "lbm" else "synthetic (reference initial state)",
         "config": config_json(args, w),
         "compression_ratio": statistics.fmean(r["ratio"] for r in timed_rows),
@@ -343,7 +358,7 @@ def bench_b200(args, w: dict):
         dist.destroy_process_group()
 
 
-def e2e_run(lib, cfg, shard, stream, host, args, dt, dist):
+def e2e_run(lib, cfg, shard, stream, host, args, dt, dist, copies=1):
     """Same metric through the public API: the host state is uploaded from
     pinned memory inside the timed region and every step's metrics row is
     read back to the host."""
@@ -372,7 +387,7 @@ def e2e_run(lib, cfg, shard, stream, host, args, dt, dist):
             secs = t.item()
     finally:
         sess.close()
-    cells = (cfg.nx - 1) ** 2
+    cells = (cfg.nx - 1) ** 2 * copies
     if host is None:
         return {"value": cells * args.steps / secs / 1e6, "unit": "MLUPS", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": C.sizeof(abi.MetricsRowC),

@@ -164,6 +164,10 @@ typedef struct wg_run_config { /* RunConfig + SimConfig, pipeline.hpp:23-38, sol
     double lbm_tau, lbm_u0, lbm_kappa, lbm_delta;
     /* compressed-store budget in bytes for the device session (0 = auto)   */
     uint64_t store_budget_bytes;
+    /* device session only: the square grid replicated `tile_rows` times
+     * along dim 0 (periodic copies, identical initial state in each; 0 or 1
+     * = the reference's grid).  Weak scaling: one copy per rank.            */
+    uint64_t tile_rows;
 } wg_run_config;
 
 typedef struct wg_metrics_row { /* MetricsRow, pipeline.hpp:40-50 */

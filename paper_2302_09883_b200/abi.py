@@ -130,6 +130,7 @@ class RunConfigC(C.Structure):
         ("lbm_kappa", f64),
         ("lbm_delta", f64),
         ("store_budget_bytes", u64),
+        ("tile_rows", u64),
     ]
 
 

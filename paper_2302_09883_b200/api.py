@@ -246,6 +246,7 @@ class RunConfig:
     lbm_kappa: float = 80.0
     lbm_delta: float = 0.05
     store_budget_bytes: int = 0
+    tile_rows: int = 1
 
     def to_c(self) -> abi.RunConfigC:
         c = abi.RunConfigC()
@@ -265,6 +266,7 @@ class RunConfig:
         c.lbm_steps = self.lbm_steps
         c.lbm_tau, c.lbm_u0, c.lbm_kappa, c.lbm_delta = self.lbm_tau, self.lbm_u0, self.lbm_kappa, self.lbm_delta
         c.store_budget_bytes = self.store_budget_bytes
+        c.tile_rows = self.tile_rows
         return c
 
     @property

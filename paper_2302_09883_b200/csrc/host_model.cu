@@ -85,6 +85,7 @@ double sim_dx(const wg_run_config& c) { return c.domain_length / static_cast<dou
 RunGeometry run_geometry(const wg_run_config& c) {
     RunGeometry g;
     g.m = scheme_components(c.scheme);
+    g.tiles = c.tile_rows > 1 ? c.tile_rows : 1;
     for (int d = 0; d < 2; ++d) {
         const uint64_t G = c.nx, P = c.splits[d];
         if (P == 0 || G < 2 || (G - 1) % P != 0)
@@ -95,6 +96,7 @@ RunGeometry run_geometry(const wg_run_config& c) {
         g.splits[d] = P;
         g.n[d] = n;
     }
+    g.splits[0] *= g.tiles;  // periodic copies stacked along dim 0
     g.npatch = g.splits[0] * g.splits[1];
     g.tcount = (g.n[0] + 2) * (g.n[1] + 2);
     return g;
@@ -149,7 +151,10 @@ void initial_state(const wg_run_config& c, uint64_t row_begin, uint64_t row_end,
             double* base = buf + p * g.m * g.tcount;
             for (uint64_t i = 1; i <= n0; ++i)
                 for (uint64_t j = 1; j <= n1; ++j) {
-                    const uint64_t gi = a * (n0 - 1) + i - 1, gj = b * (n1 - 1) + j - 1;
+                    // tiled grids repeat the square problem along dim 0 (the
+                    // reference's own grid, tiles == 1, is evaluated unreduced)
+                    const uint64_t graw = a * (n0 - 1) + i - 1;
+                    const uint64_t gi = g.tiles > 1 ? graw % (c.nx - 1) : graw, gj = b * (n1 - 1) + j - 1;
                     const uint64_t off = i * ty + j;
                     if (c.scheme == WG_SCHEME_TRANSPORT) {
                         base[off] = exact_transport_at(c, 0.0, gi, gj);

@@ -14,6 +14,7 @@ struct RunGeometry {
     uint64_t n[2] = {0, 0};  // logical points per patch side
     uint64_t npatch = 0;
     uint64_t tcount = 0;     // true cells per component (n+2)^2
+    uint64_t tiles = 1;      // periodic copies along dim 0 (wg_run_config::tile_rows)
 };
 
 bool valid_signal_length(uint64_t n);

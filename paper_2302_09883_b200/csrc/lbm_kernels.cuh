@@ -157,7 +157,7 @@ __global__ void __launch_bounds__(LbmLayout<N>::NT) k_lbm_step(const __grid_cons
             const int N1 = N - 1;
             for (int c = t; c < NN; c += Lay::NT) {
                 const int i = c / N, jj = c - (c / N) * N;
-                const uint64_t gi = (uint64_t)(g.row0 + pp.ar) * N1 + i, gj = (uint64_t)pp.b * N1 + jj;
+                const uint64_t gi = ((uint64_t)(g.row0 + pp.ar) * N1 + i) % a.ic_period, gj = (uint64_t)pp.b * N1 + jj;
                 const double X = (double)gi * a.ic_inv, Y = (double)gj * a.ic_inv;
                 const double uy = X <= 0.5 ? a.ic_u0 * tanh(a.ic_kappa * (X - 0.25)) : a.ic_u0 * tanh(a.ic_kappa * (0.75 - X));
                 const double ux = a.ic_delta * a.ic_u0 * sin(2.0 * 3.141592653589793 * (Y + 0.25));

@@ -71,6 +71,7 @@ struct StepArgs {
     double smax[4], smin[4], r;                          // transport faces, dt/dx
     double omega;                                        // D2Q9: 1/tau
     double ic_u0, ic_kappa, ic_delta, ic_inv;            // MODE_INIT: shear layer, 1/(nx-1)
+    uint64_t ic_period;                                  // MODE_INIT: nx-1 (tiled grids repeat)
     double thr[(kMaxLevels + 1) * (kMaxLevels + 1)];     // T[band_i][band_j]
 };
 

@@ -185,33 +185,31 @@ KernelSet select_kernels(int scheme, uint64_t n, int levels) {
 }
 
 // ---- upload: raw store + edge lines from a grid buffer (one thread per
-// (patch, component, row)) ----------------------------------------------------
-__global__ void k_upload(const double* grid, uint32_t N, ShardGeom g, unsigned char* store,
-                         DirEntry* dir, EdgeSet e) {
+// logical element: consecutive threads read consecutive addresses, which
+// matters when the source is page-locked host memory read over the bus) ----
+__global__ void k_upload(const double* grid, uint32_t N, ShardGeom g, unsigned char* store, DirEntry* dir,
+                         EdgeSet e) {
     const uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-    const uint64_t per = (uint64_t)g.m * N;
-    if (t >= (uint64_t)g.npatch * per) return;
-    const uint32_t p = (uint32_t)(t / per);
-    const uint32_t q = (uint32_t)((t % per) / N);
-    const uint32_t i = (uint32_t)(t % N);
+    const uint64_t per = (uint64_t)N * N;
+    if (t >= (uint64_t)g.npatch * g.m * per) return;
+    const uint64_t pq = t / per;  // patch * m + q
+    const uint32_t i = (uint32_t)((t % per) / N), j = (uint32_t)(t % N);
+    const uint32_t p = (uint32_t)(pq / g.m), q = (uint32_t)(pq % g.m);
     const uint64_t TP = N + 2, tcount = TP * TP;
-    const uint64_t block = round16((uint64_t)N * N * 8);
-    const uint64_t off = ((uint64_t)p * g.m + q) * block;
-    const double* src = grid + ((uint64_t)p * g.m + q) * tcount + (i + 1) * TP + 1;
-    double* dst = reinterpret_cast<double*>(store + off) + (uint64_t)i * N;
-    for (uint32_t j = 0; j < N; ++j) dst[j] = src[j];
-    if (i == 0) dir[(uint64_t)p * g.m + q] = DirEntry{off, 0u, DIR_RAW};
+    const uint64_t block = round16(per * 8);
+    const uint64_t off = pq * block;
+    const double x = grid[pq * tcount + (i + 1) * TP + j + 1];
+    reinterpret_cast<double*>(store + off)[(uint64_t)i * N + j] = x;
+    if (i == 0 && j == 0) dir[pq] = DirEntry{off, 0u, DIR_RAW};
     const uint32_t ar = p / g.P1, b = p % g.P1;
     const bool lbm3 = g.me != g.m;  // D2Q9 edges with the 3 crossing populations
     const int s_rl = lbm3 ? lbm_slot_rowlo((int)q) : (int)q, s_rh = lbm3 ? lbm_slot_rowhi((int)q) : (int)q;
     const int s_cl = lbm3 ? lbm_slot_collo((int)q) : (int)q, s_ch = lbm3 ? lbm_slot_colhi((int)q) : (int)q;
     auto ix = [&](uint32_t slot, int c) { return (((uint64_t)slot * g.P1 + b) * g.me + c) * N; };
-    if (i == 1 && s_rl >= 0)
-        for (uint32_t j = 0; j < N; ++j) e.rowlo[ix(ar + 1, s_rl) + j] = src[j];
-    if (i == N - 2 && s_rh >= 0)
-        for (uint32_t j = 0; j < N; ++j) e.rowhi[ix(ar + 1, s_rh) + j] = src[j];
-    if (s_cl >= 0) e.collo[ix(ar, s_cl) + i] = src[1];
-    if (s_ch >= 0) e.colhi[ix(ar, s_ch) + i] = src[N - 2];
+    if (i == 1 && s_rl >= 0) e.rowlo[ix(ar + 1, s_rl) + j] = x;
+    if (i == N - 2 && s_rh >= 0) e.rowhi[ix(ar + 1, s_rh) + j] = x;
+    if (j == 1 && s_cl >= 0) e.collo[ix(ar, s_cl) + i] = x;
+    if (j == N - 2 && s_ch >= 0) e.colhi[ix(ar, s_ch) + i] = x;
 }
 
 }  // namespace
@@ -434,8 +432,8 @@ struct Session {
         if (need > cap)
             raise(WG_OUT_OF_MEMORY, "initial state does not fit the compressed-store budget");
         cur = 0;
-        const uint64_t threads = (uint64_t)sg.npatch * sg.m * N;
-        k_upload<<<(unsigned)((threads + 127) / 128), 128, 0, stream>>>(dgrid, N, sg, store[cur], dir[cur],
+        const uint64_t threads = (uint64_t)sg.npatch * sg.m * N * N;
+        k_upload<<<(unsigned)((threads + 255) / 256), 256, 0, stream>>>(dgrid, N, sg, store[cur], dir[cur],
                                                                          edges[cur]);
         WG_LAUNCH_CHECK("upload");
         const unsigned long long used = need;
@@ -447,6 +445,15 @@ struct Session {
     }
 
     void upload_host(const double* hgrid) {
+        // page-locked host memory is read by the upload kernel directly over
+        // the bus (UVA, no staging copy); pageable memory is staged
+        cudaPointerAttributes at{};
+        if (cudaPointerGetAttributes(&at, hgrid) == cudaSuccess && at.type == cudaMemoryTypeHost &&
+            at.devicePointer) {
+            upload_dev(static_cast<const double*>(at.devicePointer));
+            return;
+        }
+        cudaGetLastError();  // clear a failed attribute query on pageable memory
         const uint64_t n = (uint64_t)sg.npatch * sg.m * geo.tcount;
         DevBuf<double> d(n);
         WG_CUDA(cudaMemcpyAsync(d.p, hgrid, n * sizeof(double), cudaMemcpyHostToDevice, stream));
@@ -465,6 +472,7 @@ struct Session {
         a.ic_kappa = cfg.lbm_kappa;
         a.ic_delta = cfg.lbm_delta;
         a.ic_inv = 1.0 / static_cast<double>(cfg.nx - 1);
+        a.ic_period = geo.tiles > 1 ? cfg.nx - 1 : ~0ull;
         grow_rows(1);
         a.row_out = rows;  // the IC's metrics row is scratch (step counter stays 0)
         a.mass_fv_out = mass_fv;
