@@ -55,6 +55,11 @@ WORKLOADS = {
     # rows over the ranks; fits ONE B200 compressed
     "lbm_c5": dict(scheme="lbm", components=9, nx=65537, splits=(1024, 1024), levels=4, c=1e-3, mode="capped",
                    budget=24 << 30, device_init=True, scaling="strong"),
+    # BASELINE.json configs[2] (C3): the reference's Riemann-type shock test —
+    # SWE dam break, 4096^2 cells, 64^2-cell patches, constant c = 5e-4
+    # (SURVEY §8d); t_end far beyond the timed steps, so every step is live
+    "swe_c3": dict(scheme="swe", components=3, nx=4097, splits=(64, 64), levels=4, c=5e-4, mode="constant",
+                   t_end=1.0, scaling="weak"),
     # C3-sized transport grid in 32^2-cell patches (C1 patch shape)
     "transport_4k_p33": dict(scheme="transport", components=1, nx=4097, splits=(128, 128), levels=4, c=1e-3, mode="capped"),
     # C3-sized transport grid (4096^2 cells, 64^2-cell patches)
@@ -69,6 +74,8 @@ def run_config(w: dict, steps: int) -> api.RunConfig:
                         spec=api.ThresholdSpec(w["mode"], w["c"]), compute_l2=False, lbm_steps=steps)
     if w["scheme"] == "transport":
         cfg.t_end = steps * cfg.cfl * (1.0 / (w["nx"] - 1)) / max(cfg.alpha, cfg.beta)
+    elif w["scheme"] == "swe":
+        cfg.t_end = w.get("t_end", 1.0)
     cfg.store_budget_bytes = w.get("budget", 0)
     return cfg
 
@@ -168,11 +175,16 @@ def cpu_run(w: dict, steps: int, threads: int):
         w = WORKLOADS["lbm_c2"]
     lib, kind = cpu_lib()
     cfg = run_config(w, steps)
+    if w["scheme"] == "swe":
+        # run() has no step cap: end the run after about `steps` CFL steps of
+        # the initial state (dam break: vmax0 = sqrt(2 g); later dts shrink,
+        # so the run takes at least that many steps — the rate counts them all)
+        cfg.t_end = steps * cfg.cfl * (cfg.domain_length / (w["nx"] - 1)) / (2.0 * cfg.gravity) ** 0.5
     cfg.threads = threads if kind == "reference" else 1
     res = api.run(cfg, lib=lib)
     secs = res.summary["total_seconds"]
     cells = (w["nx"] - 1) ** 2
-    return cells * steps / secs / 1e6, secs, kind, cfg.threads, res.rows
+    return cells * len(res.rows) / secs / 1e6, secs, kind, cfg.threads, res.rows
 
 
 # ---- the reference arm -----------------------------------------------------------
@@ -188,12 +200,12 @@ def bench_reference(args, w: dict):
     mlups, secs, kind, cores, rows = cpu_run(w, args.steps, threads)
     line = {
         "impl": "reference", "metric": METRIC, "value": mlups, "unit": "MLUPS", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * secs / args.steps,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * secs / len(rows),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (reference initial state)", "config": config_json(args, w),
         "compression_ratio": statistics.fmean(r["ratio"] for r in rows),
         "cpu_baseline": {"value": mlups, "unit": "MLUPS", "cores": cores, "kind": kind,
-                         "sample": f"{args.steps} steps of the full {w['nx'] - 1}^2 workload, run() of the "
+                         "sample": f"{len(rows)} steps of the full {w['nx'] - 1}^2 workload, run() of the "
                                    f"{'reference headers (oracle/_ref)' if kind == 'reference' else 'C port'}"},
         "e2e": {"value": mlups, "unit": "MLUPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -327,14 +339,16 @@ def bench_b200(args, w: dict):
         "metric": METRIC, "value": value, "unit": "MLUPS", "n_gpus": world, "steps": args.steps,
         "warmup": warm_steps, "ms_per_step": tot_ms / args.steps, "higher_is_better": True,
         "scaling": "weak" if weak else "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (shear-layer D2Q9 initial state)" if w["scheme"] == "lbm" else "synthetic (reference initial state)",
+        "data": {"lbm": "synthetic (shear-layer D2Q9 initial state)",
+                 "swe": "synthetic (reference dam-break initial state, pipeline.hpp:144-155)"}.get(
+                     w["scheme"], "synthetic (reference initial state)"),
         "config": config_json(args, w),
         "compression_ratio": statistics.fmean(r["ratio"] for r in timed_rows),
         "compressed_bytes_per_step": statistics.fmean(r["compressed_bytes"] for r in timed_rows),
         "mass_drift": abs(timed_rows[-1]["global_mass"] - rows[0]["global_mass"]) / abs(rows[0]["global_mass"]),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
                      "frac": achieved / pk["hbm_gbs"], "traffic": traffic_from_profiles(args.workload),
-                     "kernel": f"k_{'lbm' if w['scheme'] == 'lbm' else 'patch'}_step<MAIN>",
+                     "kernel": f"k_{ {'lbm': 'lbm', 'swe': 'swe'}.get(w['scheme'], 'patch') }_step<MAIN>",
                      "algorithmic_bytes_per_launch": cells_local * B_ALG[w["scheme"]],
                      "avg_launch_ms": launch_ms, "peak_source": pk["source"],
                      "step_share": main_max / tot_ms if tot_ms else None},
@@ -349,9 +363,9 @@ def bench_b200(args, w: dict):
         # bounded sample: calibrate on a few steps, then about 12 s of CPU work
         _, s0, _, _, _ = cpu_run(w, 3, os.cpu_count() or 1)
         cpu_steps = args.cpu_steps or int(max(3, min(2000, 12.0 / max(s0 / 3, 1e-6))))
-        mlups, secs, kind, cores, _ = cpu_run(w, cpu_steps, os.cpu_count() or 1)
+        mlups, secs, kind, cores, crow = cpu_run(w, cpu_steps, os.cpu_count() or 1)
         line["cpu_baseline"] = {"value": mlups, "unit": "MLUPS", "cores": cores, "kind": kind,
-                                "sample": f"{cpu_steps} steps of the full {w['nx'] - 1}^2 workload ({secs:.1f} s)"}
+                                "sample": f"{len(crow)} steps of the full {w['nx'] - 1}^2 workload ({secs:.1f} s)"}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -499,7 +499,15 @@ static wg_status solve_hstar(double g, double hl, double ul, double hr, double u
                              double* out) {
     if (hl <= 0.0 || hr <= 0.0) return fail(WG_DOMAIN, "SweRiemann: water depth must be positive");
     const double cl = sqrt(g * hl), cr = sqrt(g * hr);
+#ifdef WG_NEWTON_SQUARE_MUL
+    /* test-only variant (libwg_oracle_sq.so): the Newton start squared by a
+     * multiplication, as the device does — isolates the one place where
+     * glibc pow(x, 2) and a correctly rounded x * x can differ by an ulp */
+    const double b = 0.5 * (cl + cr) + 0.25 * (ul - ur);
+    double h = (b * b) / g;
+#else
     double h = pow(0.5 * (cl + cr) + 0.25 * (ul - ur), 2) / g;
+#endif
     h = smax(h, 1e-12);
     for (int it = 0; it < 100; ++it) {
         const double f = phi_side(h, hl, g) + phi_side(h, hr, g) + ur - ul;

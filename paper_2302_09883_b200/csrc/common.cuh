@@ -79,6 +79,7 @@ enum : unsigned {
     ERR_DOMAIN = 1u << 2,
     ERR_RIEMANN = 1u << 3,
     ERR_RAW_OVERFLOW = 1u << 4,
+    ERR_ZERO_SPEED = 1u << 5,
 };
 
 inline void check_device_error(unsigned word) {
@@ -89,6 +90,7 @@ inline void check_device_error(unsigned word) {
     if (word & ERR_CORRUPT) raise(WG_CORRUPT_STREAM, "csr_decode: invalid block");
     if (word & ERR_DOMAIN) raise(WG_DOMAIN, "water depth must be positive");
     if (word & ERR_RIEMANN) raise(WG_RIEMANN, "SweRiemann: Newton iteration did not converge");
+    if (word & ERR_ZERO_SPEED) raise(WG_INVALID_ARGUMENT, "cfl_dt: zero wave speed");
     raise(WG_LOGIC, "device error word " + std::to_string(word));
 }
 

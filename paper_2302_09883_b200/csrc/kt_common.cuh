@@ -1,0 +1,30 @@
+// kt_common.cuh — KernelSet construction shared by the kt_*.cu units.
+#pragma once
+
+#include "common.cuh"
+#include "kernel_table.h"
+#include "patch_phases.cuh"
+
+namespace wg {
+
+inline void kt_set_smem(const KernelSet& k) {
+    for (auto f : {k.main, k.decode, k.init})
+        if (f) WG_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k.smem));
+}
+
+// Walk L = 0.. while 2^L <= N-1 (and L <= Lmax); Make<N, L>::make() builds the set.
+template <template <int, int> class Make, int N, int Lmax, int L = 0>
+bool pick_level(int levels, KernelSet& out) {
+    if constexpr ((1 << L) <= N - 1 && L <= Lmax) {
+        if (levels == L) {
+            out = Make<N, L>::make();
+            kt_set_smem(out);
+            return true;
+        }
+        return pick_level<Make, N, Lmax, L + 1>(levels, out);
+    } else {
+        return false;
+    }
+}
+
+}  // namespace wg

@@ -1,0 +1,44 @@
+// kt_transport.cu — transport (1 component) step kernels: full-line
+// k_patch_step (P patches per CTA) and the opt-in half-line variant.
+#include "half_kernels.cuh"
+#include "kt_common.cuh"
+#include "patch_kernels.cuh"
+
+namespace wg {
+namespace {
+
+template <int P>
+struct FullT {
+    template <int N, int L>
+    struct M {
+        static KernelSet make() {
+            using Lay = Layout<N, P>;
+            return KernelSet{k_patch_step<N, L, P, MODE_STEP>, k_patch_step<N, L, P, MODE_DECODE>, nullptr, P,
+                             Lay::NT, Lay::smem_bytes(), false, 0, false};
+        }
+    };
+};
+
+template <int N, int L>
+struct HalfT {
+    static KernelSet make() {
+        using Lay = HLayout<N, 2>;
+        return KernelSet{k_patch_step_h<N, L, 2, MODE_STEP>, k_patch_step_h<N, L, 2, MODE_DECODE>, nullptr, 2,
+                         Lay::NT, Lay::smem_bytes(), false, 0, false};
+    }
+};
+
+}  // namespace
+
+bool select_transport_kernels(uint64_t n, int levels, bool half_lines, KernelSet& k) {
+    switch (n) {
+        case 9: return pick_level<FullT<7>::M, 9, kMaxLevels>(levels, k);
+        case 17: return pick_level<FullT<15>::M, 17, kMaxLevels>(levels, k);
+        case 33: return pick_level<FullT<8>::M, 33, kMaxLevels>(levels, k);
+        case 65: return half_lines ? pick_level<HalfT, 65, 6>(levels, k)
+                                   : pick_level<FullT<2>::M, 65, kMaxLevels>(levels, k);
+        default: return false;
+    }
+}
+
+}  // namespace wg

@@ -72,6 +72,12 @@ struct StepArgs {
     double omega;                                        // D2Q9: 1/tau
     double ic_u0, ic_kappa, ic_delta, ic_inv;            // MODE_INIT: shear layer, 1/(nx-1)
     uint64_t ic_period;                                  // MODE_INIT: nx-1 (tiled grids repeat)
+    // SWE: the state-dependent time step lives on the device (cfl_dt,
+    // solver.hpp:235-258; pipeline.hpp:194-196)
+    double* swe_td;                  // [t, dt] of the step about to run (nullptr: host dt)
+    unsigned long long* swe_vmax;    // max wave speed of the new state (positive-double bits)
+    unsigned long long* swe_steps;   // steps completed on the device
+    double t_end, cfl_dx, dx, gravity;
     double thr[(kMaxLevels + 1) * (kMaxLevels + 1)];     // T[band_i][band_j]
 };
 
@@ -466,10 +472,11 @@ __device__ __forceinline__ void prefetch_patch(const StepArgs& a, uint32_t p, co
 // End of a step, called by every CTA with its partial sums: the last CTA to
 // finish reduces all partials in a fixed order (deterministic), writes the
 // step's MetricsRow and resets the counter and the next pool's allocator.
-__device__ __forceinline__ void finalize_step(const StepArgs& a, const StepPartial& mine) {
+__device__ __forceinline__ void finalize_step(const StepArgs& a, const StepPartial& mine, double cta_vmax = 0.0) {
     __shared__ int am_last;
     if (threadIdx.x == 0) {
         a.partials[blockIdx.x] = mine;
+        if (a.swe_td) atomicMax(a.swe_vmax, (unsigned long long)__double_as_longlong(cta_vmax));
         __threadfence();
         const unsigned prev = atomicAdd(a.done, 1u);
         am_last = prev == gridDim.x - 1;
@@ -498,8 +505,27 @@ __device__ __forceinline__ void finalize_step(const StepArgs& a, const StepParti
     }
     if (lane == 0) {
         wg_metrics_row r;
+        wg_metrics_row* row_out = a.row_out;
+        double* mfv_out = a.mass_fv_out;
         r.step = a.step;
         r.time = a.time;
+        if (a.swe_td) {  // device-side time stepping (SWE)
+            const unsigned long long k = *a.swe_steps;
+            row_out += k;
+            mfv_out += k;
+            r.step = k + 1;
+            const double t_new = a.swe_td[0] + a.swe_td[1];  // t += dt (pipeline.hpp:210)
+            r.time = t_new;
+            const double vmax = __longlong_as_double((long long)*a.swe_vmax);
+            if (!(vmax > 0.0)) atomicOr(a.err, ERR_ZERO_SPEED);
+            double dt = a.cfl_dx / vmax;                       // cfl_dt, solver.hpp:257
+            const double rest = a.t_end - t_new;
+            dt = (rest < dt) ? rest : dt;                      // std::min, pipeline.hpp:196
+            a.swe_td[0] = t_new;
+            a.swe_td[1] = dt;
+            *a.swe_vmax = 0ull;
+            *a.swe_steps = k + 1;
+        }
         r.dense_bytes = a.compress ? a.dense_bytes : 0;
         r.compressed_bytes = a.compress ? cb : 0;
         r.ratio = (a.compress && cb > 0) ? (double)r.dense_bytes / (double)cb : 1.0;
@@ -507,8 +533,8 @@ __device__ __forceinline__ void finalize_step(const StepArgs& a, const StepParti
         r.zeroed = a.compress ? zr : 0;
         r.global_mass = m;
         r.l2 = 0.0;
-        *a.row_out = r;
-        *a.mass_fv_out = mf;
+        *row_out = r;
+        *mfv_out = mf;
         *a.done = 0;
         *a.bump_next = 0;
     }

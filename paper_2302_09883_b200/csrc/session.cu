@@ -17,9 +17,8 @@
 
 #include "common.cuh"
 #include "host_model.h"
-#include "half_kernels.cuh"
-#include "lbm_kernels.cuh"
-#include "patch_kernels.cuh"
+#include "kernel_table.h"
+#include "patch_phases.cuh"
 
 namespace wg {
 
@@ -27,162 +26,30 @@ void direction_speeds(double alpha, double beta, double* smax, double* smin);  /
 
 namespace {
 
-// ---- kernel table ---------------------------------------------------------
-struct KernelSet {
-    void (*main)(StepArgs);
-    void (*decode)(StepArgs);
-    void (*init)(StepArgs);  // device-generated, compressed initial state (D2Q9); may be null
-    int P;               // patches per CTA (non-persistent kernels)
-    int threads;
-    size_t smem;
-    bool persistent;     // D2Q9: grid-stride over patches with per-CTA scratch
-    size_t scratch_doubles;  // per CTA
-    bool edges3;         // D2Q9 edge lines hold only the 3 crossing populations
-};
-
-template <int N, int L>
-KernelSet make_lbm_set() {
-    using Lay = LbmLayout<N>;
-    KernelSet k;
-    k.main = k_lbm_step<N, L, MODE_STEP>;
-    k.decode = k_lbm_step<N, L, MODE_DECODE>;
-    k.init = k_lbm_step<N, L, MODE_INIT>;
-    k.P = 1;
-    k.threads = Lay::NT;
-    k.smem = Lay::smem_bytes();
-    k.persistent = true;
-    k.scratch_doubles = Lay::scratch_doubles();
-    k.edges3 = true;
-    for (auto f : {k.main, k.decode, k.init}) {
-        WG_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k.smem));
-    }
-    return k;
-}
-
-// 65-point patches: half-line ownership (half_kernels.cuh)
-template <int N, int L, int P>
-KernelSet make_set_h() {
-    using Lay = HLayout<N, P>;
-    KernelSet k;
-    k.main = k_patch_step_h<N, L, P, MODE_STEP>;
-    k.decode = k_patch_step_h<N, L, P, MODE_DECODE>;
-    k.init = nullptr;
-    k.P = P;
-    k.threads = Lay::NT;
-    k.smem = Lay::smem_bytes();
-    k.persistent = false;
-    k.scratch_doubles = 0;
-    k.edges3 = false;
-    for (auto f : {k.main, k.decode})
-        WG_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k.smem));
-    return k;
-}
-
-template <int N, int L>
-KernelSet make_lbm_set_h() {
-    using Lay = HLayout<N, 3>;
-    KernelSet k;
-    k.main = k_lbm_step_h<N, L, MODE_STEP>;
-    k.decode = k_lbm_step_h<N, L, MODE_DECODE>;
-    k.init = nullptr;
-    k.P = 1;
-    k.threads = Lay::NT;
-    k.smem = Lay::smem_bytes();
-    k.persistent = true;
-    k.scratch_doubles = LbmLayout<N>::scratch_doubles();
-    k.edges3 = false;
-    for (auto f : {k.main, k.decode})
-        WG_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k.smem));
-    return k;
-}
-
-template <int N, int L = 0>
-bool pick_h_levels(int levels, bool lbm, KernelSet& out) {
-    if constexpr ((1 << L) <= N - 1 && L <= 6) {
-        if (levels == L) {
-            out = lbm ? make_lbm_set_h<N, L>() : make_set_h<N, L, 2>();
-            return true;
-        }
-        return pick_h_levels<N, L + 1>(levels, lbm, out);
-    } else {
-        return false;
-    }
-}
-
-template <int N, int L = 0>
-bool pick_lbm_levels(int levels, KernelSet& out) {
-    if constexpr ((1 << L) <= N - 1 && L <= 6) {
-        if (levels == L) {
-            out = make_lbm_set<N, L>();
-            return true;
-        }
-        return pick_lbm_levels<N, L + 1>(levels, out);
-    } else {
-        return false;
-    }
-}
-
-template <int N, int L, int P>
-KernelSet make_set() {
-    using Lay = Layout<N, P>;
-    KernelSet k;
-    k.main = k_patch_step<N, L, P, MODE_STEP>;
-    k.decode = k_patch_step<N, L, P, MODE_DECODE>;
-    k.init = nullptr;
-    k.P = P;
-    k.threads = Lay::NT;
-    k.smem = Lay::smem_bytes();
-    k.persistent = false;
-    k.scratch_doubles = 0;
-    k.edges3 = false;
-    for (auto f : {k.main, k.decode}) {
-        WG_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k.smem));
-    }
-    return k;
-}
-
-template <int N, int P, int L = 0>
-bool pick_levels(int levels, KernelSet& out) {
-    if constexpr ((1 << L) <= N - 1 && L <= kMaxLevels) {
-        if (levels == L) {
-            out = make_set<N, L, P>();
-            return true;
-        }
-        return pick_levels<N, P, L + 1>(levels, out);
-    } else {
-        return false;
-    }
-}
+// ---- kernel table: kernel_table.h (one translation unit per scheme) ----------
+}  // namespace
 
 KernelSet select_kernels(int scheme, uint64_t n, int levels) {
     KernelSet k{};
+    const bool half = std::getenv("WG_HALF_LINES") != nullptr;  // opt-in 65-point half-line variants
     bool ok = false;
+    const char* what = "transport";
     if (scheme == WG_SCHEME_LBM_D2Q9) {
-        switch (n) {
-            case 17: ok = pick_lbm_levels<17>(levels, k); break;
-            case 33: ok = pick_lbm_levels<33>(levels, k); break;
-            case 65: ok = std::getenv("WG_HALF_LINES") ? pick_h_levels<65>(levels, true, k)
-                                                       : pick_lbm_levels<65>(levels, k); break;
-            default: break;
-        }
-        if (!ok)
-            raise(WG_INVALID_ARGUMENT, "device session (D2Q9): patch side " + std::to_string(n) + " with " +
-                                           std::to_string(levels) + " levels is not supported (n in 17,33,65)");
-        return k;
-    }
-    switch (n) {
-        case 9: ok = pick_levels<9, 7>(levels, k); break;
-        case 17: ok = pick_levels<17, 15>(levels, k); break;
-        case 33: ok = pick_levels<33, 8>(levels, k); break;
-        case 65: ok = std::getenv("WG_HALF_LINES") ? pick_h_levels<65>(levels, false, k)
-                                                   : pick_levels<65, 2>(levels, k); break;
-        default: break;
+        ok = select_lbm_kernels(n, levels, half, k);
+        what = "D2Q9";
+    } else if (scheme == WG_SCHEME_SWE) {
+        ok = select_swe_kernels(n, levels, k);
+        what = "SWE";
+    } else {
+        ok = select_transport_kernels(n, levels, half, k);
     }
     if (!ok)
-        raise(WG_INVALID_ARGUMENT, "device session: patch side " + std::to_string(n) + " with " +
-                                       std::to_string(levels) + " levels is not supported (n in 9,17,33,65)");
+        raise(WG_INVALID_ARGUMENT, std::string("device session (") + what + "): patch side " + std::to_string(n) +
+                                       " with " + std::to_string(levels) + " levels is not supported");
     return k;
 }
+
+namespace {
 
 // ---- upload: raw store + edge lines from a grid buffer (one thread per
 // logical element: consecutive threads read consecutive addresses, which
@@ -210,6 +77,43 @@ __global__ void k_upload(const double* grid, uint32_t N, ShardGeom g, unsigned c
     if (i == N - 2 && s_rh >= 0) e.rowhi[ix(ar + 1, s_rh) + j] = x;
     if (j == 1 && s_cl >= 0) e.collo[ix(ar, s_cl) + i] = x;
     if (j == N - 2 && s_ch >= 0) e.colhi[ix(ar, s_ch) + i] = x;
+}
+
+// ---- SWE: the first time step from the uploaded state (cfl_dt,
+// solver.hpp:242-258; dt = min(dt, t_end - 0), pipeline.hpp:195-196).  The
+// max is exact, so a grid-wide atomic max of the (positive) double bits is
+// the reference's value bit for bit.
+__global__ void k_swe_vmax(const double* grid, uint32_t N, uint64_t npatch, double gravity,
+                           unsigned long long* vmax_bits, unsigned* err) {
+    const uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    const uint64_t per = (uint64_t)N * N;
+    double v = 0.0;
+    if (t < npatch * per) {
+        const uint64_t p = t / per;
+        const uint32_t i = (uint32_t)((t % per) / N), j = (uint32_t)(t % N);
+        const uint64_t TP = N + 2, tcount = TP * TP, o = (i + 1) * TP + j + 1;
+        const double* base = grid + p * 3 * tcount;
+        const double h = base[o];
+        if (h <= 0.0) atomicOr(err, ERR_DOMAIN);
+        const double c = sqrt(gravity * h);
+        const double u = fabs(base[tcount + o] / h), w = fabs(base[2 * tcount + o] / h);
+        v = fmax(u + c, w + c);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(vmax_bits, (unsigned long long)__double_as_longlong(v));
+}
+
+__global__ void k_swe_first_dt(double* td, unsigned long long* vmax_bits, unsigned long long* steps,
+                               double cfl_dx, double t_end, unsigned* err) {
+    const double vmax = __longlong_as_double((long long)*vmax_bits);
+    if (!(vmax > 0.0)) atomicOr(err, ERR_ZERO_SPEED);
+    double dt = cfl_dx / vmax;
+    dt = (t_end < dt) ? t_end : dt;  // std::min(dt, t_end - 0.0)
+    td[0] = 0.0;
+    td[1] = dt;
+    *vmax_bits = 0ull;
+    *steps = 0ull;
 }
 
 }  // namespace
@@ -243,6 +147,9 @@ struct Session {
     uint64_t cap = 0;  // bytes per pool
     uint64_t chunk = 0;  // per-CTA sub-allocation chunk
     uint64_t device_bytes = 0;
+    // SWE device clock: [t, dt] (f64 x2), vmax bits, steps done (u64 each)
+    unsigned long long* swe = nullptr;
+    uint64_t launched = 0;  // SWE step launches (steps past t_end are no-ops)
 
     int cur = 0;  // pool/edges holding the current state
     uint64_t step = 0;
@@ -296,6 +203,8 @@ struct Session {
         cudaFree(err);
         cudaFree(rows);
         cudaFree(mass_fv);
+        cudaFree(swe);
+        swe = nullptr;
         partials = nullptr;
         done = nullptr;
         bump = nullptr;
@@ -316,13 +225,15 @@ struct Session {
         return p;
     }
 
+    bool is_swe() const { return cfg.scheme == WG_SCHEME_SWE; }
+    double* swe_td() const { return reinterpret_cast<double*>(swe); }
+
     uint64_t halo_doubles() const { return (uint64_t)sg.P1 * sg.me * N; }
 
     void create(const wg_run_config& c, const wg_shard* sh, void* strm) {
         cfg = c;
         if (cfg.codec != 1) raise(WG_INVALID_ARGUMENT, "only Codec::csr is on the hot path");
-        if (cfg.scheme != WG_SCHEME_TRANSPORT && cfg.scheme != WG_SCHEME_LBM_D2Q9)
-            raise(WG_INVALID_ARGUMENT, "device session: scheme not supported by this build");
+        if (cfg.scheme != WG_SCHEME_LBM_D2Q9) sim_validate(cfg);
         if (cfg.scheme == WG_SCHEME_LBM_D2Q9 && cfg.lbm_tau <= 0.5)
             raise(WG_INVALID_ARGUMENT, "LBM: tau must exceed 1/2");
         geo = run_geometry(cfg);
@@ -334,6 +245,8 @@ struct Session {
         if (cfg.c < 0.0) raise(WG_INVALID_ARGUMENT, "apply_threshold: c must be >= 0");
         if (cfg.threshold_mode < 0 || cfg.threshold_mode > 2)
             raise(WG_INVALID_ARGUMENT, "band_threshold: unknown mode");
+        if (sh && sh->world > 1 && cfg.scheme == WG_SCHEME_SWE)
+            raise(WG_INVALID_ARGUMENT, "device session (SWE): one shard only (the CFL max is per grid)");
         if (sh) shard = *sh;
         else {
             shard.rank = 0;
@@ -402,6 +315,10 @@ struct Session {
         WG_CUDA(cudaMemsetAsync(done, 0, sizeof(unsigned), stream));
         WG_CUDA(cudaMemsetAsync(bump, 0, 2 * sizeof(unsigned long long), stream));
         WG_CUDA(cudaMemsetAsync(err, 0, sizeof(unsigned), stream));
+        if (is_swe()) {
+            swe = dalloc<unsigned long long>(4);
+            WG_CUDA(cudaMemsetAsync(swe, 0, 4 * sizeof(unsigned long long), stream));
+        }
         grow_rows(1024);
     }
 
@@ -439,8 +356,18 @@ struct Session {
         const unsigned long long used = need;
         WG_CUDA(cudaMemcpyAsync(bump + cur, &used, sizeof used, cudaMemcpyHostToDevice, stream));
         WG_CUDA(cudaMemsetAsync(bump + (1 - cur), 0, sizeof(unsigned long long), stream));
+        if (is_swe()) {
+            WG_CUDA(cudaMemsetAsync(swe + 2, 0, sizeof(unsigned long long), stream));
+            const uint64_t cells = (uint64_t)sg.npatch * N * N;
+            k_swe_vmax<<<(unsigned)((cells + 255) / 256), 256, 0, stream>>>(dgrid, N, sg.npatch, cfg.gravity,
+                                                                            swe + 2, err);
+            WG_LAUNCH_CHECK("swe wave speed");
+            k_swe_first_dt<<<1, 1, 0, stream>>>(swe_td(), swe + 2, swe + 3, cfg.cfl * sim_dx(cfg), cfg.t_end, err);
+            WG_LAUNCH_CHECK("swe first dt");
+        }
         WG_CUDA(cudaStreamSynchronize(stream));  // `used` lives on this stack frame
         step = 0;
+        launched = 0;
         time = 0.0;
     }
 
@@ -504,11 +431,26 @@ struct Session {
         a.compress = cfg.no_compression ? 0 : 1;
         a.thr_any = (cfg.c > 0.0 && levels > 0) ? 1 : 0;
         a.dense_bytes = (uint64_t)sg.npatch * 8ull * N * N * sg.m;
+        if (is_swe()) {
+            a.swe_td = swe_td();
+            a.swe_vmax = swe + 2;
+            a.swe_steps = swe + 3;
+            a.t_end = cfg.t_end;
+            a.cfl_dx = cfg.cfl * sim_dx(cfg);  // cfg.cfl * cfg.dx() (solver.hpp:257)
+            a.dx = sim_dx(cfg);
+            a.gravity = cfg.gravity;
+        }
         std::memcpy(a.thr, thr, sizeof(thr));
         return a;
     }
 
+    // One step launch.  SWE: dt is ignored — the step runs with the device
+    // clock's dt, or does nothing once t_end is reached.
     void do_step(double dt) {
+        if (is_swe()) {
+            do_swe_step();
+            return;
+        }
         const int src = cur, dst = 1 - cur;
         grow_rows(step + 1);
         StepArgs a = step_args(src, dst);
@@ -536,14 +478,49 @@ struct Session {
         time += dt;
     }
 
+    void do_swe_step() {
+        grow_rows(launched + 1);
+        const int src = cur, dst = 1 - cur;
+        StepArgs a = step_args(src, dst);
+        a.row_out = rows;  // offset by the device step counter
+        a.mass_fv_out = mass_fv;
+        cudaEvent_t e0 = nullptr, e1 = nullptr;
+        if (profiling) {
+            e0 = take_event();
+            e1 = take_event();
+            WG_CUDA(cudaEventRecord(e0, stream));
+        }
+        ks.main<<<grid, ks.threads, ks.smem, stream>>>(a);
+        WG_LAUNCH_CHECK("fused swe step");
+        if (profiling) {
+            WG_CUDA(cudaEventRecord(e1, stream));
+            ev_main.emplace_back(e0, e1);
+        }
+        ++launched;
+        // a no-op launch leaves both pools untouched: the host learns which
+        // pool is current from the device step counter (sync())
+        cur = dst;
+    }
+
     void sync() {
         WG_CUDA(cudaStreamSynchronize(stream));
         unsigned e = 0;
         WG_CUDA(cudaMemcpy(&e, err, sizeof e, cudaMemcpyDeviceToHost));
         check_device_error(e);
+        if (is_swe()) {
+            unsigned long long h[4];
+            WG_CUDA(cudaMemcpy(h, swe, sizeof h, cudaMemcpyDeviceToHost));
+            double t;
+            std::memcpy(&t, &h[0], sizeof t);
+            step = h[3];
+            time = t;
+            cur = (int)(step & 1);  // step k writes pool k & 1 (pool 0 holds the upload)
+            launched = step;
+        }
     }
 
     void download(double* hgrid) {
+        if (is_swe()) sync();  // the current pool follows the device step counter
         const uint64_t n = (uint64_t)sg.npatch * sg.m * geo.tcount;
         DevBuf<double> d(n);
         WG_CUDA(cudaMemsetAsync(d.p, 0, n * sizeof(double), stream));
@@ -663,6 +640,7 @@ wg_status wg_session_sync(wg_session* s) {
 wg_status wg_session_last_row(wg_session* sp, wg_metrics_row* row) {
     return guard([&] {
         Session* s = reinterpret_cast<Session*>(sp);
+        if (s->is_swe()) s->sync();
         if (s->step == 0) raise(WG_LOGIC, "no step has run");
         WG_CUDA(cudaMemcpyAsync(row, s->rows + (s->step - 1), sizeof(wg_metrics_row), cudaMemcpyDeviceToHost,
                                 s->stream));
@@ -722,7 +700,6 @@ wg_status wg_run(const wg_run_config* cfg, wg_metrics_row* rows, uint64_t max_ro
         std::vector<double> dts;
         if (cfg->scheme == WG_SCHEME_TRANSPORT) dts = transport_dts(*cfg);
         else if (cfg->scheme == WG_SCHEME_LBM_D2Q9) dts.assign(cfg->lbm_steps, 1.0);
-        else raise(WG_INVALID_ARGUMENT, "wg_run: scheme not supported by this build");
         Session s;
         s.create(*cfg, nullptr, nullptr);
         std::vector<double> grid(g.npatch * g.m * g.tcount);
@@ -732,7 +709,23 @@ wg_status wg_run(const wg_run_config* cfg, wg_metrics_row* rows, uint64_t max_ro
         WG_CUDA(cudaEventCreate(&e1));
         s.upload_host(grid.data());
         WG_CUDA(cudaEventRecord(e0, s.stream));
-        for (double dt : dts) s.do_step(dt);
+        if (s.is_swe()) {
+            // the step count is known only on the device: launch batches
+            // sized from the current dt, then read the clock back
+            s.sync();
+            while (s.time < cfg->t_end - 1e-15) {
+                double td[2];
+                WG_CUDA(cudaMemcpy(td, s.swe_td(), sizeof td, cudaMemcpyDeviceToHost));
+                const double est = std::ceil((cfg->t_end - td[0]) / td[1]);
+                const uint64_t batch = (uint64_t)std::clamp(est, 1.0, 512.0);
+                const uint64_t before = s.step;
+                for (uint64_t k = 0; k < batch; ++k) s.do_step(0.0);
+                s.sync();
+                if (s.step == before) raise(WG_LOGIC, "SWE step loop made no progress");
+            }
+        } else {
+            for (double dt : dts) s.do_step(dt);
+        }
         WG_CUDA(cudaEventRecord(e1, s.stream));
         s.sync();
         float ms = 0.f;

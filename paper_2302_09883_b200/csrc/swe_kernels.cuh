@@ -1,0 +1,253 @@
+// swe_kernels.cuh — the fused per-patch step for the shallow-water scheme
+// (3 components h, hu, hv; exact-Riemann Godunov flux, solver.hpp:74-199).
+//
+// One launch = one step of run() for Scheme::swe (pipeline.hpp:194-289), with
+// the time step kept on the device: the step reads [t, dt] from swe_td,
+// exits at once when t >= t_end (pipeline.hpp:194), and its last CTA computes
+// the next dt = cfl dx / vmax from the maximum wave speed of the new
+// (post-compression) state (cfl_dt, solver.hpp:242-257 — a max, hence
+// order-independent and bit-identical), clipped to t_end - t.
+//
+// Per patch (one CTA, the three components in three slots):
+//   decode h, hu, hv (CSR -> inverse DWT) + ghost ring      -> tiles
+//   Godunov FV, 4 faces per cell (each face twice, like fv_step) -> scratch
+//   forward DWT, threshold, CSR, reconstruction, edges (all 3), mass of h
+//   skip rule: nothing zeroed -> the FV output is stored raw (pipeline.hpp:243-249)
+//   max wave speed of the stored state (reconstructed or raw)
+// The compression stages are bit-exact; the FV differs from the reference
+// only where glibc pow(x, 2) (the Newton start, solver.hpp:112) is not the
+// correctly rounded square the device uses.
+#pragma once
+
+#include "patch_phases.cuh"
+
+namespace wg {
+
+template <int N>
+struct SweLayout {
+    static constexpr int TP = N + 2;
+    static constexpr int TILE = TP * TP;
+    static constexpr int NT = ((3 * N + 31) / 32) * 32;
+    static constexpr size_t smem_bytes() {
+        return sizeof(double) * (size_t)(3 * TILE) + sizeof(unsigned long long) * NT;
+    }
+    static constexpr size_t scratch_doubles() { return (size_t)3 * N * N; }
+};
+
+template <int N, int L, int MODE>
+__global__ void __launch_bounds__(SweLayout<N>::NT) k_swe_step(const __grid_constant__ StepArgs a) {
+    using Lay = SweLayout<N>;
+    constexpr int TP = Lay::TP, TILE = Lay::TILE, NT = Lay::NT, NN = N * N;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    double* tiles = reinterpret_cast<double*>(smem_raw);
+    unsigned long long* inc = reinterpret_cast<unsigned long long*>(tiles + 3 * TILE);
+    __shared__ uint64_t slot_off[3];
+    __shared__ int slot_ok[3];
+    __shared__ uint32_t comp_nnz[3];
+    __shared__ unsigned long long patch_bytes, patch_nnz, patch_zero;
+    __shared__ ChunkState cs;
+    __shared__ double wmax[NT / 32];
+
+    const int t = threadIdx.x;
+    const int s = t / N;  // slot == component
+    const int li = t - s * N;
+    const bool lane_ok = t < 3 * N;
+    const ShardGeom& g = a.g;
+    double* T = tiles + (lane_ok ? s : 0) * TILE;
+    double* S = a.scratch + (size_t)blockIdx.x * Lay::scratch_doubles();
+
+    if (MODE == MODE_DECODE) {
+        for (uint32_t p = blockIdx.x; p < g.npatch; p += gridDim.x) {
+            bool raw_in = false;
+            if (lane_ok) raw_in = decode_row<N, L>(T, li, a.dir_in[(size_t)p * 3 + s], a.store_in);
+            __syncthreads();
+            if (lane_ok) {
+                double v[N];
+                decode_col<N, L>(T, li, raw_in, v);
+                double* out = a.decode_out + ((size_t)p * 3 + s) * TILE;
+#pragma unroll
+                for (int i = 0; i < N; ++i) out[(i + 1) * TP + li + 1] = v[i];
+            }
+            __syncthreads();
+        }
+        return;
+    }
+
+    // the device-side clock (uniform for all CTAs of the launch)
+    const double t_now = a.swe_td[0], dt = a.swe_td[1];
+    if (!(t_now < a.t_end - 1e-15)) return;  // run() loop condition, pipeline.hpp:194
+    const double r = dt / a.dx;              // solver.hpp:212
+
+    StepPartial part{0, 0, 0, 0.0, 0.0};
+    double macc = 0.0, mfacc = 0.0, vmax = 0.0;
+    if (t == 0) cs.cur = cs.end = 0;
+    for (uint32_t p = blockIdx.x; p < g.npatch; p += gridDim.x) {
+        const PatchPos pp = patch_pos(p, g);
+        // ---- decode h, hu, hv + ghost ring --------------------------------
+        bool raw_in = false;
+        if (lane_ok) {
+            raw_in = decode_row<N, L>(T, li, a.dir_in[(size_t)p * 3 + s], a.store_in);
+            fill_ghosts<N>(T, li, a.ein, pp, s, g);
+        }
+        __syncthreads();
+        if (lane_ok && !raw_in) {
+            double v[N];
+            decode_col<N, L>(T, li, false, v);
+            store_col<N>(T, li, v);
+        }
+        __syncthreads();
+        // ---- Godunov FV (fv_step<SweFlux>, solver.hpp:207-231) -------------
+        const double* T0 = tiles;
+        const double* T1 = tiles + TILE;
+        const double* T2 = tiles + 2 * TILE;
+        const int di[4] = {1, -1, 0, 0}, dj[4] = {0, 0, 1, -1};  // +x, -x, +y, -y
+        double mfv = 0.0;
+        for (int c = t; c < NN; c += NT) {
+            const int i = c / N, j = c - (c / N) * N;
+            const int o = (i + 1) * TP + j + 1;
+            double w[3] = {T0[o], T1[o], T2[o]};
+            double out[3] = {w[0], w[1], w[2]};
+            int e = 0;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int on = o + di[k] * TP + dj[k];
+                const double wn[3] = {T0[on], T1[on], T2[on]};
+                double f[3];
+                flux_swe(w, wn, di[k], dj[k], a.gravity, f, e);
+#pragma unroll
+                for (int q = 0; q < 3; ++q) out[q] -= r * f[q];
+            }
+            if (e) atomicOr(a.err, e == 1 ? ERR_DOMAIN : ERR_RIEMANN);
+#pragma unroll
+            for (int q = 0; q < 3; ++q) S[(size_t)q * NN + c] = out[q];
+            const double wgt = ((i == 0 || i == N - 1) ? 0.5 : 1.0) * ((j == 0 || j == N - 1) ? 0.5 : 1.0);
+            mfv += wgt * out[0];  // global_mass(grid, 0): h only (pipeline.hpp:274)
+        }
+        mfacc += mfv;
+        __syncthreads();
+
+        double m = 0.0;
+        bool store_raw = !a.compress;
+        if (a.compress) {
+            if (t == 0) {
+                patch_bytes = 0;
+                patch_nnz = 0;
+                patch_zero = 0;
+            }
+            const bool cycle = a.thr_any != 0;
+            double v[N];
+            if (lane_ok) {
+#pragma unroll
+                for (int i = 0; i < N; ++i) v[i] = S[(size_t)s * NN + i * N + li];
+                fwd_col_to_tile<N, L>(T, li, v);
+            }
+            __syncthreads();
+            unsigned nz = 0, zr = 0;
+            if (lane_ok) fwd_row_threshold<N, L>(T, li, a.thr, v, nz, zr);
+            cta_inclusive_scan<NT>(((unsigned long long)zr << 32) | nz, inc);
+            if (t == 0) {
+                for (int sl = 0; sl < 3; ++sl) {
+                    const unsigned long long base = sl == 0 ? 0ull : inc[sl * N - 1];
+                    const unsigned long long tot = inc[sl * N + N - 1] - base;
+                    const uint32_t snz = (uint32_t)(tot & 0xffffffffu);
+                    comp_nnz[sl] = snz;
+                    patch_bytes += 12ull * snz + 4ull * (N + 1);
+                    patch_nnz += snz;
+                    patch_zero += tot >> 32;
+                }
+                // skip rule decided before anything is written (pipeline.hpp:243)
+                for (int sl = 0; sl < 3; ++sl) {
+                    if (!cycle || patch_zero == 0) {
+                        slot_ok[sl] = 0;
+                        continue;
+                    }
+                    const uint64_t off = chunk_alloc(a, cs, round16(12ull * comp_nnz[sl] + 4ull * (N + 1)));
+                    slot_ok[sl] = off != ~0ull;
+                    slot_off[sl] = off;
+                    a.dir_out[(size_t)p * 3 + sl] =
+                        slot_ok[sl] ? DirEntry{off, comp_nnz[sl], 0u} : DirEntry{0, 0u, DIR_DEAD};
+                }
+                part.comp_bytes += patch_bytes;
+                part.nnz += patch_nnz;
+                part.zeroed += patch_zero;
+            }
+            __syncthreads();
+            store_raw = patch_zero == 0;
+            const bool ok = lane_ok && slot_ok[s];
+            if (ok) {
+                const unsigned long long base = s == 0 ? 0ull : inc[s * N - 1];
+                const uint32_t k = (uint32_t)((inc[t] - base) & 0xffffffffu) - nz;
+                write_csr_row<N, L>(a.store_out + slot_off[s], comp_nnz[s], li, k, nz, v);
+                inv_row_to_tile<N, L>(T, li, v);
+            }
+            __syncthreads();
+            if (ok) {
+                decode_col<N, L>(T, li, false, v);
+                write_edges<N>(a.eout, pp, s, g, li, v);
+                if (s == 0) m += col_mass<N>(li, v);
+            }
+            __syncthreads();
+            if (ok) store_col<N>(T, li, v);  // the new state, for the wave speed
+            __syncthreads();
+            if (!store_raw) {
+                for (int c = t; c < NN; c += NT) {
+                    const int o = (c / N + 1) * TP + c - (c / N) * N + 1;
+                    const double h = T0[o];
+                    if (h <= 0.0) atomicOr(a.err, ERR_DOMAIN);  // cfl_dt, solver.hpp:248
+                    const double cc = sqrt(a.gravity * h);
+                    const double u = fabs(T1[o] / h), w2 = fabs(T2[o] / h);
+                    vmax = fmax(vmax, fmax(u + cc, w2 + cc));
+                }
+                __syncthreads();  // the next patch's decode overwrites the tiles
+            }
+        }
+        if (store_raw) {  // raw store of the FV output (skip rule / no_compression)
+            if (t == 0) {
+                for (int sl = 0; sl < 3; ++sl) {
+                    const uint64_t off = chunk_alloc(a, cs, round16((uint64_t)NN * 8));
+                    slot_ok[sl] = off != ~0ull;
+                    slot_off[sl] = off;
+                    a.dir_out[(size_t)p * 3 + sl] = slot_ok[sl] ? DirEntry{off, 0u, DIR_RAW} : DirEntry{0, 0u, DIR_DEAD};
+                }
+            }
+            __syncthreads();
+            m = 0.0;
+            if (lane_ok) {
+                double v[N];
+#pragma unroll
+                for (int i = 0; i < N; ++i) v[i] = S[(size_t)s * NN + i * N + li];
+                if (slot_ok[s]) {
+                    double* d = reinterpret_cast<double*>(a.store_out + slot_off[s]);
+#pragma unroll
+                    for (int i = 0; i < N; ++i) d[i * N + li] = v[i];
+                }
+                write_edges<N>(a.eout, pp, s, g, li, v);
+                if (s == 0) m = col_mass<N>(li, v);
+            }
+            for (int c = t; c < NN; c += NT) {
+                const double h = S[c];
+                if (h <= 0.0) atomicOr(a.err, ERR_DOMAIN);
+                const double cc = sqrt(a.gravity * h);
+                const double u = fabs(S[(size_t)NN + c] / h), w2 = fabs(S[(size_t)2 * NN + c] / h);
+                vmax = fmax(vmax, fmax(u + cc, w2 + cc));
+            }
+            __syncthreads();
+        }
+        macc += m;
+    }
+    part.mass = macc;
+    part.mass_fv = mfacc;
+    if (t != 0) part.comp_bytes = part.nnz = part.zeroed = 0;
+    const StepPartial tot = cta_reduce_partial<NT>(part);
+    // CTA max of the wave speed (exact: order-independent)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) vmax = fmax(vmax, __shfl_xor_sync(0xffffffffu, vmax, o));
+    if ((t & 31) == 0) wmax[t >> 5] = vmax;
+    __syncthreads();
+    double cta_v = 0.0;
+    if (t == 0)
+        for (int w = 0; w < NT / 32; ++w) cta_v = fmax(cta_v, wmax[w]);
+    finalize_step(a, tot, cta_v);
+}
+
+}  // namespace wg

@@ -16,6 +16,7 @@ if str(REPO) not in sys.path:
 from paper_2302_09883_b200 import abi  # noqa: E402
 
 ORACLE_C = REPO / "oracle" / "libwg_oracle.so"
+ORACLE_SQ = REPO / "oracle" / "libwg_oracle_sq.so"
 ORACLE_REF = REPO / "oracle" / "_ref" / "libwg_ref.so"
 GOLDEN = REPO / "tests" / "golden"
 
@@ -31,6 +32,15 @@ def oracle():
     if not ORACLE_C.exists():
         subprocess.run(["make", "-s", "-C", str(REPO / "oracle"), "c"], check=True)
     return abi.Lib(ORACLE_C)
+
+
+@pytest.fixture(scope="session")
+def oracle_sq():
+    """The restatement with the SWE Newton start squared by multiplication
+    (oracle/wg_oracle.c WG_NEWTON_SQUARE_MUL) — the device's arithmetic."""
+    if not ORACLE_SQ.exists():
+        subprocess.run(["make", "-s", "-C", str(REPO / "oracle"), "c"], check=True)
+    return abi.Lib(ORACLE_SQ)
 
 
 @pytest.fixture(scope="session")
