@@ -257,9 +257,19 @@ wg_status wg_dev_session_upload(wg_session* s, const double* dev_grid);
  * bit-identical to the host's: results are not pinned to run().  D2Q9. */
 wg_status wg_session_init_device(wg_session* s);
 
-/* Advance one step with time step dt (ignored for LBM).  After it returns
- * (asynchronously), the halo send blocks of the next step are ready. */
+/* Advance one step with time step dt (ignored for LBM and SWE).  After it
+ * returns (asynchronously), the halo send blocks of the next step are ready.
+ * SWE keeps its clock on the device: each step takes dt = cfl dx / vmax
+ * (cfl_dt, solver.hpp:242-258) clipped to t_end - t, and steps launched
+ * once t >= t_end are no-ops (run()'s loop, pipeline.hpp:194-196);
+ * wg_session_metrics reports the steps actually taken. */
 wg_status wg_session_step(wg_session* s, double dt);
+
+/* SWE, world > 1: the max wave speed the NEXT step's dt is computed from
+ * (IEEE bits of a non-negative double, so an int64 MAX is the double max).
+ * Multi-GPU callers all-reduce it with MAX after every upload and step —
+ * the per-step CFL all-reduce of SURVEY §8e.  Device pointer, 1 element. */
+wg_status wg_session_cfl_vmax(wg_session* s, unsigned long long** vmax_bits);
 
 /* Halo blocks for multi-GPU (world > 1).  send_lo: logical row 1 of every
  * patch of the first owned patch row; send_hi: logical row n-2 of the last

@@ -73,9 +73,12 @@ struct StepArgs {
     double ic_u0, ic_kappa, ic_delta, ic_inv;            // MODE_INIT: shear layer, 1/(nx-1)
     uint64_t ic_period;                                  // MODE_INIT: nx-1 (tiled grids repeat)
     // SWE: the state-dependent time step lives on the device (cfl_dt,
-    // solver.hpp:235-258; pipeline.hpp:194-196)
-    double* swe_td;                  // [t, dt] of the step about to run (nullptr: host dt)
-    unsigned long long* swe_vmax;    // max wave speed of the new state (positive-double bits)
+    // solver.hpp:235-258; pipeline.hpp:194-196).  Step k reads the max wave
+    // speed of its input state from swe_vmax[k & 1] (all-reduced with MAX
+    // across shards by the host between steps when world > 1) and
+    // accumulates that of its output state into swe_vmax[(k + 1) & 1].
+    double* swe_td;                  // [t, dt of the last step] (nullptr: host dt)
+    unsigned long long* swe_vmax;    // [2] max wave speed, bits of a non-negative double
     unsigned long long* swe_steps;   // steps completed on the device
     double t_end, cfl_dx, dx, gravity;
     double thr[(kMaxLevels + 1) * (kMaxLevels + 1)];     // T[band_i][band_j]
@@ -469,14 +472,38 @@ __device__ __forceinline__ void prefetch_patch(const StepArgs& a, uint32_t p, co
     prefetch_edges<N>(a, p, tid, nthreads);
 }
 
+// The device clock of an SWE step, read by every CTA at its start (the
+// inputs are written only by the previous launch, so the values are uniform).
+struct SweClock {
+    unsigned long long k;  // steps done before this one
+    double t, dt;
+    bool live;             // t < t_end (run() loop condition, pipeline.hpp:194)
+};
+
+__device__ __forceinline__ SweClock swe_clock(const StepArgs& a) {
+    SweClock c;
+    c.k = *a.swe_steps;
+    c.t = a.swe_td[0];
+    c.live = c.t < a.t_end - 1e-15;
+    const double vmax = __longlong_as_double((long long)a.swe_vmax[c.k & 1]);
+    if (c.live && !(vmax > 0.0) && blockIdx.x == 0 && threadIdx.x == 0) atomicOr(a.err, ERR_ZERO_SPEED);
+    double dt = a.cfl_dx / vmax;        // cfl_dt: cfg.cfl * cfg.dx() / vmax (solver.hpp:257)
+    const double rest = a.t_end - c.t;
+    c.dt = (rest < dt) ? rest : dt;     // std::min(dt, t_end - t) (pipeline.hpp:196)
+    return c;
+}
+
 // End of a step, called by every CTA with its partial sums: the last CTA to
 // finish reduces all partials in a fixed order (deterministic), writes the
 // step's MetricsRow and resets the counter and the next pool's allocator.
-__device__ __forceinline__ void finalize_step(const StepArgs& a, const StepPartial& mine, double cta_vmax = 0.0) {
+// SWE (clk != nullptr): every CTA max-accumulates the wave speed of its
+// patches of the new state; the last CTA advances the clock.
+__device__ __forceinline__ void finalize_step(const StepArgs& a, const StepPartial& mine, double cta_vmax = 0.0,
+                                              const SweClock* clk = nullptr) {
     __shared__ int am_last;
     if (threadIdx.x == 0) {
         a.partials[blockIdx.x] = mine;
-        if (a.swe_td) atomicMax(a.swe_vmax, (unsigned long long)__double_as_longlong(cta_vmax));
+        if (clk) atomicMax(a.swe_vmax + ((clk->k + 1) & 1), (unsigned long long)__double_as_longlong(cta_vmax));
         __threadfence();
         const unsigned prev = atomicAdd(a.done, 1u);
         am_last = prev == gridDim.x - 1;
@@ -509,22 +536,15 @@ __device__ __forceinline__ void finalize_step(const StepArgs& a, const StepParti
         double* mfv_out = a.mass_fv_out;
         r.step = a.step;
         r.time = a.time;
-        if (a.swe_td) {  // device-side time stepping (SWE)
-            const unsigned long long k = *a.swe_steps;
-            row_out += k;
-            mfv_out += k;
-            r.step = k + 1;
-            const double t_new = a.swe_td[0] + a.swe_td[1];  // t += dt (pipeline.hpp:210)
-            r.time = t_new;
-            const double vmax = __longlong_as_double((long long)*a.swe_vmax);
-            if (!(vmax > 0.0)) atomicOr(a.err, ERR_ZERO_SPEED);
-            double dt = a.cfl_dx / vmax;                       // cfl_dt, solver.hpp:257
-            const double rest = a.t_end - t_new;
-            dt = (rest < dt) ? rest : dt;                      // std::min, pipeline.hpp:196
-            a.swe_td[0] = t_new;
-            a.swe_td[1] = dt;
-            *a.swe_vmax = 0ull;
-            *a.swe_steps = k + 1;
+        if (clk) {  // device-side time stepping (SWE)
+            row_out += clk->k;
+            mfv_out += clk->k;
+            r.step = clk->k + 1;
+            r.time = clk->t + clk->dt;  // t += dt (pipeline.hpp:210)
+            a.swe_td[0] = r.time;
+            a.swe_td[1] = clk->dt;
+            a.swe_vmax[clk->k & 1] = 0ull;  // read by every CTA already; accumulates step k + 1's output
+            *a.swe_steps = clk->k + 1;
         }
         r.dense_bytes = a.compress ? a.dense_bytes : 0;
         r.compressed_bytes = a.compress ? cb : 0;

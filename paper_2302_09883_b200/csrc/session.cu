@@ -104,15 +104,10 @@ __global__ void k_swe_vmax(const double* grid, uint32_t N, uint64_t npatch, doub
     if ((threadIdx.x & 31) == 0) atomicMax(vmax_bits, (unsigned long long)__double_as_longlong(v));
 }
 
-__global__ void k_swe_first_dt(double* td, unsigned long long* vmax_bits, unsigned long long* steps,
-                               double cfl_dx, double t_end, unsigned* err) {
-    const double vmax = __longlong_as_double((long long)*vmax_bits);
-    if (!(vmax > 0.0)) atomicOr(err, ERR_ZERO_SPEED);
-    double dt = cfl_dx / vmax;
-    dt = (t_end < dt) ? t_end : dt;  // std::min(dt, t_end - 0.0)
+__global__ void k_swe_clock_reset(double* td, unsigned long long* vmax_bits, unsigned long long* steps) {
     td[0] = 0.0;
-    td[1] = dt;
-    *vmax_bits = 0ull;
+    td[1] = 0.0;
+    vmax_bits[1] = 0ull;  // vmax_bits[0]: the uploaded state's (k_swe_vmax)
     *steps = 0ull;
 }
 
@@ -147,7 +142,7 @@ struct Session {
     uint64_t cap = 0;  // bytes per pool
     uint64_t chunk = 0;  // per-CTA sub-allocation chunk
     uint64_t device_bytes = 0;
-    // SWE device clock: [t, dt] (f64 x2), vmax bits, steps done (u64 each)
+    // SWE device clock: [t, last dt] (f64), vmax bits [2], steps done (u64)
     unsigned long long* swe = nullptr;
     uint64_t launched = 0;  // SWE step launches (steps past t_end are no-ops)
 
@@ -245,8 +240,6 @@ struct Session {
         if (cfg.c < 0.0) raise(WG_INVALID_ARGUMENT, "apply_threshold: c must be >= 0");
         if (cfg.threshold_mode < 0 || cfg.threshold_mode > 2)
             raise(WG_INVALID_ARGUMENT, "band_threshold: unknown mode");
-        if (sh && sh->world > 1 && cfg.scheme == WG_SCHEME_SWE)
-            raise(WG_INVALID_ARGUMENT, "device session (SWE): one shard only (the CFL max is per grid)");
         if (sh) shard = *sh;
         else {
             shard.rank = 0;
@@ -316,8 +309,8 @@ struct Session {
         WG_CUDA(cudaMemsetAsync(bump, 0, 2 * sizeof(unsigned long long), stream));
         WG_CUDA(cudaMemsetAsync(err, 0, sizeof(unsigned), stream));
         if (is_swe()) {
-            swe = dalloc<unsigned long long>(4);
-            WG_CUDA(cudaMemsetAsync(swe, 0, 4 * sizeof(unsigned long long), stream));
+            swe = dalloc<unsigned long long>(5);
+            WG_CUDA(cudaMemsetAsync(swe, 0, 5 * sizeof(unsigned long long), stream));
         }
         grow_rows(1024);
     }
@@ -362,8 +355,8 @@ struct Session {
             k_swe_vmax<<<(unsigned)((cells + 255) / 256), 256, 0, stream>>>(dgrid, N, sg.npatch, cfg.gravity,
                                                                             swe + 2, err);
             WG_LAUNCH_CHECK("swe wave speed");
-            k_swe_first_dt<<<1, 1, 0, stream>>>(swe_td(), swe + 2, swe + 3, cfg.cfl * sim_dx(cfg), cfg.t_end, err);
-            WG_LAUNCH_CHECK("swe first dt");
+            k_swe_clock_reset<<<1, 1, 0, stream>>>(swe_td(), swe + 2, swe + 4);
+            WG_LAUNCH_CHECK("swe clock");
         }
         WG_CUDA(cudaStreamSynchronize(stream));  // `used` lives on this stack frame
         step = 0;
@@ -434,7 +427,7 @@ struct Session {
         if (is_swe()) {
             a.swe_td = swe_td();
             a.swe_vmax = swe + 2;
-            a.swe_steps = swe + 3;
+            a.swe_steps = swe + 4;
             a.t_end = cfg.t_end;
             a.cfl_dx = cfg.cfl * sim_dx(cfg);  // cfg.cfl * cfg.dx() (solver.hpp:257)
             a.dx = sim_dx(cfg);
@@ -508,11 +501,11 @@ struct Session {
         WG_CUDA(cudaMemcpy(&e, err, sizeof e, cudaMemcpyDeviceToHost));
         check_device_error(e);
         if (is_swe()) {
-            unsigned long long h[4];
+            unsigned long long h[5];
             WG_CUDA(cudaMemcpy(h, swe, sizeof h, cudaMemcpyDeviceToHost));
             double t;
             std::memcpy(&t, &h[0], sizeof t);
-            step = h[3];
+            step = h[4];
             time = t;
             cur = (int)(step & 1);  // step k writes pool k & 1 (pool 0 holds the upload)
             launched = step;
@@ -620,6 +613,14 @@ wg_status wg_session_halo(wg_session* sp, double** send_lo, double** send_hi, do
     });
 }
 
+wg_status wg_session_cfl_vmax(wg_session* sp, unsigned long long** vmax_bits) {
+    return guard([&] {
+        Session* s = reinterpret_cast<Session*>(sp);
+        if (!s->is_swe()) raise(WG_INVALID_ARGUMENT, "wg_session_cfl_vmax: SWE sessions only");
+        *vmax_bits = s->swe + 2 + (s->launched & 1);
+    });
+}
+
 wg_status wg_session_metrics(wg_session* s, wg_metrics_row* rows, uint64_t max_rows, uint64_t* nrows) {
     return guard([&] { reinterpret_cast<Session*>(s)->metrics(rows, max_rows, nrows); });
 }
@@ -714,9 +715,9 @@ wg_status wg_run(const wg_run_config* cfg, wg_metrics_row* rows, uint64_t max_ro
             // sized from the current dt, then read the clock back
             s.sync();
             while (s.time < cfg->t_end - 1e-15) {
-                double td[2];
+                double td[2];  // [t, dt of the last step]
                 WG_CUDA(cudaMemcpy(td, s.swe_td(), sizeof td, cudaMemcpyDeviceToHost));
-                const double est = std::ceil((cfg->t_end - td[0]) / td[1]);
+                const double est = td[1] > 0.0 ? std::ceil((cfg->t_end - td[0]) / td[1]) : 16.0;
                 const uint64_t batch = (uint64_t)std::clamp(est, 1.0, 512.0);
                 const uint64_t before = s.step;
                 for (uint64_t k = 0; k < batch; ++k) s.do_step(0.0);

@@ -2,11 +2,12 @@
 // (3 components h, hu, hv; exact-Riemann Godunov flux, solver.hpp:74-199).
 //
 // One launch = one step of run() for Scheme::swe (pipeline.hpp:194-289), with
-// the time step kept on the device: the step reads [t, dt] from swe_td,
-// exits at once when t >= t_end (pipeline.hpp:194), and its last CTA computes
-// the next dt = cfl dx / vmax from the maximum wave speed of the new
-// (post-compression) state (cfl_dt, solver.hpp:242-257 — a max, hence
-// order-independent and bit-identical), clipped to t_end - t.
+// the time step kept on the device: every CTA derives dt = cfl dx / vmax,
+// clipped to t_end - t, from the clock and the max wave speed of the input
+// state (cfl_dt, solver.hpp:242-257 — a max, hence order-independent and
+// bit-identical); the launch is a no-op once t >= t_end (pipeline.hpp:194).
+// The max wave speed of the output state is accumulated for the next step
+// (and all-reduced across shards between steps when world > 1).
 //
 // Per patch (one CTA, the three components in three slots):
 //   decode h, hu, hv (CSR -> inverse DWT) + ghost ring      -> tiles
@@ -74,9 +75,9 @@ __global__ void __launch_bounds__(SweLayout<N>::NT) k_swe_step(const __grid_cons
     }
 
     // the device-side clock (uniform for all CTAs of the launch)
-    const double t_now = a.swe_td[0], dt = a.swe_td[1];
-    if (!(t_now < a.t_end - 1e-15)) return;  // run() loop condition, pipeline.hpp:194
-    const double r = dt / a.dx;              // solver.hpp:212
+    const SweClock clk = swe_clock(a);
+    if (!clk.live) return;        // t >= t_end: the launch is a no-op
+    const double r = clk.dt / a.dx;  // solver.hpp:212
 
     StepPartial part{0, 0, 0, 0.0, 0.0};
     double macc = 0.0, mfacc = 0.0, vmax = 0.0;
@@ -247,7 +248,7 @@ __global__ void __launch_bounds__(SweLayout<N>::NT) k_swe_step(const __grid_cons
     double cta_v = 0.0;
     if (t == 0)
         for (int w = 0; w < NT / 32; ++w) cta_v = fmax(cta_v, wmax[w]);
-    finalize_step(a, tot, cta_v);
+    finalize_step(a, tot, cta_v, &clk);
 }
 
 }  // namespace wg

@@ -7,6 +7,10 @@ rank r sends logical row 1 of its first patch row to r-1 and logical row n-2
 of its last patch row to r+1 (periodic ring), i.e. exactly the values that
 sync_ghosts (patchgrid.hpp:131-201) copies across the rank boundary.
 Reductions (mass, nnz, zeroed, bytes) are all-reduced once, at the end.
+The shallow-water scheme adds one collective per step: its CFL time step is a
+max over the whole grid (cfl_dt, solver.hpp:242-258), so every rank's max
+wave speed is all-reduced with MAX before the next step (8 bytes; the session
+computes dt from it on the device).
 
 The exchange uses torch.distributed point-to-point (NCCL over NVLink on GPU,
 gloo on CPU in the tests) on tensors that alias the session's halo blocks.
@@ -107,6 +111,7 @@ class ShardedSession:
         self.info = abi.SessionInfoC()
         lib.check(lib.wg_session_info_get(self.handle, C.byref(self.info)))
         self._halo = None
+        self.swe = cfg.scheme == "swe"
 
     def close(self):
         if self.handle:
@@ -126,6 +131,19 @@ class ShardedSession:
         if self.shard.world > 1:
             s_lo, s_hi, r_lo, r_hi = self.halo_tensors()
             exchange_halos(s_lo, s_hi, r_lo, r_hi, self.shard.rank, self.shard.world, self.dist)
+            if self.swe:
+                self.dist.all_reduce(self.cfl_vmax_tensor(), op=self.dist.ReduceOp.MAX)
+
+    def cfl_vmax_tensor(self):
+        """SWE: the next step's max wave speed (int64 view of the non-negative
+        double's bits, so MAX over int64 is MAX over the doubles)."""
+        import torch
+
+        p = abi.vp()
+        self.lib.check(self.lib.wg_session_cfl_vmax(self.handle, C.byref(p)))
+        arr = _DevArray(p.value, 1)
+        arr.__cuda_array_interface__["typestr"] = "<i8"
+        return torch.as_tensor(arr, device=f"cuda:{self.shard.device}")
 
     def halo_tensors(self):
         import torch

@@ -1,0 +1,152 @@
+"""The sharded device path on ONE GPU: `world` patch-row shards
+as `world` sessions of one process, stepped in lock-step on one stream, with
+the halo ring (and the SWE CFL max) exchanged by device copies between
+steps — exactly the data movement distributed.ShardedSession does over NCCL,
+minus the transport.  No kernel waits on another shard's kernel.
+
+The N-shard state must be bitwise equal to the 1-shard state (the exchange
+is a pure copy; SURVEY §8e "Test"), and the per-shard metrics must sum to
+the 1-shard metrics (integer counts exactly, mass to round-off)."""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+import pytest
+
+from paper_2302_09883_b200 import abi, api
+from paper_2302_09883_b200.distributed import ShardInfo, ShardedSession, shard_rows
+
+from .test_gpu_session import bits
+
+pytestmark = pytest.mark.gpu
+
+
+class LocalShards:
+    def __init__(self, lib, cfg: api.RunConfig, world: int):
+        import torch
+
+        self.torch = torch
+        self.lib, self.cfg, self.world = lib, cfg, world
+        self.stream = torch.cuda.Stream()
+        P0 = cfg.splits[0] * max(cfg.tile_rows, 1)
+        self.ranges = [shard_rows(P0, r, world) for r in range(world)]
+        self.sessions = [ShardedSession(lib, cfg, ShardInfo(r, world, rb, re_, 0), self.stream.cuda_stream, None)
+                         for r, (rb, re_) in enumerate(self.ranges)]
+
+    def close(self):
+        for s in self.sessions:
+            s.close()
+
+    def upload(self, grid: api.PatchGrid):
+        P1 = self.cfg.splits[1]
+        per = grid.data.size // grid.data.shape[0]
+        flat = grid.data.reshape(grid.data.shape[0], per)
+        self._keep = []
+        for s, (rb, re_) in zip(self.sessions, self.ranges):
+            part = np.ascontiguousarray(flat[rb * P1: re_ * P1]).reshape(-1)
+            self._keep.append(part)
+            self.lib.check(self.lib.wg_session_upload(s.handle, abi.dptr(part)))
+        self.exchange()
+
+    def exchange(self):
+        torch = self.torch
+        halos = [s.halo_tensors() for s in self.sessions]
+        with torch.cuda.stream(self.stream):
+            for r in range(self.world):
+                above, below = (r - 1) % self.world, (r + 1) % self.world
+                halos[r][2].copy_(halos[above][1])  # recv_lo <- above.send_hi
+                halos[r][3].copy_(halos[below][0])  # recv_hi <- below.send_lo
+            if self.cfg.scheme == "swe":
+                v = [s.cfl_vmax_tensor() for s in self.sessions]
+                m = torch.stack(v).max()
+                for t in v:
+                    t.copy_(m)
+
+    def step(self):
+        for s in self.sessions:
+            self.lib.check(self.lib.wg_session_step(s.handle, 1.0))
+        self.exchange()
+
+    def download(self) -> np.ndarray:
+        self.stream.synchronize()
+        parts = []
+        for s in self.sessions:
+            n = s.info.npatch_local * s.info.components * (s.info.patch_n + 2) ** 2
+            out = np.zeros(n)
+            self.lib.check(self.lib.wg_session_download(s.handle, abi.dptr(out)))
+            parts.append(out)
+        return np.concatenate(parts)
+
+    def rows(self):
+        per = [s.rows() for s in self.sessions]
+        assert len({len(p) for p in per}) == 1
+        return per
+
+
+def _cfg(scheme, nx, splits, levels, c, **kw):
+    cfg = api.RunConfig(scheme=scheme, nx=nx, splits=splits, levels=levels,
+                        spec=api.ThresholdSpec("capped" if scheme != "swe" else "constant", c), compute_l2=False,
+                        **kw)
+    if scheme == "transport":
+        cfg.t_end = 1.0
+    return cfg
+
+
+@pytest.mark.parametrize(
+    "scheme,nx,splits,levels,c,world,steps",
+    [("transport", 257, (8, 8), 4, 1e-3, 2, 6),
+     ("transport", 257, (8, 8), 4, 1e-3, 3, 6),   # uneven shards (3, 3, 2 rows)
+     ("lbm", 257, (8, 8), 4, 1e-3, 2, 5),
+     ("lbm", 129, (4, 4), 4, 1e-3, 4, 5),          # one patch row per shard
+     ("swe", 129, (4, 4), 4, 5e-4, 2, 8),
+     ("swe", 257, (4, 4), 4, 5e-4, 4, 6)],         # one patch row per shard, CFL max all-reduced
+)
+def test_shards_equal_single(product, scheme, nx, splits, levels, c, world, steps):
+    cfg = _cfg(scheme, nx, splits, levels, c, t_end=1.0) if scheme == "swe" else _cfg(scheme, nx, splits, levels, c)
+    g0 = api.initial_state(cfg, lib=product)
+    single = LocalShards(product, cfg, 1)
+    multi = LocalShards(product, cfg, world)
+    try:
+        single.upload(g0)
+        multi.upload(g0)
+        dt = cfg.cfl / (nx - 1) / 0.9
+        for _ in range(steps):
+            for s in single.sessions:
+                product.check(product.wg_session_step(s.handle, dt))
+            single.exchange()
+            for s in multi.sessions:
+                product.check(product.wg_session_step(s.handle, dt))
+            multi.exchange()
+        a, b = single.download(), multi.download()
+        assert np.array_equal(bits(a), bits(b)), f"{np.sum(a != b)} values differ"
+        r1 = single.rows()[0]
+        rn = multi.rows()
+        assert len(r1) == steps
+        for k in range(steps):
+            for key in ("step", "dense_bytes", "compressed_bytes", "nnz", "zeroed"):
+                assert r1[k][key] == (rn[0][k][key] if key == "step" else sum(p[k][key] for p in rn)), key
+            assert all(p[k]["time"] == r1[k]["time"] for p in rn)
+            m = sum(p[k]["global_mass"] for p in rn)
+            assert abs(m - r1[k]["global_mass"]) <= 1e-12 * abs(r1[k]["global_mass"])
+    finally:
+        single.close()
+        multi.close()
+
+
+def test_swe_single_shard_session_matches_run(product, oracle_sq):
+    """The single-shard path above is the product's own run(): cross-check
+    one SWE case against the oracle end to end."""
+    cfg = _cfg("swe", 129, (4, 4), 4, 5e-4, t_end=0.002)
+    ref = api.run(cfg, lib=oracle_sq)
+    g0 = api.initial_state(cfg, lib=product)
+    one = LocalShards(product, cfg, 1)
+    try:
+        one.upload(g0)
+        for _ in range(len(ref.rows) + 2):
+            one.step()
+        a = one.download().reshape(ref.grid.data.shape)
+        la = a[(slice(None), slice(None)) + tuple(slice(1, n + 1) for n in ref.grid.logical)]
+        assert np.array_equal(bits(la), bits(ref.grid.logical_view()))
+    finally:
+        one.close()

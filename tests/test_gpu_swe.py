@@ -133,15 +133,6 @@ def test_swe_nonpositive_depth_fails_loudly(product):
         product.wg_session_destroy(s)
 
 
-def test_swe_multi_shard_rejected(product):
-    cfg = swe_cfg(65, (2, 2), 3, 5e-4, 0.01)
-    c = cfg.to_c()
-    sh = abi.ShardC()
-    sh.rank, sh.world, sh.device, sh.row_begin, sh.row_end = 0, 2, 0, 0, 1
-    s = abi.vp()
-    assert product.wg_session_create(C.byref(c), C.byref(sh), None, C.byref(s)) == 1  # WG_INVALID_ARGUMENT
-
-
 @pytest.mark.parametrize("scheme", ["transport", "lbm", "swe"])
 def test_many_patches_per_cta(product, oracle_sq, monkeypatch, scheme):
     """Persistent CTAs looping over many patches (the large-grid regime: C2-C5
