@@ -116,6 +116,138 @@ __device__ __forceinline__ void flux_swe(const double* wl, const double* wr, int
     f[2] = fn_mom * ny + ft_mom * nx;
 }
 
+// ---- the four faces of one cell, solved in lock-step -------------------------
+// Same arithmetic as flux_swe (every value below is produced by the very
+// expression the reference evaluates, so the results are bit-identical), with
+// two changes that only remove work or add parallelism:
+//  * common subexpressions are computed once: sqrt(g h) and sqrt(g / h) are
+//    shared by both sides of the Newton function, the shock factor
+//    sqrt(g (h + hs) / (2 h hs)) by phi_side and phi_side_deriv, and
+//    sqrt(g hl), sqrt(g hr) (the cl, cr of solve_hstar) by the whole solve;
+//  * the 4 Newton iterations of a cell (faces +x, -x, +y, -y) advance
+//    together, each stopping at its own convergence (or after its own 100
+//    iterations), so a thread has 4 independent dependency chains in flight.
+// f[k] receives the flux of face k; err as flux_swe (1 domain, 2 riemann).
+__device__ __forceinline__ void swe_cell_fluxes(const double (&w)[3], const double (&wn)[4][3], double g,
+                                                double (&f)[4][3], int& err) {
+    constexpr double NX[4] = {1.0, -1.0, 0.0, 0.0}, NY[4] = {0.0, 0.0, 1.0, -1.0};
+    const double hl = w[0];
+    double hr[4], ul[4], utl[4], ur[4], utr[4], cr[4], h[4];
+    unsigned act = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        hr[k] = wn[k][0];
+        f[k][0] = f[k][1] = f[k][2] = 0.0;
+        if (hl <= 0.0 || hr[k] <= 0.0) {  // flux_godunov_swe / solve_hstar domain checks
+            err = 1;
+            continue;
+        }
+        act |= 1u << k;
+    }
+    if (!act) return;
+    const double cl = sqrt(g * hl);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        ul[k] = (w[1] * NX[k] + w[2] * NY[k]) / hl;
+        utl[k] = (-w[1] * NY[k] + w[2] * NX[k]) / hl;
+        ur[k] = (wn[k][1] * NX[k] + wn[k][2] * NY[k]) / hr[k];
+        utr[k] = (-wn[k][1] * NY[k] + wn[k][2] * NX[k]) / hr[k];
+        cr[k] = sqrt(g * hr[k]);
+        const double b = 0.5 * (cl + cr[k]) + 0.25 * (ul[k] - ur[k]);
+        const double h0 = (b * b) / g;  // std::pow(b, 2) / g
+        h[k] = (h0 < 1e-12) ? 1e-12 : h0;
+    }
+    const unsigned valid = act;
+    for (int it = 0; it < 100 && act; ++it) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            if (!((act >> k) & 1u)) continue;
+            const double hk = h[k];
+            const bool rl = hk <= hl, rr = hk <= hr[k];
+            double sgh = 0.0, sgoh = 0.0;
+            if (rl || rr) {
+                sgh = sqrt(g * hk);
+                sgoh = sqrt(g / hk);
+            }
+            double pl, dl, pr, dr;
+            if (rl) {
+                pl = 2.0 * (sgh - cl);
+                dl = sgoh;
+            } else {
+                const double a = sqrt(g * (hk + hl) / (2.0 * hk * hl));
+                pl = (hk - hl) * a;
+                dl = a - (hk - hl) * g / (4.0 * a * hk * hk);
+            }
+            if (rr) {
+                pr = 2.0 * (sgh - cr[k]);
+                dr = sgoh;
+            } else {
+                const double a = sqrt(g * (hk + hr[k]) / (2.0 * hk * hr[k]));
+                pr = (hk - hr[k]) * a;
+                dr = a - (hk - hr[k]) * g / (4.0 * a * hk * hk);
+            }
+            const double fk = pl + pr + ur[k] - ul[k];
+            const double dfk = dl + dr;
+            double dh = fk / dfk;
+            if (hk - dh <= 0.0) dh = hk / 2.0;
+            h[k] = hk - dh;
+            if (fabs(dh) < 1e-10) act &= ~(1u << k);
+        }
+    }
+    if (act) err = 2;  // SweRiemann: Newton iteration did not converge
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        if (!((valid >> k) & 1u)) continue;
+        const double hs = h[k], xi = 0.0;
+        const double cs = sqrt(g * hs);
+        const double phr = (hs <= hr[k]) ? 2.0 * (cs - cr[k])
+                                          : (hs - hr[k]) * sqrt(g * (hs + hr[k]) / (2.0 * hs * hr[k]));
+        const double phl = (hs <= hl) ? 2.0 * (cs - cl) : (hs - hl) * sqrt(g * (hs + hl) / (2.0 * hs * hl));
+        const double us = 0.5 * (ul[k] + ur[k]) + 0.5 * (phr - phl);
+        const double ut = xi <= us ? utl[k] : utr[k];
+        double H, U;
+        if (xi <= us) {
+            if (hs > hl) {
+                const double sl = ul[k] - cl * sqrt(0.5 * (hs + hl) * hs / (hl * hl));
+                if (xi <= sl) { H = hl; U = ul[k]; }
+                else { H = hs; U = us; }
+            } else {
+                const double head = ul[k] - cl, tail = us - cs;
+                if (xi <= head) { H = hl; U = ul[k]; }
+                else if (xi >= tail) { H = hs; U = us; }
+                else {
+                    const double u = (ul[k] + 2.0 * cl + 2.0 * xi) / 3.0;
+                    const double c = (ul[k] + 2.0 * cl - xi) / 3.0;
+                    H = c * c / g;
+                    U = u;
+                }
+            }
+        } else {
+            if (hs > hr[k]) {
+                const double sr = ur[k] + cr[k] * sqrt(0.5 * (hs + hr[k]) * hs / (hr[k] * hr[k]));
+                if (xi >= sr) { H = hr[k]; U = ur[k]; }
+                else { H = hs; U = us; }
+            } else {
+                const double head = ur[k] + cr[k], tail = us + cs;
+                if (xi >= head) { H = hr[k]; U = ur[k]; }
+                else if (xi <= tail) { H = hs; U = us; }
+                else {
+                    const double u = (ur[k] - 2.0 * cr[k] + 2.0 * xi) / 3.0;
+                    const double c = (-ur[k] + 2.0 * cr[k] + xi) / 3.0;
+                    H = c * c / g;
+                    U = u;
+                }
+            }
+        }
+        const double fn_mass = H * U;
+        const double fn_mom = H * U * U + 0.5 * g * H * H;
+        const double ft_mom = H * U * ut;
+        f[k][0] = fn_mass;
+        f[k][1] = fn_mom * NX[k] - ft_mom * NY[k];
+        f[k][2] = fn_mom * NY[k] + ft_mom * NX[k];
+    }
+}
+
 // ---- D2Q9 BGK (builder-defined, oracle/ref_shim.cpp) -------
 // q: 0 rest, 1 +x, 2 -x, 3 +y, 4 -y, 5 (+1,+1), 6 (-1,-1), 7 (+1,-1), 8 (-1,+1)
 __host__ __device__ constexpr int lbm_cx(int q) {

@@ -109,15 +109,19 @@ __global__ void __launch_bounds__(SweLayout<N>::NT) k_swe_step(const __grid_cons
             double w[3] = {T0[o], T1[o], T2[o]};
             double out[3] = {w[0], w[1], w[2]};
             int e = 0;
+            double wn[4][3], f[4][3];
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
                 const int on = o + di[k] * TP + dj[k];
-                const double wn[3] = {T0[on], T1[on], T2[on]};
-                double f[3];
-                flux_swe(w, wn, di[k], dj[k], a.gravity, f, e);
-#pragma unroll
-                for (int q = 0; q < 3; ++q) out[q] -= r * f[q];
+                wn[k][0] = T0[on];
+                wn[k][1] = T1[on];
+                wn[k][2] = T2[on];
             }
+            swe_cell_fluxes(w, wn, a.gravity, f, e);
+#pragma unroll
+            for (int k = 0; k < 4; ++k)  // directions in order +x, -x, +y, -y (solver.hpp:219-226)
+#pragma unroll
+                for (int q = 0; q < 3; ++q) out[q] -= r * f[k][q];
             if (e) atomicOr(a.err, e == 1 ? ERR_DOMAIN : ERR_RIEMANN);
 #pragma unroll
             for (int q = 0; q < 3; ++q) S[(size_t)q * NN + c] = out[q];
