@@ -28,11 +28,17 @@ struct LbmLayout {
     static constexpr int TILE = TP * TP;
     static constexpr int SLOTS = 3;
     static constexpr int NT = ((SLOTS * N + 31) / 32) * 32;
+    // 3 tiles + the scan buffer: 109.5 KB at N = 65, so two CTAs fit an SM
+    // (the per-patch mass reductions reuse the tiles once a patch is done)
     static constexpr size_t smem_bytes() {
-        return sizeof(double) * (size_t)(SLOTS * TILE + 2 * NT) + sizeof(unsigned long long) * NT;
+        return sizeof(double) * (size_t)(SLOTS * TILE) + sizeof(unsigned long long) * NT;
     }
     static constexpr size_t scratch_doubles() { return (size_t)9 * N * N; }
 };
+
+#ifndef WG_LBM_MIN_BLOCKS
+#define WG_LBM_MIN_BLOCKS 1
+#endif
 
 // decode + pull streaming (3 rounds of 3 populations) then BGK collide, all
 // into the scratch S; returns this thread's trapezoid mass partial of the
@@ -99,14 +105,14 @@ __device__ __forceinline__ double decode_stream_collide(const StepArgs& a, doubl
 }
 
 template <int N, int L, int MODE>
-__global__ void __launch_bounds__(LbmLayout<N>::NT) k_lbm_step(const __grid_constant__ StepArgs a) {
+__global__ void __launch_bounds__(LbmLayout<N>::NT, WG_LBM_MIN_BLOCKS) k_lbm_step(const __grid_constant__ StepArgs a) {
     using Lay = LbmLayout<N>;
     constexpr int TP = Lay::TP, TILE = Lay::TILE, NT = Lay::NT, NN = N * N;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     double* tiles = reinterpret_cast<double*>(smem_raw);
-    double* red = tiles + Lay::SLOTS * TILE;
-    double* red_fv = red + NT;
-    unsigned long long* inc = reinterpret_cast<unsigned long long*>(red_fv + NT);
+    unsigned long long* inc = reinterpret_cast<unsigned long long*>(tiles + Lay::SLOTS * TILE);
+    double* red = tiles;          // per-patch sums: tiles are free by then
+    double* red_fv = tiles + NT;
     __shared__ uint64_t slot_off[3];
     __shared__ int slot_ok[3];
     __shared__ ChunkState cs;
@@ -148,6 +154,7 @@ __global__ void __launch_bounds__(LbmLayout<N>::NT) k_lbm_step(const __grid_cons
     for (uint32_t p = blockIdx.x; p < g.npatch; p += gridDim.x) {
         const PatchPos pp = patch_pos(p, g);
         const uint32_t pn = p + gridDim.x;  // this CTA's next patch
+        double mfv = 0.0;
         if (t < 9) next_dir[t] = (MODE != MODE_INIT && pn < g.npatch) ? a.dir_in[(size_t)pn * 9 + t] : DirEntry{0, 0u, DIR_DEAD};
         if (MODE == MODE_INIT) {
             // initial state generated on the device (CUDA libm: not bit-pinned
@@ -166,9 +173,8 @@ __global__ void __launch_bounds__(LbmLayout<N>::NT) k_lbm_step(const __grid_cons
                 for (int q = 0; q < 9; ++q) S[(size_t)q * NN + c] = lbm_feq(q, 1.0, lbm_cu(q, ux, uy), usq);
             }
             __syncthreads();
-            red_fv[t] = 0.0;
         } else {
-            red_fv[t] = decode_stream_collide<N, L>(a, T, S, p, pp, s, li, lane_ok);
+            mfv = decode_stream_collide<N, L>(a, T, S, p, pp, s, li, lane_ok);
         }
         if (MODE != MODE_INIT && pn < g.npatch && lane_ok) {  // warm L2 with the next patch's inputs
             for (int q = s; q < 9; q += 3) prefetch_block<N>(a, next_dir[q], li, N);
@@ -285,7 +291,8 @@ __global__ void __launch_bounds__(LbmLayout<N>::NT) k_lbm_step(const __grid_cons
                 __syncthreads();
             }
         }
-        red[t] = m;
+        red[t] = m;  // every round / the raw path ended with a barrier: tiles are free
+        red_fv[t] = mfv;
         __syncthreads();
         if (t < 32) {
             const double mm = warp_sum_range(red, 0, NT);

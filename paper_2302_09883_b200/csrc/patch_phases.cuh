@@ -19,21 +19,21 @@ constexpr int kMaxLevels = 8;
 
 // ---- optional phase timing (tuning builds only: -DWG_PHASE_TIMING) ---------
 // Thread 0 of every CTA adds the cycles since its previous mark (i.e. the
-// wall time of the phase that just ended at a barrier) to g_phase_cycles[k].
+// wall time of the phase that just ended at a barrier) to a.phase[k] (a
+// 32-entry device buffer of the session, read by wg_debug_phase_cycles).
 #ifdef WG_PHASE_TIMING
-__device__ unsigned long long g_phase_cycles[32];
 __device__ __forceinline__ unsigned long long& phase_last() {
     __shared__ unsigned long long last;
     return last;
 }
-__device__ __forceinline__ void phase_mark(int k) {
+__device__ __forceinline__ void phase_mark(unsigned long long* buf, int k) {
     if (threadIdx.x == 0) {
         const unsigned long long t = clock64();
-        if (k >= 0) atomicAdd(&g_phase_cycles[k], t - phase_last());
+        if (k >= 0 && buf) atomicAdd(&buf[k], t - phase_last());
         phase_last() = t;
     }
 }
-#define WG_PHASE_MARK(k) ::wg::phase_mark(k)
+#define WG_PHASE_MARK(k) ::wg::phase_mark(a.phase, k)
 #else
 #define WG_PHASE_MARK(k) ((void)0)
 #endif
@@ -81,6 +81,7 @@ struct StepArgs {
     unsigned long long* swe_vmax;    // [2] max wave speed, bits of a non-negative double
     unsigned long long* swe_steps;   // steps completed on the device
     double t_end, cfl_dx, dx, gravity;
+    unsigned long long* phase;       // WG_PHASE_TIMING builds: per-phase cycle sums [32]
     double thr[(kMaxLevels + 1) * (kMaxLevels + 1)];     // T[band_i][band_j]
 };
 

@@ -144,6 +144,7 @@ struct Session {
     uint64_t device_bytes = 0;
     // SWE device clock: [t, last dt] (f64), vmax bits [2], steps done (u64)
     unsigned long long* swe = nullptr;
+    unsigned long long* phase = nullptr;  // WG_PHASE_TIMING builds only
     uint64_t launched = 0;  // SWE step launches (steps past t_end are no-ops)
 
     int cur = 0;  // pool/edges holding the current state
@@ -200,6 +201,8 @@ struct Session {
         cudaFree(mass_fv);
         cudaFree(swe);
         swe = nullptr;
+        cudaFree(phase);
+        phase = nullptr;
         partials = nullptr;
         done = nullptr;
         bump = nullptr;
@@ -312,6 +315,10 @@ struct Session {
             swe = dalloc<unsigned long long>(5);
             WG_CUDA(cudaMemsetAsync(swe, 0, 5 * sizeof(unsigned long long), stream));
         }
+#ifdef WG_PHASE_TIMING
+        phase = dalloc<unsigned long long>(32);
+        WG_CUDA(cudaMemsetAsync(phase, 0, 32 * sizeof(unsigned long long), stream));
+#endif
         grow_rows(1024);
     }
 
@@ -424,6 +431,7 @@ struct Session {
         a.compress = cfg.no_compression ? 0 : 1;
         a.thr_any = (cfg.c > 0.0 && levels > 0) ? 1 : 0;
         a.dense_bytes = (uint64_t)sg.npatch * 8ull * N * N * sg.m;
+        a.phase = phase;
         if (is_swe()) {
             a.swe_td = swe_td();
             a.swe_vmax = swe + 2;
@@ -650,21 +658,17 @@ wg_status wg_session_last_row(wg_session* sp, wg_metrics_row* row) {
 }
 
 // Tuning builds (-DWG_PHASE_TIMING) only: summed per-phase cycles of thread 0
-// of every CTA; `reset` zeroes them.  Not part of the product ABI.
-wg_status wg_debug_phase_cycles(uint64_t* out, int32_t n, int32_t reset) {
+// of every CTA of the session's step launches; `reset` zeroes them.  Not
+// part of the product ABI.
+wg_status wg_debug_phase_cycles(wg_session* sp, uint64_t* out, int32_t n, int32_t reset) {
     return guard([&] {
-#ifdef WG_PHASE_TIMING
+        Session* s = reinterpret_cast<Session*>(sp);
+        if (!s->phase) raise(WG_LOGIC, "built without WG_PHASE_TIMING");
+        s->sync();
         unsigned long long h[32];
-        WG_CUDA(cudaMemcpyFromSymbol(h, g_phase_cycles, sizeof h));
+        WG_CUDA(cudaMemcpy(h, s->phase, sizeof h, cudaMemcpyDeviceToHost));
         for (int k = 0; k < n && k < 32; ++k) out[k] = h[k];
-        if (reset) {
-            std::memset(h, 0, sizeof h);
-            WG_CUDA(cudaMemcpyToSymbol(g_phase_cycles, h, sizeof h));
-        }
-#else
-        (void)out; (void)n; (void)reset;
-        raise(WG_LOGIC, "built without WG_PHASE_TIMING");
-#endif
+        if (reset) WG_CUDA(cudaMemset(s->phase, 0, sizeof h));
     });
 }
 

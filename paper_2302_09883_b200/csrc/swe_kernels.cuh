@@ -35,8 +35,12 @@ struct SweLayout {
     static constexpr size_t scratch_doubles() { return (size_t)3 * N * N; }
 };
 
+#ifndef WG_SWE_MIN_BLOCKS
+#define WG_SWE_MIN_BLOCKS 2  // 2 CTAs per SM (spills in the lifting phases, +44% C3)
+#endif
+
 template <int N, int L, int MODE>
-__global__ void __launch_bounds__(SweLayout<N>::NT) k_swe_step(const __grid_constant__ StepArgs a) {
+__global__ void __launch_bounds__(SweLayout<N>::NT, WG_SWE_MIN_BLOCKS) k_swe_step(const __grid_constant__ StepArgs a) {
     using Lay = SweLayout<N>;
     constexpr int TP = Lay::TP, TILE = Lay::TILE, NT = Lay::NT, NN = N * N;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -82,6 +86,7 @@ __global__ void __launch_bounds__(SweLayout<N>::NT) k_swe_step(const __grid_cons
     StepPartial part{0, 0, 0, 0.0, 0.0};
     double macc = 0.0, mfacc = 0.0, vmax = 0.0;
     if (t == 0) cs.cur = cs.end = 0;
+    WG_PHASE_MARK(-1);
     for (uint32_t p = blockIdx.x; p < g.npatch; p += gridDim.x) {
         const PatchPos pp = patch_pos(p, g);
         // ---- decode h, hu, hv + ghost ring --------------------------------
@@ -91,12 +96,14 @@ __global__ void __launch_bounds__(SweLayout<N>::NT) k_swe_step(const __grid_cons
             fill_ghosts<N>(T, li, a.ein, pp, s, g);
         }
         __syncthreads();
+        WG_PHASE_MARK(0);
         if (lane_ok && !raw_in) {
             double v[N];
             decode_col<N, L>(T, li, false, v);
             store_col<N>(T, li, v);
         }
         __syncthreads();
+        WG_PHASE_MARK(1);
         // ---- Godunov FV (fv_step<SweFlux>, solver.hpp:207-231) -------------
         const double* T0 = tiles;
         const double* T1 = tiles + TILE;
@@ -130,6 +137,7 @@ __global__ void __launch_bounds__(SweLayout<N>::NT) k_swe_step(const __grid_cons
         }
         mfacc += mfv;
         __syncthreads();
+        WG_PHASE_MARK(2);
 
         double m = 0.0;
         bool store_raw = !a.compress;
@@ -147,6 +155,7 @@ __global__ void __launch_bounds__(SweLayout<N>::NT) k_swe_step(const __grid_cons
                 fwd_col_to_tile<N, L>(T, li, v);
             }
             __syncthreads();
+            WG_PHASE_MARK(4);
             unsigned nz = 0, zr = 0;
             if (lane_ok) fwd_row_threshold<N, L>(T, li, a.thr, v, nz, zr);
             cta_inclusive_scan<NT>(((unsigned long long)zr << 32) | nz, inc);
@@ -177,6 +186,7 @@ __global__ void __launch_bounds__(SweLayout<N>::NT) k_swe_step(const __grid_cons
                 part.zeroed += patch_zero;
             }
             __syncthreads();
+            WG_PHASE_MARK(5);
             store_raw = patch_zero == 0;
             const bool ok = lane_ok && slot_ok[s];
             if (ok) {
@@ -186,14 +196,17 @@ __global__ void __launch_bounds__(SweLayout<N>::NT) k_swe_step(const __grid_cons
                 inv_row_to_tile<N, L>(T, li, v);
             }
             __syncthreads();
+            WG_PHASE_MARK(7);
             if (ok) {
                 decode_col<N, L>(T, li, false, v);
                 write_edges<N>(a.eout, pp, s, g, li, v);
                 if (s == 0) m += col_mass<N>(li, v);
             }
             __syncthreads();
+            WG_PHASE_MARK(8);
             if (ok) store_col<N>(T, li, v);  // the new state, for the wave speed
             __syncthreads();
+            WG_PHASE_MARK(13);
             if (!store_raw) {
                 for (int c = t; c < NN; c += NT) {
                     const int o = (c / N + 1) * TP + c - (c / N) * N + 1;
@@ -204,6 +217,7 @@ __global__ void __launch_bounds__(SweLayout<N>::NT) k_swe_step(const __grid_cons
                     vmax = fmax(vmax, fmax(u + cc, w2 + cc));
                 }
                 __syncthreads();  // the next patch's decode overwrites the tiles
+                WG_PHASE_MARK(14);
             }
         }
         if (store_raw) {  // raw store of the FV output (skip rule / no_compression)
@@ -237,6 +251,7 @@ __global__ void __launch_bounds__(SweLayout<N>::NT) k_swe_step(const __grid_cons
                 vmax = fmax(vmax, fmax(u + cc, w2 + cc));
             }
             __syncthreads();
+            WG_PHASE_MARK(9);
         }
         macc += m;
     }
@@ -253,6 +268,7 @@ __global__ void __launch_bounds__(SweLayout<N>::NT) k_swe_step(const __grid_cons
     if (t == 0)
         for (int w = 0; w < NT / 32; ++w) cta_v = fmax(cta_v, wmax[w]);
     finalize_step(a, tot, cta_v, &clk);
+    WG_PHASE_MARK(11);
 }
 
 }  // namespace wg

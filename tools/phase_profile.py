@@ -21,13 +21,16 @@ LBM_NAMES = {0: "decode rows (round 0)", 12: "decode rows (rounds 1,2)", 1: "dec
 NAMES = {0: "decode rows+ghosts", 1: "decode cols", 2: "FV + mass", 3: "sync before fwd", 4: "fwd col DWT",
          5: "row DWT+thr+scan", 6: "alloc", 7: "CSR write + row inv", 8: "col recon+edges", 9: "raw store",
          10: "group sums", 11: "finalize"}
+SWE_NAMES = {0: "decode rows+ghosts", 1: "decode cols", 2: "Godunov FV + mass", 4: "fwd col DWT",
+             5: "row DWT+thr+scan", 6: "alloc", 7: "CSR write + row inv", 8: "col recon+edges",
+             13: "store tile", 14: "wave speed", 9: "raw store", 11: "finalize"}
 ap = argparse.ArgumentParser()
 ap.add_argument("--workload", default="transport_4k_p33")
 ap.add_argument("--steps", type=int, default=10)
 args = ap.parse_args()
 w = bench.WORKLOADS[args.workload]
 lib = abi.load_product()
-lib.dll.wg_debug_phase_cycles.argtypes = [C.POINTER(C.c_uint64), C.c_int32, C.c_int32]
+lib.dll.wg_debug_phase_cycles.argtypes = [C.c_void_p, C.POINTER(C.c_uint64), C.c_int32, C.c_int32]
 cfg = bench.run_config(w, args.steps + 3)
 dt = bench.transport_dt(cfg) if w["scheme"] == "transport" else 1.0
 grid = api.initial_state(cfg, lib=lib)
@@ -37,16 +40,16 @@ for _ in range(3):
     sess.step(dt)
 sess.sync()
 buf = (C.c_uint64 * 32)()
-lib.check(lib.dll.wg_debug_phase_cycles(buf, 32, 1))
+lib.check(lib.dll.wg_debug_phase_cycles(sess.handle, buf, 32, 1))
 for _ in range(args.steps):
     sess.step(dt)
 sess.sync()
-lib.check(lib.dll.wg_debug_phase_cycles(buf, 32, 0))
-tot = sum(buf[:16])
+lib.check(lib.dll.wg_debug_phase_cycles(sess.handle, buf, 32, 0))
+tot = sum(buf[:32])
 ctas = sess.info  # noqa
 print(f"{args.workload}: total thread0 cycles {tot:.3e} over {args.steps} steps")
-for k in range(16):
+for k in range(32):
     if buf[k]:
-        nm = (LBM_NAMES if w["scheme"] == "lbm" else NAMES).get(k, "?")
+        nm = {"lbm": LBM_NAMES, "swe": SWE_NAMES}.get(w["scheme"], NAMES).get(k, "?")
         print(f"  {k:2d} {nm:26s} {100 * buf[k] / tot:5.1f}%")
 sess.close()
