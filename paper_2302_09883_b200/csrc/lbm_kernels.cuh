@@ -48,14 +48,20 @@ __device__ __forceinline__ double decode_stream_collide(const StepArgs& a, doubl
                                                         const PatchPos& pp, int s, int li, bool lane_ok) {
     using Lay = LbmLayout<N>;
     constexpr int TP = Lay::TP, NT = Lay::NT, NN = N * N;
+    // ROW phase thread mapping: rows interleaved over the 3 slots (thread t
+    // takes row t / 3 of slot t % 3), so the coarse rows that hold the few
+    // surviving coefficients share warps and the warps of empty detail rows
+    // skip their transforms (decode_row)
+    const int rs = threadIdx.x % 3, rli = threadIdx.x / 3;
+    double* TR = T + (rs - s) * (Lay::TILE);
     for (int rd = 0; rd < 3; ++rd) {
         const int q = 3 * rd + s;
-        bool raw_in = false;
         if (lane_ok) {
-            raw_in = decode_row<N, L>(T, li, a.dir_in[(size_t)p * 9 + q], a.store_in);
-            fill_ghosts_lbm<N>(T, li, a.ein, pp, q, a.g);
+            decode_row<N, L>(TR, rli, a.dir_in[(size_t)p * 9 + 3 * rd + rs], a.store_in);
+            fill_ghosts_lbm<N>(TR, rli, a.ein, pp, 3 * rd + rs, a.g);
         }
         __syncthreads();
+        const bool raw_in = (a.dir_in[(size_t)p * 9 + q].flags & (DIR_RAW | DIR_DEAD)) != 0;
         if (lane_ok && !raw_in) {
             double v[N];
             decode_col<N, L>(T, li, false, v);
@@ -245,8 +251,12 @@ __global__ void __launch_bounds__(LbmLayout<N>::NT, WG_LBM_MIN_BLOCKS) k_lbm_ste
                 WG_PHASE_MARK(6);
                 if (ok) {
                     decode_col<N, L>(T, li, false, v);
-                    write_edges_lbm<N>(a.eout, pp, q, g, li, v);
-                    m += col_mass<N>(li, v);
+                    store_col<N>(T, li, v);
+                }
+                __syncthreads();
+                if (ok) {  // edges and mass from the tile: no register line live
+                    write_edges_lbm_tile<N>(a.eout, pp, q, g, li, T);
+                    m += tile_col_mass<N>(T, li);
                 }
                 __syncthreads();
                 WG_PHASE_MARK(7);
@@ -275,18 +285,20 @@ __global__ void __launch_bounds__(LbmLayout<N>::NT, WG_LBM_MIN_BLOCKS) k_lbm_ste
                     }
                 }
                 __syncthreads();
-                if (lane_ok) {
+                if (lane_ok) {  // through the tile: no register line live
                     const int j = li;
-                    double v[N];
-#pragma unroll
-                    for (int i = 0; i < N; ++i) v[i] = S[(size_t)q * NN + i * N + j];
-                    if (slot_ok[s]) {
-                        double* d = reinterpret_cast<double*>(a.store_out + slot_off[s]);
-#pragma unroll
-                        for (int i = 0; i < N; ++i) d[i * N + j] = v[i];
+                    double* d = slot_ok[s] ? reinterpret_cast<double*>(a.store_out + slot_off[s]) : nullptr;
+#pragma unroll 5
+                    for (int i = 0; i < N; ++i) {
+                        const double x = S[(size_t)q * NN + i * N + j];
+                        T[(i + 1) * Lay::TP + j + 1] = x;
+                        if (d) d[i * N + j] = x;
                     }
-                    write_edges_lbm<N>(a.eout, pp, q, g, j, v);
-                    m += col_mass<N>(j, v);
+                }
+                __syncthreads();
+                if (lane_ok) {
+                    write_edges_lbm_tile<N>(a.eout, pp, q, g, li, T);
+                    m += tile_col_mass<N>(T, li);
                 }
                 __syncthreads();
             }

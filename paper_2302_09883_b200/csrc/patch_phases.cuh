@@ -138,6 +138,11 @@ __device__ __forceinline__ bool decode_row(double* T, int li, const DirEntry e,
         const uint32_t k0 = ro[li], k1 = ro[li + 1];
 #pragma unroll
         for (int j = 0; j < N; ++j) rowp[j] = 0.0;
+        // an empty row inverse-transforms to +0.0 everywhere (every lifting
+        // step maps zeros to +0.0): nothing more to do.  Well-compressed
+        // patches keep their few coefficients in the coarse rows, so whole
+        // warps of detail rows take this exit.
+        if (k0 == k1) return false;
         for (uint32_t k = k0; k < k1; ++k) rowp[col[k]] = v[k];
         double x[N];
 #pragma unroll
@@ -313,6 +318,35 @@ __device__ __forceinline__ void write_edges_lbm(const EdgeSet& e, const PatchPos
 #pragma unroll
         for (int i = 0; i < N; ++i) d[i] = v[i];
     }
+}
+
+// D2Q9 edge lines of component q from the reconstructed TILE (logical cells
+// at (i+1, j+1)); thread li writes element li of every line it owns, so the
+// column lines are written in parallel and no register line stays live.
+template <int N>
+__device__ __forceinline__ void write_edges_lbm_tile(const EdgeSet& e, const PatchPos& pp, int q, const ShardGeom& g,
+                                                     int li, const double* T) {
+    constexpr int TP = N + 2;
+    const int cxq = lbm_cx(q), cyq = lbm_cy(q);
+    if (cxq == -1) e.rowlo[edge_ix((uint32_t)(pp.ar + 1), pp.b, lbm_slot_rowlo(q), g, N) + li] = T[2 * TP + li + 1];
+    if (cxq == 1)
+        e.rowhi[edge_ix((uint32_t)(pp.ar + 1), pp.b, lbm_slot_rowhi(q), g, N) + li] = T[(N - 1) * TP + li + 1];
+    if (cyq == -1) e.collo[edge_ix((uint32_t)pp.ar, pp.b, lbm_slot_collo(q), g, N) + li] = T[(li + 1) * TP + 2];
+    if (cyq == 1) e.colhi[edge_ix((uint32_t)pp.ar, pp.b, lbm_slot_colhi(q), g, N) + li] = T[(li + 1) * TP + N - 1];
+}
+
+// col_mass of tile column j (same weights and association).
+template <int N>
+__device__ __forceinline__ double tile_col_mass(const double* T, int j) {
+    constexpr int TP = N + 2;
+    const double wj = (j == 0 || j == N - 1) ? 0.5 : 1.0;
+    double m[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+        const double wi = (i == 0 || i == N - 1) ? 0.5 : 1.0;
+        m[i & 3] += (wi * wj) * T[(i + 1) * TP + j + 1];
+    }
+    return (m[0] + m[1]) + (m[2] + m[3]);
 }
 
 // Trapezoid-weighted column sum (global_mass weights, patchgrid.hpp:244-266),
