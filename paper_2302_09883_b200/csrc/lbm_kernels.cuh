@@ -57,11 +57,21 @@ __device__ __forceinline__ double decode_stream_collide(const StepArgs& a, doubl
     for (int rd = 0; rd < 3; ++rd) {
         const int q = 3 * rd + s;
         if (lane_ok) {
+#ifdef WG_BOUNDS_CHECK
+            {
+                const DirEntry e = a.dir_in[(size_t)p * 9 + 3 * rd + rs];
+                const uint64_t bytes = (e.flags & DIR_RAW) ? 8ull * N * N : 12ull * e.nnz + 4ull * (N + 1);
+                WG_CHECK((e.flags & DIR_DEAD) || e.off + bytes <= a.cap_out, 6);
+                WG_CHECK(p < a.g.npatch, 7);
+            }
+#endif
             decode_row<N, L>(TR, rli, a.dir_in[(size_t)p * 9 + 3 * rd + rs], a.store_in);
             fill_ghosts_lbm<N>(TR, rli, a.ein, pp, 3 * rd + rs, a.g);
         }
         __syncthreads();
-        const bool raw_in = (a.dir_in[(size_t)p * 9 + q].flags & (DIR_RAW | DIR_DEAD)) != 0;
+        // (threads past the 3 slots have q = 9..11: they must not read — the
+        // last patch's q = 9 lies past the end of the directory)
+        const bool raw_in = lane_ok && (a.dir_in[(size_t)p * 9 + q].flags & (DIR_RAW | DIR_DEAD)) != 0;
         if (lane_ok && !raw_in) {
             double v[N];
             decode_col<N, L>(T, li, false, v);
@@ -244,6 +254,7 @@ __global__ void __launch_bounds__(LbmLayout<N>::NT, WG_LBM_MIN_BLOCKS) k_lbm_ste
                 if (ok) {
                     const unsigned long long base = s == 0 ? 0ull : inc[s * N - 1];
                     const uint32_t k = (uint32_t)((inc[t] - base) & 0xffffffffu) - nz;
+                    WG_CHECK(slot_off[s] + 12ull * comp_nnz[s] + 4ull * (N + 1) <= a.cap_out && k + nz <= comp_nnz[s], 10);
                     write_csr_row<N, L>(a.store_out + slot_off[s], comp_nnz[s], li, k, nz, v);
                     inv_row_to_tile<N, L>(T, li, v);
                 }
@@ -255,6 +266,8 @@ __global__ void __launch_bounds__(LbmLayout<N>::NT, WG_LBM_MIN_BLOCKS) k_lbm_ste
                 }
                 __syncthreads();
                 if (ok) {  // edges and mass from the tile: no register line live
+                    WG_CHECK(edge_ix((uint32_t)(pp.ar + 1), pp.b, 2, g, N) + N <= a.edge_row_elems, 8);
+                    WG_CHECK(edge_ix((uint32_t)pp.ar, pp.b, 2, g, N) + N <= a.edge_col_elems, 9);
                     write_edges_lbm_tile<N>(a.eout, pp, q, g, li, T);
                     m += tile_col_mass<N>(T, li);
                 }

@@ -38,6 +38,20 @@ __device__ __forceinline__ void phase_mark(unsigned long long* buf, int k) {
 #define WG_PHASE_MARK(k) ((void)0)
 #endif
 
+// ---- optional device bounds checks (debug builds only: -DWG_BOUNDS_CHECK) ---
+#ifdef WG_BOUNDS_CHECK
+#define WG_CHECK(cond, code)                                                                   \
+    do {                                                                                       \
+        if (!(cond)) {                                                                         \
+            printf("WG_CHECK %d failed: block %d thread %d (%s:%d)\n", (code), blockIdx.x,     \
+                   threadIdx.x, __FILE__, __LINE__);                                           \
+            __trap();                                                                          \
+        }                                                                                      \
+    } while (0)
+#else
+#define WG_CHECK(cond, code) ((void)0)
+#endif
+
 // Per-CTA partial sums of the step metrics (fixed order inside the CTA).
 struct StepPartial {
     unsigned long long comp_bytes, nnz, zeroed;
@@ -54,6 +68,7 @@ struct StepArgs {
     unsigned long long* bump_out;
     unsigned long long* bump_next;  // pool written by the next step: reset by the last CTA
     uint64_t cap_out;
+    uint64_t edge_row_elems, edge_col_elems;  // sizes of the edge line arrays (bounds checks)
     uint64_t chunk;                 // per-CTA sub-allocation chunk of the output pool (bytes)
     unsigned* err;
     double* decode_out;   // MODE_DECODE: grid buffer (true layout) of this shard
@@ -136,6 +151,7 @@ __device__ __forceinline__ bool decode_row(double* T, int li, const DirEntry e,
         const uint32_t* col = reinterpret_cast<const uint32_t*>(base + 8ull * e.nnz);
         const uint32_t* ro = col + e.nnz;
         const uint32_t k0 = ro[li], k1 = ro[li + 1];
+        WG_CHECK(k0 <= k1 && k1 <= e.nnz && e.nnz <= (uint32_t)(N * N), 1);
 #pragma unroll
         for (int j = 0; j < N; ++j) rowp[j] = 0.0;
         // an empty row inverse-transforms to +0.0 everywhere (every lifting
@@ -143,7 +159,10 @@ __device__ __forceinline__ bool decode_row(double* T, int li, const DirEntry e,
         // patches keep their few coefficients in the coarse rows, so whole
         // warps of detail rows take this exit.
         if (k0 == k1) return false;
-        for (uint32_t k = k0; k < k1; ++k) rowp[col[k]] = v[k];
+        for (uint32_t k = k0; k < k1; ++k) {
+            WG_CHECK(col[k] < (uint32_t)N, 2);
+            rowp[col[k]] = v[k];
+        }
         double x[N];
 #pragma unroll
         for (int r = 0; r < N; ++r) x[r] = rowp[corner_pos<N, L>(r)];
@@ -290,6 +309,8 @@ __device__ __forceinline__ void fill_ghosts_lbm(double* T, int li, const EdgeSet
                                                 const ShardGeom& g) {
     constexpr int TP = N + 2;
     const int cxq = lbm_cx(q), cyq = lbm_cy(q);
+    WG_CHECK(pp.su <= g.R + 1 && pp.sd <= g.R + 1 && pp.b < g.P1 && pp.bl < g.P1 && pp.br < g.P1 && pp.ar >= 0 &&
+                 (uint32_t)pp.ar < g.R, 3);
     if (cxq == 1) T[li + 1] = e.rowhi[edge_ix(pp.su, pp.b, lbm_slot_rowhi(q), g, N) + li];
     if (cxq == -1) T[(N + 1) * TP + li + 1] = e.rowlo[edge_ix(pp.sd, pp.b, lbm_slot_rowlo(q), g, N) + li];
     if (cyq == 1) T[(li + 1) * TP] = e.colhi[edge_ix(pp.ar, pp.bl, lbm_slot_colhi(q), g, N) + li];
@@ -458,6 +479,7 @@ __device__ __forceinline__ unsigned long long chunk_alloc(const StepArgs& a, Chu
     }
     const unsigned long long off = cs.cur;
     cs.cur += bytes;
+    WG_CHECK(off + bytes <= a.cap_out, 5);
     return off;
 }
 

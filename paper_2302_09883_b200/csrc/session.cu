@@ -422,6 +422,8 @@ struct Session {
         a.bump_out = bump + dst;
         a.bump_next = bump + src;
         a.cap_out = cap;
+        a.edge_row_elems = (uint64_t)(sg.R + 2) * sg.P1 * sg.me * N;
+        a.edge_col_elems = (uint64_t)sg.R * sg.P1 * sg.me * N;
         a.chunk = chunk;
         a.err = err;
         a.partials = partials;

@@ -287,3 +287,18 @@ def test_pinned_upload_equals_pageable(product):
     a, ra = _run_session(product, cfg, g0, 3, dt)
     b, rb = _run_session(product, cfg, pinned.numpy(), 3, dt)
     assert np.array_equal(bits(a), bits(b)) and ra == rb
+
+
+def test_lbm_directory_ends_on_page_boundary(product):
+    """512^2 patches x 9 populations x 16 B = 36 MiB of directory, ending
+    exactly on a 2 MiB page: a read past the last patch's entries faults
+    (regression: idle threads of the last patch read entry 9)."""
+    cfg = lbm_cfg(8193, (512, 512), 3, 1e-3, 2)
+    s = _session(product, cfg)
+    try:
+        product.check(product.wg_session_init_device(s))
+        for _ in range(2):
+            product.check(product.wg_session_step(s, 1.0))
+        product.check(product.wg_session_sync(s))
+    finally:
+        product.wg_session_destroy(s)
