@@ -44,6 +44,9 @@ WORKLOADS = {
     # BASELINE.json configs[1] (C2)
     "lbm_c2": dict(scheme="lbm", components=9, nx=1025, splits=(16, 16), levels=4, c=1e-3, mode="capped",
                    scaling="weak"),
+    # C2 grid in 32^2-cell patches (occupancy study: 33-point lines need half the registers)
+    "lbm_c2_p33": dict(scheme="lbm", components=9, nx=1025, splits=(32, 32), levels=4, c=1e-3, mode="capped",
+                       scaling="weak"),
     # BASELINE.json configs[0] (C1): the reference's own CPU-runnable case
     "transport_c1": dict(scheme="transport", components=1, nx=257, splits=(8, 8), levels=4, c=1e-3, mode="capped"),
     # BASELINE.json configs[3] (C4): 16384^2 D2Q9 on one GPU; the raw f-field

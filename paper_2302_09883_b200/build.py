@@ -80,6 +80,9 @@ def build_oracles(reference: bool = True) -> None:
     if reference and Path("/root/reference/proj/include/wavegrid").is_dir():
         targets.append("ref")
     subprocess.run(["make", "-s", "-C", str(REPO / "oracle"), *targets], check=True)
+    if "ref" in targets and LIB.exists():
+        # the C++ drop-in test programs need the reference headers (here only)
+        subprocess.run(["make", "-s", "-C", str(REPO / "tests" / "cpp"), "all"], check=True)
 
 
 if __name__ == "__main__":

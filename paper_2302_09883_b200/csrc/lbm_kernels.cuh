@@ -56,7 +56,11 @@ __device__ __forceinline__ double decode_stream_collide(const StepArgs& a, doubl
     double* TR = T + (rs - s) * (Lay::TILE);
     for (int rd = 0; rd < 3; ++rd) {
         const int q = 3 * rd + s;
+#ifdef WG_ABL_NO_DECODE
+        if (false) {
+#else
         if (lane_ok) {
+#endif
 #ifdef WG_BOUNDS_CHECK
             {
                 const DirEntry e = a.dir_in[(size_t)p * 9 + 3 * rd + rs];
@@ -72,14 +76,22 @@ __device__ __forceinline__ double decode_stream_collide(const StepArgs& a, doubl
         // (threads past the 3 slots have q = 9..11: they must not read — the
         // last patch's q = 9 lies past the end of the directory)
         const bool raw_in = lane_ok && (a.dir_in[(size_t)p * 9 + q].flags & (DIR_RAW | DIR_DEAD)) != 0;
+#ifdef WG_ABL_NO_DECODE
+        if (false) {
+#else
         if (lane_ok && !raw_in) {
+#endif
             double v[N];
             decode_col<N, L>(T, li, false, v);
             store_col<N>(T, li, v);
         }
         __syncthreads();
         WG_PHASE_MARK(rd == 0 ? 0 : 12);
+#ifdef WG_ABL_NO_STREAM
+        if (false) {
+#else
         if (lane_ok) {  // pull streaming f_q(x) <- f_q(x - c_q), ghost ring included
+#endif
             const int cx = lbm_cx(q), cy = lbm_cy(q);
             double* Sq = S + (size_t)q * NN;
             const int j = li;
@@ -91,6 +103,9 @@ __device__ __forceinline__ double decode_stream_collide(const StepArgs& a, doubl
     }
     double mfv = 0.0;
     // two cells per iteration: 18 independent scratch loads in flight
+#ifdef WG_ABL_NO_COLLIDE
+    if (false)
+#endif
     for (int c0 = threadIdx.x; c0 < NN; c0 += 2 * NT) {
         const int c1 = c0 + NT;
         const bool two = c1 < NN;
@@ -256,20 +271,20 @@ __global__ void __launch_bounds__(LbmLayout<N>::NT, WG_LBM_MIN_BLOCKS) k_lbm_ste
                     const uint32_t k = (uint32_t)((inc[t] - base) & 0xffffffffu) - nz;
                     WG_CHECK(slot_off[s] + 12ull * comp_nnz[s] + 4ull * (N + 1) <= a.cap_out && k + nz <= comp_nnz[s], 10);
                     write_csr_row<N, L>(a.store_out + slot_off[s], comp_nnz[s], li, k, nz, v);
-                    inv_row_to_tile<N, L>(T, li, v);
+                    inv_row_to_tile<N, L>(T, li, v, nz);
                 }
                 __syncthreads();
                 WG_PHASE_MARK(6);
                 if (ok) {
                     decode_col<N, L>(T, li, false, v);
+                    m += col_mass<N>(li, v);
                     store_col<N>(T, li, v);
                 }
                 __syncthreads();
-                if (ok) {  // edges and mass from the tile: no register line live
+                if (ok) {  // edges from the tile: no register line live
                     WG_CHECK(edge_ix((uint32_t)(pp.ar + 1), pp.b, 2, g, N) + N <= a.edge_row_elems, 8);
                     WG_CHECK(edge_ix((uint32_t)pp.ar, pp.b, 2, g, N) + N <= a.edge_col_elems, 9);
                     write_edges_lbm_tile<N>(a.eout, pp, q, g, li, T);
-                    m += tile_col_mass<N>(T, li);
                 }
                 __syncthreads();
                 WG_PHASE_MARK(7);

@@ -228,7 +228,7 @@ __global__ void __launch_bounds__(Layout<N, P>::NT, WG_MIN_BLOCKS)
                 const uint32_t k = (uint32_t)((inc[t] - base) & 0xffffffffu) - nz;
                 const uint32_t snz = (uint32_t)((inc[ps * N + N - 1] - base) & 0xffffffffu);
                 write_csr_row<N, L>(a.store_out + slot_off[ps], snz, li, k, nz, v);
-                inv_row_to_tile<N, L>(T, li, v);  // reconstruction, dim 1 inverse
+                inv_row_to_tile<N, L>(T, li, v, nz);  // reconstruction, dim 1 inverse
             }
             __syncthreads();
             WG_PHASE_MARK(7);

@@ -265,6 +265,7 @@ __device__ __forceinline__ void write_csr_row(unsigned char* base, uint32_t nnz_
     uint32_t* ro = co + nnz_tot;
     if (i == 0) ro[0] = 0;
     ro[i + 1] = k + nz;
+    if (nz == 0) return;  // empty row (most detail rows of a well-compressed patch)
 #pragma unroll
     for (int pc = 0; pc < N; ++pc) {
         const double x = v[interleaved_of<N, L>(pc)];
@@ -278,8 +279,13 @@ __device__ __forceinline__ void write_csr_row(unsigned char* base, uint32_t nnz_
 
 // Inverse transform of a thresholded register row, stored into the tile.
 template <int N, int L>
-__device__ __forceinline__ void inv_row_to_tile(double* T, int i, double (&v)[N]) {
+__device__ __forceinline__ void inv_row_to_tile(double* T, int i, double (&v)[N], unsigned nz = ~0u) {
     constexpr int TP = N + 2;
+    if (nz == 0) {  // all coefficients zero: the inverse is +0.0 everywhere
+#pragma unroll
+        for (int jj = 0; jj < N; ++jj) T[(i + 1) * TP + jj + 1] = 0.0;
+        return;
+    }
     idwt_line_reg<N, L>(v);
 #pragma unroll
     for (int jj = 0; jj < N; ++jj) T[(i + 1) * TP + jj + 1] = v[jj];

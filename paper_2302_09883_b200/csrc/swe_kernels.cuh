@@ -193,7 +193,7 @@ __global__ void __launch_bounds__(SweLayout<N>::NT, WG_SWE_MIN_BLOCKS) k_swe_ste
                 const unsigned long long base = s == 0 ? 0ull : inc[s * N - 1];
                 const uint32_t k = (uint32_t)((inc[t] - base) & 0xffffffffu) - nz;
                 write_csr_row<N, L>(a.store_out + slot_off[s], comp_nnz[s], li, k, nz, v);
-                inv_row_to_tile<N, L>(T, li, v);
+                inv_row_to_tile<N, L>(T, li, v, nz);
             }
             __syncthreads();
             WG_PHASE_MARK(7);
