@@ -265,6 +265,19 @@ wg_status wg_session_init_device(wg_session* s);
  * wg_session_metrics reports the steps actually taken. */
 wg_status wg_session_step(wg_session* s, double dt);
 
+/* Checkpoint / resume straight from the compressed store.
+ * The file is a "WGS1" header (configuration, shard, step, time, SWE
+ * clock) followed by one WGC1 record per patch in the reference's
+ * container format (save_wgc, codec.hpp:364-391): compressed patches as
+ * Codec::csr records holding their CSR blocks byte for byte, raw patches
+ * (skip rule, initial state) as Codec::lz records with levels 0 made of
+ * literal-only LZ sequences, so load_wgc/decode_patch of the reference
+ * read every record.  wg_session_load restores a session created with the
+ * same configuration and shard; stepping on continues bit-identically.
+ * wg_session_metrics then reports the rows of the steps after the load. */
+wg_status wg_session_save(wg_session* s, const char* path);
+wg_status wg_session_load(wg_session* s, const char* path);
+
 /* SWE, world > 1: the max wave speed the NEXT step's dt is computed from
  * (IEEE bits of a non-negative double, so an int64 MAX is the double max).
  * Multi-GPU callers all-reduce it with MAX after every upload and step —

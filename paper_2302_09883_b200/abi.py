@@ -218,6 +218,8 @@ _PROTOS = {
     "wg_session_step": (i32, [vp, f64]),
     "wg_session_halo": (i32, [vp, P(vp), P(vp), P(vp), P(vp)]),
     "wg_session_cfl_vmax": (i32, [vp, P(vp)]),
+    "wg_session_save": (i32, [vp, C.c_char_p]),
+    "wg_session_load": (i32, [vp, C.c_char_p]),
     "wg_session_metrics": (i32, [vp, P(MetricsRowC), u64, P(u64)]),
     "wg_session_last_row": (i32, [vp, P(MetricsRowC)]),
     "wg_session_download": (i32, [vp, dp]),

@@ -120,6 +120,139 @@ def csr_encode(dense, rows: int, cols: int, lib=None) -> CsrBlock:
     return CsrBlock(v[:k].copy(), col[:k].copy(), row, rows, cols)
 
 
+@dataclass
+class CompressedPatch:  # codec.hpp:259-277
+    codec: int                     # 1 = csr, 2 = lz
+    dims: tuple
+    components: int
+    levels: int
+    csr: list                      # CsrBlock per component (codec csr)
+    lz: list                       # per component: (chunk_size, [(raw_len, payload bytes)]) (codec lz)
+
+
+def lz_decode_stream(stream) -> bytes:
+    """lz_decode (codec.hpp:177-244) of one LzStream: token = literal count
+    (high nibble) | match length - 4 (low nibble), 255-extended lengths,
+    literals, 2-byte little-endian offset; the chunk ends after its literals
+    once raw_len bytes are produced."""
+    _, chunks = stream
+    out = bytearray()
+    for raw_len, pl in chunks:
+        o, p = bytearray(), 0
+
+        def length(base):
+            nonlocal p
+            n = base
+            if base == 15:
+                while True:
+                    if p >= len(pl):
+                        raise abi.CorruptStreamError("lz_decode: truncated chunk")
+                    b = pl[p]
+                    p += 1
+                    n += b
+                    if b != 255:
+                        break
+            return n
+
+        while len(o) < raw_len:
+            if p >= len(pl):
+                raise abi.CorruptStreamError("lz_decode: truncated chunk")
+            tok = pl[p]
+            p += 1
+            lit = length(tok >> 4)
+            if p + lit > len(pl):
+                raise abi.CorruptStreamError("lz_decode: truncated chunk")
+            o += pl[p:p + lit]
+            p += lit
+            if len(o) == raw_len:
+                break
+            off = pl[p] | (pl[p + 1] << 8)
+            p += 2
+            ml = length(tok & 15) + 4
+            if off == 0 or off > len(o) or len(o) + ml > raw_len:
+                raise abi.CorruptStreamError("lz_decode: bad match")
+            for _ in range(ml):
+                o.append(o[-off])
+        if p != len(pl):
+            raise abi.CorruptStreamError("lz_decode: trailing bytes")
+        out += o
+    return bytes(out)
+
+
+def load_wgc(f) -> CompressedPatch:
+    """load_wgc(istream) (codec.hpp:393-433): one WGC1 record from a binary
+    file object."""
+    import struct
+
+    def get(fmt):
+        b = f.read(struct.calcsize(fmt))
+        if len(b) != struct.calcsize(fmt):
+            raise abi.CorruptStreamError("unexpected end of stream")
+        return struct.unpack("<" + fmt, b)
+
+    if f.read(4) != b"WGC1":
+        raise abi.CorruptStreamError("not a WGC1 file")
+    (codec,) = get("I")
+    if codec not in (1, 2):
+        raise abi.CorruptStreamError("unknown codec id")
+    (nd,) = get("I")
+    dims = get("I" * nd)
+    comps, levels = get("II")
+    csr, lz = [], []
+    for _ in range(comps):
+        if codec == 1:
+            rows, cols = get("II")
+            (n,) = get("Q")
+            v = np.frombuffer(f.read(8 * n), dtype="<f8").copy()
+            (n2,) = get("Q")
+            col = np.frombuffer(f.read(4 * n2), dtype="<u4").copy()
+            (n3,) = get("Q")
+            row = np.frombuffer(f.read(4 * n3), dtype="<u4").copy()
+            csr.append(CsrBlock(v, col, row, rows, cols))
+        else:
+            chunk, nch = get("QQ")
+            chunks = []
+            for _ in range(nch):
+                raw_len, enc = get("II")
+                chunks.append((raw_len, f.read(enc)))
+            lz.append((chunk, chunks))
+    return CompressedPatch(codec, tuple(dims), comps, levels, csr, lz)
+
+
+def decode_patch(p: CompressedPatch, lib=None) -> list:
+    """decode_patch (codec.hpp:308-325): the coefficient arrays of a record."""
+    if p.codec == 1:
+        return [csr_decode(b, lib) for b in p.csr]
+    n = int(np.prod(p.dims))
+    out = []
+    for s in p.lz:
+        raw = lz_decode_stream(s)
+        if len(raw) != 8 * n:
+            raise abi.CorruptStreamError("decode_patch: payload size mismatch")
+        out.append(np.frombuffer(raw, dtype="<f8").copy())
+    return out
+
+
+def read_checkpoint(path) -> tuple[dict, list]:
+    """A device-session checkpoint (wg_session_save): the WGS1 header and one
+    WGC1 record per patch of the shard."""
+    import struct
+
+    with open(path, "rb") as f:
+        hdr = f.read(4 + 4 + 4 + 4 + 8 * 10 + 8 * 3)
+        magic = hdr[:4]
+        if magic != b"WGS1":
+            raise abi.CorruptStreamError("not a WGS1 checkpoint")
+        vals = struct.unpack("<IiiQQQQQQQQQQddQ", hdr[4:])
+        keys = ["version", "scheme", "levels", "nx", "split0", "split1", "tile_rows", "row_begin", "row_end",
+                "npatch", "m", "n", "step", "time", "swe_last_dt", "swe_vmax_bits"]
+        h = dict(zip(keys, vals))
+        recs = [load_wgc(f) for _ in range(h["npatch"])]
+        if f.read(1):
+            raise abi.CorruptStreamError("checkpoint: trailing bytes")
+    return h, recs
+
+
 def csr_decode(b: CsrBlock, lib=None) -> np.ndarray:
     L = _lib(lib)
     v = _f64(b.v)

@@ -79,6 +79,30 @@ __global__ void k_upload(const double* grid, uint32_t N, ShardGeom g, unsigned c
     if (j == N - 2 && s_ch >= 0) e.colhi[ix(ar, s_ch) + i] = x;
 }
 
+// ---- edge lines of patches [p0, p0 + count) from their decoded grid buffer
+// (the ghost-ring sources of the next step; same mapping as k_upload) -------
+__global__ void k_edges_from_grid(const double* grid, uint32_t N, ShardGeom g, uint32_t p0, uint32_t count,
+                                  EdgeSet e) {
+    const uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    const uint64_t per = (uint64_t)N * N;
+    if (t >= (uint64_t)count * g.m * per) return;
+    const uint64_t pq = t / per;
+    const uint32_t i = (uint32_t)((t % per) / N), j = (uint32_t)(t % N);
+    if (!(i == 1 || i == N - 2 || j == 1 || j == N - 2)) return;
+    const uint32_t p = p0 + (uint32_t)(pq / g.m), q = (uint32_t)(pq % g.m);
+    const uint64_t TP = N + 2, tcount = TP * TP;
+    const double x = grid[pq * tcount + (i + 1) * TP + j + 1];
+    const uint32_t ar = p / g.P1, b = p % g.P1;
+    const bool lbm3 = g.me != g.m;
+    const int s_rl = lbm3 ? lbm_slot_rowlo((int)q) : (int)q, s_rh = lbm3 ? lbm_slot_rowhi((int)q) : (int)q;
+    const int s_cl = lbm3 ? lbm_slot_collo((int)q) : (int)q, s_ch = lbm3 ? lbm_slot_colhi((int)q) : (int)q;
+    auto ix = [&](uint32_t slot, int c) { return (((uint64_t)slot * g.P1 + b) * g.me + c) * N; };
+    if (i == 1 && s_rl >= 0) e.rowlo[ix(ar + 1, s_rl) + j] = x;
+    if (i == N - 2 && s_rh >= 0) e.rowhi[ix(ar + 1, s_rh) + j] = x;
+    if (j == 1 && s_cl >= 0) e.collo[ix(ar, s_cl) + i] = x;
+    if (j == N - 2 && s_ch >= 0) e.colhi[ix(ar, s_ch) + i] = x;
+}
+
 // ---- SWE: the first time step from the uploaded state (cfl_dt,
 // solver.hpp:242-258; dt = min(dt, t_end - 0), pipeline.hpp:195-196).  The
 // max is exact, so a grid-wide atomic max of the (positive) double bits is
@@ -146,6 +170,7 @@ struct Session {
     unsigned long long* swe = nullptr;
     unsigned long long* phase = nullptr;  // WG_PHASE_TIMING builds only
     uint64_t launched = 0;  // SWE step launches (steps past t_end are no-ops)
+    uint64_t row0 = 0;      // step count at upload/load: rows[k] holds step row0 + k + 1
 
     int cur = 0;  // pool/edges holding the current state
     uint64_t step = 0;
@@ -368,6 +393,7 @@ struct Session {
         WG_CUDA(cudaStreamSynchronize(stream));  // `used` lives on this stack frame
         step = 0;
         launched = 0;
+        row0 = 0;
         time = 0.0;
     }
 
@@ -407,6 +433,7 @@ struct Session {
         WG_LAUNCH_CHECK("device initial state");
         cur = 0;
         step = 0;
+        row0 = 0;
         time = 0.0;
         sync();
     }
@@ -455,15 +482,15 @@ struct Session {
             return;
         }
         const int src = cur, dst = 1 - cur;
-        grow_rows(step + 1);
+        grow_rows(step - row0 + 1);
         StepArgs a = step_args(src, dst);
         direction_speeds(cfg.alpha, cfg.beta, a.smax, a.smin);
         a.r = dt / sim_dx(cfg);  // solver.hpp:212
         a.omega = 1.0 / cfg.lbm_tau;
         a.step = step + 1;
         a.time = time + dt;
-        a.row_out = rows + step;
-        a.mass_fv_out = mass_fv + step;
+        a.row_out = rows + (step - row0);
+        a.mass_fv_out = mass_fv + (step - row0);
         cudaEvent_t e0 = nullptr, e1 = nullptr;
         if (profiling) {
             e0 = take_event();
@@ -482,11 +509,11 @@ struct Session {
     }
 
     void do_swe_step() {
-        grow_rows(launched + 1);
+        grow_rows(launched - row0 + 1);
         const int src = cur, dst = 1 - cur;
         StepArgs a = step_args(src, dst);
-        a.row_out = rows;  // offset by the device step counter
-        a.mass_fv_out = mass_fv;
+        a.row_out = rows - row0;  // indexed by the device step counter (>= row0)
+        a.mass_fv_out = mass_fv - row0;
         cudaEvent_t e0 = nullptr, e1 = nullptr;
         if (profiling) {
             e0 = take_event();
@@ -537,9 +564,292 @@ struct Session {
 
     void metrics(wg_metrics_row* out, uint64_t max_rows, uint64_t* nrows) {
         sync();
-        const uint64_t n = std::min<uint64_t>(step, max_rows);
+        const uint64_t n = std::min<uint64_t>(step - row0, max_rows);
         if (out && n) WG_CUDA(cudaMemcpy(out, rows, n * sizeof(wg_metrics_row), cudaMemcpyDeviceToHost));
-        if (nrows) *nrows = step;
+        if (nrows) *nrows = step - row0;
+    }
+
+    // ---- checkpoint / resume from the compressed store -------
+    // File: a WGS1 header, then one WGC1 record per patch exactly as
+    // save_wgc writes a CompressedPatch (codec.hpp:364-391): compressed
+    // patches as Codec::csr records of their CSR blocks (the bytes the
+    // reference would write), raw patches (skip rule / initial state) as
+    // Codec::lz records with levels 0 whose chunks are literal-only LZ
+    // sequences (codec.hpp:81-89, decodable by lz_decode; -0.0 survives).
+    struct CkptHeader {
+        char magic[4];
+        uint32_t version;
+        int32_t scheme, levels;
+        uint64_t nx, splits[2], tile_rows, row_begin, row_end, npatch, m, n, step;
+        double time, swe_last_dt;
+        uint64_t swe_vmax_bits;
+    };
+
+    void save(const char* path) {
+        sync();
+        const uint64_t blocks = (uint64_t)sg.npatch * sg.m;
+        std::vector<DirEntry> hd(blocks);
+        WG_CUDA(cudaMemcpy(hd.data(), dir[cur], blocks * sizeof(DirEntry), cudaMemcpyDeviceToHost));
+        unsigned long long used = 0;
+        WG_CUDA(cudaMemcpy(&used, bump + cur, sizeof used, cudaMemcpyDeviceToHost));
+        std::vector<unsigned char> pool(used);
+        if (used) WG_CUDA(cudaMemcpy(pool.data(), store[cur], used, cudaMemcpyDeviceToHost));
+        CkptHeader h{};
+        std::memcpy(h.magic, "WGS1", 4);
+        h.version = 1;
+        h.scheme = cfg.scheme;
+        h.levels = levels;
+        h.nx = cfg.nx;
+        h.splits[0] = cfg.splits[0];
+        h.splits[1] = cfg.splits[1];
+        h.tile_rows = geo.tiles;
+        h.row_begin = shard.row_begin;
+        h.row_end = shard.row_end;
+        h.npatch = sg.npatch;
+        h.m = sg.m;
+        h.n = N;
+        h.step = step;
+        h.time = time;
+        if (is_swe()) {
+            unsigned long long c[5];
+            WG_CUDA(cudaMemcpy(c, swe, sizeof c, cudaMemcpyDeviceToHost));
+            std::memcpy(&h.swe_last_dt, &c[1], sizeof(double));
+            h.swe_vmax_bits = c[2 + (step & 1)];
+        }
+        std::unique_ptr<FILE, int (*)(FILE*)> fh(std::fopen(path, "wb"), &std::fclose);
+        FILE* f = fh.get();
+        if (!f) raise(WG_INVALID_ARGUMENT, std::string("cannot open for writing: ") + path);
+        std::vector<unsigned char> out;
+        auto put = [&](const void* p, size_t nb) {
+            const unsigned char* c = static_cast<const unsigned char*>(p);
+            out.insert(out.end(), c, c + nb);
+        };
+        auto put32 = [&](uint32_t v) { put(&v, 4); };
+        auto put64 = [&](uint64_t v) { put(&v, 8); };
+        put(&h, sizeof h);
+        const uint64_t nn = (uint64_t)N * N, rawb = nn * 8;
+        for (uint64_t p = 0; p < sg.npatch; ++p) {
+            const DirEntry* e = &hd[p * sg.m];
+            bool raw = false;
+            for (uint32_t q = 0; q < sg.m; ++q) {
+                if (e[q].flags & DIR_DEAD)
+                    raise(WG_OUT_OF_MEMORY, "checkpoint: the store holds blocks lost to an overflow");
+                raw = raw || (e[q].flags & DIR_RAW);
+            }
+            put("WGC1", 4);
+            put32(raw ? 2u : 1u);  // Codec::lz / Codec::csr
+            put32(2);
+            put32(N);
+            put32(N);
+            put32(sg.m);
+            put32(raw ? 0u : (uint32_t)levels);
+            for (uint32_t q = 0; q < sg.m; ++q) {
+                if (e[q].off + (raw ? rawb : 12ull * e[q].nnz + 4ull * (N + 1)) > used)
+                    raise(WG_CORRUPT_STREAM, "checkpoint: directory entry outside the pool");
+                const unsigned char* b = pool.data() + e[q].off;
+                if (raw) {
+                    if (!(e[q].flags & DIR_RAW)) raise(WG_LOGIC, "checkpoint: mixed raw/CSR patch");
+                    const uint64_t chunk = 64 * 1024, nch = (rawb + chunk - 1) / chunk;
+                    put64(chunk);
+                    put64(nch);
+                    for (uint64_t c = 0; c < nch; ++c) {
+                        const uint64_t len = std::min(chunk, rawb - c * chunk);
+                        std::vector<unsigned char> pl;  // literal-only sequence
+                        pl.push_back(len >= 15 ? 0xF0 : (unsigned char)(len << 4));
+                        if (len >= 15) {
+                            uint64_t r = len - 15;
+                            while (r >= 255) {
+                                pl.push_back(255);
+                                r -= 255;
+                            }
+                            pl.push_back((unsigned char)r);
+                        }
+                        pl.insert(pl.end(), b + c * chunk, b + c * chunk + len);
+                        put32((uint32_t)len);
+                        put32((uint32_t)pl.size());
+                        put(pl.data(), pl.size());
+                    }
+                } else {
+                    const uint32_t nz = e[q].nnz;
+                    put32(N);
+                    put32(N);
+                    put64(nz);
+                    put(b, 8ull * nz);
+                    put64(nz);
+                    put(b + 8ull * nz, 4ull * nz);
+                    put64(N + 1);
+                    put(b + 12ull * nz, 4ull * (N + 1));
+                }
+            }
+            if (out.size() > (64u << 20)) {
+                if (std::fwrite(out.data(), 1, out.size(), f) != out.size())
+                    raise(WG_INVALID_ARGUMENT, "checkpoint: write failed");
+                out.clear();
+            }
+        }
+        const bool ok = std::fwrite(out.data(), 1, out.size(), f) == out.size();
+        if (std::fclose(fh.release()) != 0 || !ok) raise(WG_INVALID_ARGUMENT, "checkpoint: write failed");
+    }
+
+    void load(const char* path) {
+        FILE* f = std::fopen(path, "rb");
+        if (!f) raise(WG_INVALID_ARGUMENT, std::string("cannot open: ") + path);
+        std::vector<unsigned char> in;
+        {
+            unsigned char buf[1 << 16];
+            size_t k;
+            while ((k = std::fread(buf, 1, sizeof buf, f)) > 0) in.insert(in.end(), buf, buf + k);
+            std::fclose(f);
+        }
+        size_t pos = 0;
+        auto get = [&](void* p, size_t nb) {
+            if (pos + nb > in.size()) raise(WG_CORRUPT_STREAM, "unexpected end of stream");
+            std::memcpy(p, in.data() + pos, nb);
+            pos += nb;
+        };
+        auto get32 = [&] { uint32_t v; get(&v, 4); return v; };
+        auto get64 = [&] { uint64_t v; get(&v, 8); return v; };
+        CkptHeader h;
+        get(&h, sizeof h);
+        if (std::memcmp(h.magic, "WGS1", 4) != 0 || h.version != 1) raise(WG_CORRUPT_STREAM, "not a WGS1 checkpoint");
+        if (h.scheme != cfg.scheme || h.levels != levels || h.nx != cfg.nx || h.splits[0] != cfg.splits[0] ||
+            h.splits[1] != cfg.splits[1] || h.tile_rows != geo.tiles || h.row_begin != shard.row_begin ||
+            h.row_end != shard.row_end || h.npatch != sg.npatch || h.m != sg.m || h.n != N)
+            raise(WG_INVALID_ARGUMENT, "checkpoint: written for a different configuration or shard");
+        const uint64_t blocks = (uint64_t)sg.npatch * sg.m, nn = (uint64_t)N * N, rawb = nn * 8;
+        std::vector<DirEntry> hd(blocks);
+        std::vector<unsigned char> pool;
+        pool.reserve(std::min<uint64_t>(cap, in.size() + blocks * 16));
+        for (uint64_t p = 0; p < sg.npatch; ++p) {
+            char mg[4];
+            get(mg, 4);
+            if (std::memcmp(mg, "WGC1", 4) != 0) raise(WG_CORRUPT_STREAM, "not a WGC1 file");
+            const uint32_t codec = get32();
+            if (codec != 1 && codec != 2) raise(WG_CORRUPT_STREAM, "unknown codec id");
+            const uint32_t nd = get32();
+            if (nd != 2) raise(WG_INVALID_ARGUMENT, "checkpoint: patch rank");
+            const uint32_t d0 = get32(), d1 = get32(), comps = get32(), lv = get32();
+            if (d0 != N || d1 != N || comps != sg.m) raise(WG_INVALID_ARGUMENT, "checkpoint: patch shape");
+            if ((codec == 1 && lv != (uint32_t)levels) || (codec == 2 && lv != 0))
+                raise(WG_INVALID_ARGUMENT, "checkpoint: record levels do not match the session");
+            for (uint32_t q = 0; q < sg.m; ++q) {
+                const uint64_t off = round16(pool.size());
+                pool.resize(off);
+                DirEntry& e = hd[p * sg.m + q];
+                e.off = off;
+                if (codec == 1) {  // CsrBlock (codec.hpp:62-79 checks)
+                    const uint32_t rows = get32(), cols = get32();
+                    if (rows != N || cols != N) raise(WG_CORRUPT_STREAM, "csr_decode: block shape");
+                    const uint64_t nv = get64();
+                    if (nv > nn) raise(WG_CORRUPT_STREAM, "csr_decode: too many entries");
+                    pool.resize(off + 12ull * nv + 4ull * (N + 1));
+                    get(pool.data() + off, 8ull * nv);
+                    if (get64() != nv) raise(WG_CORRUPT_STREAM, "csr_decode: v/col length mismatch");
+                    get(pool.data() + off + 8ull * nv, 4ull * nv);
+                    if (get64() != (uint64_t)N + 1) raise(WG_CORRUPT_STREAM, "csr_decode: row offsets");
+                    uint32_t* ro = reinterpret_cast<uint32_t*>(pool.data() + off + 12ull * nv);
+                    get(ro, 4ull * (N + 1));
+                    const uint32_t* co = reinterpret_cast<const uint32_t*>(pool.data() + off + 8ull * nv);
+                    if (ro[0] != 0 || ro[N] != nv) raise(WG_CORRUPT_STREAM, "csr_decode: row offsets");
+                    for (uint32_t r = 0; r < N; ++r)
+                        if (ro[r] > ro[r + 1]) raise(WG_CORRUPT_STREAM, "csr_decode: row offsets");
+                    for (uint64_t k = 0; k < nv; ++k)
+                        if (co[k] >= N) raise(WG_CORRUPT_STREAM, "csr_decode: column out of range");
+                    e.nnz = (uint32_t)nv;
+                    e.flags = 0;
+                } else {  // LzStream (lz_decode, codec.hpp:177-244) of the raw block
+                    pool.resize(off + rawb);
+                    unsigned char* dst = pool.data() + off;
+                    uint64_t done = 0;
+                    const uint64_t chunk = get64(), nch = get64();
+                    (void)chunk;
+                    for (uint64_t c = 0; c < nch; ++c) {
+                        const uint32_t raw_len = get32(), enc = get32();
+                        if (pos + enc > in.size()) raise(WG_CORRUPT_STREAM, "truncated LZ chunk");
+                        if (done + raw_len > rawb) raise(WG_CORRUPT_STREAM, "decode_patch: payload size mismatch");
+                        const unsigned char* src = in.data() + pos;
+                        size_t sp = 0;
+                        uint64_t o = 0;
+                        auto length = [&](size_t base) {
+                            size_t len = base;
+                            if (base == 15) {
+                                unsigned char b;
+                                do {
+                                    if (sp >= enc) raise(WG_CORRUPT_STREAM, "lz_decode: truncated chunk");
+                                    b = src[sp++];
+                                    len += b;
+                                } while (b == 255);
+                            }
+                            return len;
+                        };
+                        while (o < raw_len) {
+                            if (sp >= enc) raise(WG_CORRUPT_STREAM, "lz_decode: truncated chunk");
+                            const unsigned char token = src[sp++];
+                            const size_t lit = length(token >> 4);
+                            if (sp + lit > enc || o + lit > raw_len) raise(WG_CORRUPT_STREAM, "lz_decode: truncated chunk");
+                            std::memcpy(dst + done + o, src + sp, lit);
+                            sp += lit;
+                            o += lit;
+                            if (o == raw_len) break;
+                            if (sp + 2 > enc) raise(WG_CORRUPT_STREAM, "lz_decode: truncated chunk");
+                            const size_t moff = src[sp] | ((size_t)src[sp + 1] << 8);
+                            sp += 2;
+                            const size_t ml = length(token & 0x0f) + 4;
+                            if (moff == 0 || moff > o) raise(WG_CORRUPT_STREAM, "lz_decode: bad match offset");
+                            if (o + ml > raw_len) raise(WG_CORRUPT_STREAM, "lz_decode: raw_len overrun");
+                            for (size_t i = 0; i < ml; ++i) dst[done + o + i] = dst[done + o - moff + i];
+                            o += ml;
+                        }
+                        if (sp != enc) raise(WG_CORRUPT_STREAM, "lz_decode: trailing bytes");
+                        pos += enc;
+                        done += raw_len;
+                    }
+                    if (done != rawb) raise(WG_CORRUPT_STREAM, "decode_patch: payload size mismatch");
+                    e.nnz = 0;
+                    e.flags = DIR_RAW;
+                }
+            }
+        }
+        if (pos != in.size()) raise(WG_CORRUPT_STREAM, "checkpoint: trailing bytes");
+        const uint64_t used = round16(pool.size());
+        if (used > cap) raise(WG_OUT_OF_MEMORY, "checkpoint does not fit the compressed-store budget");
+        pool.resize(used);
+        // the pool parity follows the step count (SWE derives it on the device)
+        const int k = (int)(h.step & 1);
+        WG_CUDA(cudaMemcpy(store[k], pool.data(), used, cudaMemcpyHostToDevice));
+        WG_CUDA(cudaMemcpy(dir[k], hd.data(), blocks * sizeof(DirEntry), cudaMemcpyHostToDevice));
+        const unsigned long long bu[2] = {k == 0 ? used : 0ull, k == 1 ? used : 0ull};
+        WG_CUDA(cudaMemcpy(bump, bu, sizeof bu, cudaMemcpyHostToDevice));
+        cur = k;
+        // edge lines: decode patch batches, copy their boundary lines
+        const uint64_t tcount = (uint64_t)(N + 2) * (N + 2);
+        const uint32_t batch = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(sg.npatch, (256ull << 20) /
+                                                                                                (8 * sg.m * tcount)));
+        DevBuf<double> buf((uint64_t)batch * sg.m * tcount);
+        for (uint32_t p0 = 0; p0 < sg.npatch; p0 += batch) {
+            const uint32_t cnt = std::min<uint32_t>(batch, sg.npatch - p0);
+            StepArgs a = step_args(k, 1 - k);
+            a.dir_in = dir[k] + (uint64_t)p0 * sg.m;
+            a.g.npatch = cnt;
+            a.decode_out = buf.p;
+            ks.decode<<<grid, ks.threads, ks.smem, stream>>>(a);
+            WG_LAUNCH_CHECK("checkpoint decode");
+            const uint64_t th = (uint64_t)cnt * sg.m * N * N;
+            k_edges_from_grid<<<(unsigned)((th + 255) / 256), 256, 0, stream>>>(buf.p, N, sg, p0, cnt, edges[k]);
+            WG_LAUNCH_CHECK("checkpoint edges");
+        }
+        step = h.step;
+        row0 = h.step;
+        launched = h.step;
+        time = h.time;
+        if (is_swe()) {
+            unsigned long long c[5] = {0, 0, 0, 0, h.step};
+            std::memcpy(&c[0], &h.time, sizeof(double));
+            std::memcpy(&c[1], &h.swe_last_dt, sizeof(double));
+            c[2 + (h.step & 1)] = h.swe_vmax_bits;
+            WG_CUDA(cudaMemcpyAsync(swe, c, sizeof c, cudaMemcpyHostToDevice, stream));
+        }
+        sync();
     }
 
     void patch_csr(uint64_t p, uint32_t q, double* v, uint32_t* col, uint32_t* row, uint64_t* nnz,
@@ -631,6 +941,14 @@ wg_status wg_session_cfl_vmax(wg_session* sp, unsigned long long** vmax_bits) {
     });
 }
 
+wg_status wg_session_save(wg_session* s, const char* path) {
+    return guard([&] { reinterpret_cast<Session*>(s)->save(path); });
+}
+
+wg_status wg_session_load(wg_session* s, const char* path) {
+    return guard([&] { reinterpret_cast<Session*>(s)->load(path); });
+}
+
 wg_status wg_session_metrics(wg_session* s, wg_metrics_row* rows, uint64_t max_rows, uint64_t* nrows) {
     return guard([&] { reinterpret_cast<Session*>(s)->metrics(rows, max_rows, nrows); });
 }
@@ -652,8 +970,8 @@ wg_status wg_session_last_row(wg_session* sp, wg_metrics_row* row) {
     return guard([&] {
         Session* s = reinterpret_cast<Session*>(sp);
         if (s->is_swe()) s->sync();
-        if (s->step == 0) raise(WG_LOGIC, "no step has run");
-        WG_CUDA(cudaMemcpyAsync(row, s->rows + (s->step - 1), sizeof(wg_metrics_row), cudaMemcpyDeviceToHost,
+        if (s->step <= s->row0) raise(WG_LOGIC, "no step has run");
+        WG_CUDA(cudaMemcpyAsync(row, s->rows + (s->step - 1 - s->row0), sizeof(wg_metrics_row), cudaMemcpyDeviceToHost,
                                 s->stream));
         s->sync();
     });

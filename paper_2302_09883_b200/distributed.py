@@ -153,6 +153,15 @@ class ShardedSession:
         n = self.info.halo_doubles
         return [torch.as_tensor(_DevArray(p.value, n), device=f"cuda:{self.shard.device}") for p in ptrs]
 
+    def save(self, path: str):
+        """Checkpoint this shard's compressed store (WGS1 + WGC1 records)."""
+        self.lib.check(self.lib.wg_session_save(self.handle, str(path).encode()))
+
+    def load(self, path: str):
+        """Resume from a checkpoint written by save() for the same shard."""
+        self.lib.check(self.lib.wg_session_load(self.handle, str(path).encode()))
+        self._exchange()
+
     def step(self, dt: float = 1.0):
         self.lib.check(self.lib.wg_session_step(self.handle, dt))
         self._exchange()  # the halo blocks move with the double buffer: re-fetched every step
