@@ -380,6 +380,7 @@ class RunConfig:
     lbm_delta: float = 0.05
     store_budget_bytes: int = 0
     tile_rows: int = 1
+    metrics_path: str = ""       # RunConfig::metrics_path: CSV of the rows (pipeline.hpp:162-166)
 
     def to_c(self) -> abi.RunConfigC:
         c = abi.RunConfigC()
@@ -432,7 +433,27 @@ def run(cfg: RunConfig, lib=None, max_rows: int = 1 << 17) -> RunResult:
     L.check(L.wg_run(C.byref(c), rows, cap, C.byref(nr), abi.dptr(grid.data), C.byref(s)))
     out_rows = [{k: getattr(r, k) for k in _ROW_FIELDS} for r in rows[: min(nr.value, cap)]]
     summary = {k: getattr(s, k) for k, _ in abi.RunSummaryC._fields_}
+    if cfg.metrics_path:
+        write_metrics_csv(out_rows, cfg.metrics_path)
     return RunResult(out_rows, summary, grid, s.t_final)
+
+
+METRICS_HEADER = "step,time,dense_bytes,compressed_bytes,ratio,nnz,zeroed,global_mass,l2_error\n"
+
+
+def metrics_csv_row(r: dict) -> str:
+    """write_metrics_row (pipeline.hpp:78-84): %zu for counts, %.17g for reals."""
+    return "%d,%.17g,%d,%d,%.17g,%d,%d,%.17g,%.17g\n" % (
+        r["step"], r["time"], r["dense_bytes"], r["compressed_bytes"], r["ratio"], r["nnz"], r["zeroed"],
+        r["global_mass"], r["l2"])
+
+
+def write_metrics_csv(rows, path) -> None:
+    """The metrics file of run() (write_metrics_header/row, pipeline.hpp:74-84)."""
+    with open(path, "w") as f:
+        f.write(METRICS_HEADER)
+        for r in rows:
+            f.write(metrics_csv_row(r))
 
 
 def initial_state(cfg: RunConfig, lib=None) -> PatchGrid:

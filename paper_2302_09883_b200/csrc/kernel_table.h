@@ -20,6 +20,7 @@ struct KernelSet {
     bool persistent;         // grid-stride over patches with per-CTA scratch
     size_t scratch_doubles;  // per CTA
     bool edges3;             // D2Q9 edge lines hold only the 3 crossing populations
+    bool decode_l2;          // decode with decode_out == nullptr runs the transport l2 pass
 };
 
 // Each returns false when (n, levels) has no instantiation.

@@ -12,7 +12,7 @@ struct FullL {
     static KernelSet make() {
         using Lay = LbmLayout<N>;
         return KernelSet{k_lbm_step<N, L, MODE_STEP>, k_lbm_step<N, L, MODE_DECODE>, k_lbm_step<N, L, MODE_INIT>,
-                         1, Lay::NT, Lay::smem_bytes(), true, Lay::scratch_doubles(), true};
+                         1, Lay::NT, Lay::smem_bytes(), true, Lay::scratch_doubles(), true, false};
     }
 };
 
@@ -21,7 +21,7 @@ struct HalfL {
     static KernelSet make() {
         using Lay = HLayout<N, 3>;
         return KernelSet{k_lbm_step_h<N, L, MODE_STEP>, k_lbm_step_h<N, L, MODE_DECODE>, nullptr, 1, Lay::NT,
-                         Lay::smem_bytes(), true, LbmLayout<N>::scratch_doubles(), false};
+                         Lay::smem_bytes(), true, LbmLayout<N>::scratch_doubles(), false, false};
     }
 };
 

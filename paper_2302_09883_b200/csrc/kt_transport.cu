@@ -14,7 +14,7 @@ struct FullT {
         static KernelSet make() {
             using Lay = Layout<N, P>;
             return KernelSet{k_patch_step<N, L, P, MODE_STEP>, k_patch_step<N, L, P, MODE_DECODE>, nullptr, P,
-                             Lay::NT, Lay::smem_bytes(), false, 0, false};
+                             Lay::NT, Lay::smem_bytes(), false, 0, false, true};
         }
     };
 };
@@ -24,7 +24,7 @@ struct HalfT {
     static KernelSet make() {
         using Lay = HLayout<N, 2>;
         return KernelSet{k_patch_step_h<N, L, 2, MODE_STEP>, k_patch_step_h<N, L, 2, MODE_DECODE>, nullptr, 2,
-                         Lay::NT, Lay::smem_bytes(), false, 0, false};
+                         Lay::NT, Lay::smem_bytes(), false, 0, false, false};
     }
 };
 

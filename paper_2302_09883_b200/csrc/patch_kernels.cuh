@@ -105,7 +105,7 @@ __global__ void __launch_bounds__(Layout<N, P>::NT, WG_MIN_BLOCKS)
     const uint32_t ngroups = (g.npatch + P - 1) / P;
     // running partials: every thread its columns' masses, lane s of warp 0
     // the byte/nnz/zeroed counts of slot s (fixed order -> deterministic)
-    StepPartial acc{0, 0, 0, 0.0, 0.0};
+    StepPartial acc{0, 0, 0, 0.0, 0.0, 0.0};
     WG_PHASE_MARK(-1);
 
     if (t == 0) cs.cur = cs.end = 0;
@@ -133,9 +133,13 @@ __global__ void __launch_bounds__(Layout<N, P>::NT, WG_MIN_BLOCKS)
             if (valid) {
                 double v[N];
                 decode_col<N, L>(T, j, raw_in, v);
-                double* out = a.decode_out + (size_t)p * TILE;
+                if (a.decode_out) {
+                    double* out = a.decode_out + (size_t)p * TILE;
 #pragma unroll
-                for (int i = 0; i < N; ++i) out[(i + 1) * TP + j + 1] = v[i];
+                    for (int i = 0; i < N; ++i) out[(i + 1) * TP + j + 1] = v[i];
+                } else {  // l2 pass: the step's output against exact_transport
+                    acc.l2 += col_l2<N>(a, pp, j, v);
+                }
             }
             __syncthreads();
             if (t < P) slot_dir[t] = next_dir[t];
@@ -256,7 +260,10 @@ __global__ void __launch_bounds__(Layout<N, P>::NT, WG_MIN_BLOCKS)
         __syncthreads();
         WG_PHASE_MARK(9);
     }
-    if (MODE == MODE_DECODE) return;
+    if (MODE == MODE_DECODE) {
+        if (!a.decode_out) finalize_l2<NT>(a, acc.l2);
+        return;
+    }
     const StepPartial part = cta_reduce_partial<NT>(acc);
     WG_PHASE_MARK(10);
     finalize_step(a, part);

@@ -56,6 +56,7 @@ __device__ __forceinline__ void phase_mark(unsigned long long* buf, int k) {
 struct StepPartial {
     unsigned long long comp_bytes, nnz, zeroed;
     double mass, mass_fv;
+    double l2;  // transport: sum of squared errors vs exact_transport (l2_error, solver.hpp:293-305)
 };
 
 struct StepArgs {
@@ -97,6 +98,10 @@ struct StepArgs {
     unsigned long long* swe_steps;   // steps completed on the device
     double t_end, cfl_dx, dx, gravity;
     unsigned long long* phase;       // WG_PHASE_TIMING builds: per-phase cycle sums [32]
+    // transport l2_error diagnostic every step (pipeline.hpp:275-276)
+    int l2_on;
+    uint64_t l2_nx;
+    double l2_scale, l2_dx, l2_alpha, l2_beta;          // area / nx^2, dx, speeds
     double thr[(kMaxLevels + 1) * (kMaxLevels + 1)];     // T[band_i][band_j]
 };
 
@@ -376,6 +381,35 @@ __device__ __forceinline__ double tile_col_mass(const double* T, int j) {
     return (m[0] + m[1]) + (m[2] + m[3]);
 }
 
+// Squared error of tile column j against exact_transport (solver.hpp:264-287)
+// at the step's time, over the global points this patch owns (its last row
+// and column belong to the next patch, except at the global boundary).
+__device__ __forceinline__ double wrap_unit_d(double x) {
+    x = fmod(x, 1.0);
+    return x < 0.0 ? x + 1.0 : x;
+}
+
+template <int N>
+__device__ __forceinline__ double col_l2(const StepArgs& a, const PatchPos& pp, int j, const double (&v)[N]) {
+    const uint64_t gi0 = (uint64_t)(a.g.row0 + pp.ar) * (N - 1), gj = (uint64_t)pp.b * (N - 1) + j;
+    if (j == N - 1 && gj != a.l2_nx - 1) return 0.0;
+    double py = wrap_unit_d((double)gj * a.l2_dx - a.l2_beta * a.time) - 0.5;
+    if (py < -0.5) py += 1.0;
+    if (py >= 0.5) py -= 1.0;
+    double s = 0.0;
+#pragma unroll 5
+    for (int i = 0; i < N; ++i) {
+        const uint64_t gi = gi0 + i;
+        if (i == N - 1 && gi != a.l2_nx - 1) continue;
+        double px = wrap_unit_d((double)gi * a.l2_dx - a.l2_alpha * a.time) - 0.5;
+        if (px < -0.5) px += 1.0;
+        if (px >= 0.5) px -= 1.0;
+        const double d = v[i] - (1.0 + exp(-30.0 * (px * px + py * py)));
+        s += d * d;
+    }
+    return s;
+}
+
 // Trapezoid-weighted column sum (global_mass weights, patchgrid.hpp:244-266),
 // with four interleaved partial sums (fixed association: deterministic; the
 // mass is a tolerance-checked diagnostic).
@@ -436,10 +470,11 @@ __device__ __forceinline__ StepPartial cta_reduce_partial(StepPartial x) {
         x.zeroed += __shfl_xor_sync(0xffffffffu, x.zeroed, o);
         x.mass += __shfl_xor_sync(0xffffffffu, x.mass, o);
         x.mass_fv += __shfl_xor_sync(0xffffffffu, x.mass_fv, o);
+        x.l2 += __shfl_xor_sync(0xffffffffu, x.l2, o);
     }
     if ((threadIdx.x & 31) == 0) wpart[threadIdx.x >> 5] = x;
     __syncthreads();
-    StepPartial r{0, 0, 0, 0.0, 0.0};
+    StepPartial r{0, 0, 0, 0.0, 0.0, 0.0};
     if (threadIdx.x == 0) {
         for (int w = 0; w < NT / 32; ++w) {
             r.comp_bytes += wpart[w].comp_bytes;
@@ -447,6 +482,7 @@ __device__ __forceinline__ StepPartial cta_reduce_partial(StepPartial x) {
             r.zeroed += wpart[w].zeroed;
             r.mass += wpart[w].mass;
             r.mass_fv += wpart[w].mass_fv;
+            r.l2 += wpart[w].l2;
         }
     }
     return r;
@@ -576,7 +612,7 @@ __device__ __forceinline__ void finalize_step(const StepArgs& a, const StepParti
     __threadfence();
     const int lane = threadIdx.x;
     unsigned long long cb = 0, nz = 0, zr = 0;
-    double m = 0.0, mf = 0.0;
+    double m = 0.0, mf = 0.0, l2 = 0.0;
     for (unsigned c = lane; c < gridDim.x; c += 32) {
         const StepPartial* pp = a.partials + c;
         cb += __ldcg(&pp->comp_bytes);
@@ -584,6 +620,7 @@ __device__ __forceinline__ void finalize_step(const StepArgs& a, const StepParti
         zr += __ldcg(&pp->zeroed);
         m += __ldcg(&pp->mass);
         mf += __ldcg(&pp->mass_fv);
+        l2 += __ldcg(&pp->l2);
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -592,6 +629,7 @@ __device__ __forceinline__ void finalize_step(const StepArgs& a, const StepParti
         zr += __shfl_xor_sync(0xffffffffu, zr, o);
         m += __shfl_xor_sync(0xffffffffu, m, o);
         mf += __shfl_xor_sync(0xffffffffu, mf, o);
+        l2 += __shfl_xor_sync(0xffffffffu, l2, o);
     }
     if (lane == 0) {
         wg_metrics_row r;
@@ -615,11 +653,41 @@ __device__ __forceinline__ void finalize_step(const StepArgs& a, const StepParti
         r.nnz = a.compress ? nz : 0;
         r.zeroed = a.compress ? zr : 0;
         r.global_mass = m;
-        r.l2 = 0.0;
+        r.l2 = a.l2_on ? a.l2_scale * l2 : 0.0;  // area / size * sum (solver.hpp:302-304)
         *row_out = r;
         *mfv_out = mf;
         *a.done = 0;
         *a.bump_next = 0;
+    }
+}
+
+// End of an l2 pass (transport, compute_l2): fixed-order reduction of the
+// per-thread squared errors; the last CTA writes the step's row.l2.
+template <int NT>
+__device__ __forceinline__ void finalize_l2(const StepArgs& a, double mine) {
+    __shared__ double wl2[NT / 32];
+    __shared__ int am_last;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
+    if ((threadIdx.x & 31) == 0) wl2[threadIdx.x >> 5] = mine;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double c = 0.0;
+        for (int w = 0; w < NT / 32; ++w) c += wl2[w];
+        a.partials[blockIdx.x].l2 = c;
+        __threadfence();
+        am_last = atomicAdd(a.done, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!am_last || threadIdx.x >= 32) return;
+    __threadfence();
+    double s = 0.0;
+    for (unsigned c = threadIdx.x; c < gridDim.x; c += 32) s += __ldcg(&a.partials[c].l2);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (threadIdx.x == 0) {
+        a.row_out->l2 = a.l2_scale * s;  // area / size * sum (solver.hpp:302-304)
+        *a.done = 0;
     }
 }
 

@@ -491,6 +491,7 @@ struct Session {
         a.time = time + dt;
         a.row_out = rows + (step - row0);
         a.mass_fv_out = mass_fv + (step - row0);
+
         cudaEvent_t e0 = nullptr, e1 = nullptr;
         if (profiling) {
             e0 = take_event();
@@ -502,6 +503,22 @@ struct Session {
         if (profiling) {
             WG_CUDA(cudaEventRecord(e1, stream));
             ev_main.emplace_back(e0, e1);
+        }
+        if (ks.decode_l2 && cfg.compute_l2 && geo.tiles == 1) {
+            // l2_error(assemble(grid, 0), exact_transport(t), cfg) of the new
+            // state (pipeline.hpp:275-276): a decode pass over the output pool
+            StepArgs b = step_args(dst, src);
+            b.decode_out = nullptr;
+            b.time = a.time;
+            b.row_out = a.row_out;
+            b.l2_on = 1;
+            b.l2_nx = cfg.nx;
+            b.l2_scale = cfg.domain_length * cfg.domain_length / static_cast<double>(cfg.nx * cfg.nx);
+            b.l2_dx = sim_dx(cfg);
+            b.l2_alpha = cfg.alpha;
+            b.l2_beta = cfg.beta;
+            ks.decode<<<grid, ks.threads, ks.smem, stream>>>(b);
+            WG_LAUNCH_CHECK("l2 pass");
         }
         cur = dst;
         ++step;
@@ -1071,8 +1088,9 @@ wg_status wg_run(const wg_run_config* cfg, wg_metrics_row* rows, uint64_t max_ro
             }
         }
         if (cfg->scheme == WG_SCHEME_TRANSPORT && cfg->compute_l2 && !r.empty()) {
-            // l2_error of the final state only (the per-step l2 diagnostic is
-            // host-side harness work)
+            // every row's l2 comes from the device (col_l2, CUDA exp); the
+            // final row is recomputed here with the host's glibc exp, the
+            // reference's own libm
             std::vector<double> fg(grid.size());
             s.download(fg.data());
             const uint64_t n0 = g.n[0], n1 = g.n[1], ty = n1 + 2;

@@ -71,6 +71,18 @@ def test_transport_parity(product, oracle, nx, splits, levels, c, mode, steps):
     compare_runs(api.run(cfg, lib=product), api.run(cfg, lib=oracle))
 
 
+def test_l2_every_step(product, oracle):
+    """l2_error(assemble(grid), exact_transport(t)) of every row (pipeline.hpp:
+    275-276) computed in the fused kernel; CUDA exp vs glibc exp and the
+    summation order: relative 1e-12."""
+    cfg = api.RunConfig(scheme="transport", nx=129, splits=(4, 4), levels=4, t_end=0.05,
+                        spec=api.ThresholdSpec("capped", 1e-3), compute_l2=True)
+    a, b = api.run(cfg, lib=product), api.run(cfg, lib=oracle)
+    assert len(a.rows) == len(b.rows)
+    for ra, rb in zip(a.rows, b.rows):
+        assert abs(ra["l2"] - rb["l2"]) <= 1e-12 * rb["l2"], (ra["step"], ra["l2"], rb["l2"])
+
+
 def test_zero_threshold_equals_no_compression(product):
     """test_pipeline.cpp:33-53 — c=0 keeps every patch raw (skip rule)."""
     a = api.run(transport_cfg(33, (2, 2), 3, 0.0, 12), lib=product)
