@@ -237,3 +237,19 @@ def test_error_types_vs_reference(oracle, reference):
         with pytest.raises(abi.DomainError):
             api.fv_step(bad, api.PatchGrid((17, 17), (1, 1), 3, True), "swe", 1e-3, 1 / 16, lib=lib)
         assert math.isfinite(api.band_threshold([1, 2], api.ThresholdSpec("capped", 1.0), lib=lib))
+
+
+def test_metrics_csv_schema(oracle, tmp_path):
+    """test_pipeline.cpp:79-95: the metrics file has the documented header and
+    one line per row, each formatted as write_metrics_row (pipeline.hpp:78-84)."""
+    path = tmp_path / "m.csv"
+    cfg = api.RunConfig(scheme="transport", nx=33, splits=(2, 2), levels=3, t_end=0.02,
+                        spec=api.ThresholdSpec("capped", 0.01), metrics_path=str(path))
+    r = api.run(cfg, lib=oracle)
+    lines = path.read_text().splitlines()
+    assert lines[0] == "step,time,dense_bytes,compressed_bytes,ratio,nnz,zeroed,global_mass,l2_error"
+    assert len([x for x in lines[1:] if x]) == len(r.rows)
+    for line, row in zip(lines[1:], r.rows):
+        f = line.split(",")
+        assert int(f[0]) == row["step"] and float(f[1]) == row["time"] and int(f[5]) == row["nnz"]
+        assert float(f[7]) == row["global_mass"] and float(f[8]) == row["l2"]  # %.17g round-trips
