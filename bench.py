@@ -233,14 +233,21 @@ def bench_b200(args, w: dict):
     import torch
     import torch.distributed as dist
 
-    from paper_2302_09883_b200.distributed import ShardInfo, ShardedSession, reduce_rows, shard_rows
+    from paper_2302_09883_b200.distributed import ShardInfo, ShardedSession, collective_device, reduce_rows, shard_rows
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # WG_FORCE_DEVICE / WG_DIST_BACKEND=gloo: the N>1 orchestration run on one
+    # GPU by tests/test_gpu_multiproc.py (correctness only; never a bench line)
+    local = int(os.environ.get("WG_FORCE_DEVICE", local))
     torch.cuda.set_device(local)
+    backend = os.environ.get("WG_DIST_BACKEND", "nccl")
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        else:
+            dist.init_process_group(backend)
     lib = abi.load_product()
     cfg = run_config(w, args.warmup + args.steps)
     dt = transport_dt(cfg) if w["scheme"] == "transport" else 1.0
@@ -288,7 +295,8 @@ def bench_b200(args, w: dict):
             # reported are those of the loaded GPU around the timed region
             t_w = time.perf_counter()
             done = 0
-            while done < args.warmup or (world == 1 and clocks.count() < 3 and time.perf_counter() - t_w < 3.0):
+            adaptive = world == 1 and not os.environ.get("WG_FIXED_WARMUP")
+            while done < args.warmup or (adaptive and clocks.count() < 3 and time.perf_counter() - t_w < 3.0):
                 sess.step(dt)
                 done += 1
                 if done % 8 == 0:
@@ -317,7 +325,8 @@ def bench_b200(args, w: dict):
         free_b, total_b = torch.cuda.mem_get_info(local)
         mem_used = total_b - free_b
         if world > 1:
-            t = torch.tensor([tot_ms, main_ms.value], dtype=torch.float64, device=f"cuda:{local}")
+            t = torch.tensor([tot_ms, main_ms.value], dtype=torch.float64,
+                             device=collective_device(dist, f"cuda:{local}"))
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             tot_ms, main_max = t.tolist()
             rows = reduce_rows(rows, dist, f"cuda:{local}")
@@ -381,7 +390,7 @@ def e2e_run(lib, cfg, shard, stream, host, args, dt, dist, copies=1):
     read back to the host."""
     import torch
 
-    from paper_2302_09883_b200.distributed import ShardedSession
+    from paper_2302_09883_b200.distributed import ShardedSession, collective_device
 
     sess = ShardedSession(lib, cfg, shard, stream.cuda_stream, dist)
     try:
@@ -399,7 +408,7 @@ def e2e_run(lib, cfg, shard, stream, host, args, dt, dist, copies=1):
         torch.cuda.synchronize()
         secs = time.perf_counter() - t0
         if dist:
-            t = torch.tensor([secs], dtype=torch.float64, device=f"cuda:{shard.device}")
+            t = torch.tensor([secs], dtype=torch.float64, device=collective_device(dist, f"cuda:{shard.device}"))
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             secs = t.item()
     finally:

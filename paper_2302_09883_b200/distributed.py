@@ -47,6 +47,11 @@ def exchange_halos(send_lo, send_hi, recv_lo, recv_hi, rank: int, world: int, di
     recv_hi <- below.send_lo.  Operations are posted in one fixed order on
     every rank so that world == 2 (above == below) still pairs correctly."""
     above, below = ring_neighbours(rank, world)
+    staged = send_lo.is_cuda and dist.get_backend() == "gloo"  # gloo moves host tensors only
+    if staged:
+        dev = (recv_lo, recv_hi)
+        send_lo, send_hi = send_lo.cpu(), send_hi.cpu()
+        recv_lo, recv_hi = torch_empty_like_cpu(recv_lo), torch_empty_like_cpu(recv_hi)
     ops = [
         dist.P2POp(dist.isend, send_hi, below),
         dist.P2POp(dist.isend, send_lo, above),
@@ -55,6 +60,21 @@ def exchange_halos(send_lo, send_hi, recv_lo, recv_hi, rank: int, world: int, di
     ]
     for req in dist.batch_isend_irecv(ops):
         req.wait()
+    if staged:
+        dev[0].copy_(recv_lo)
+        dev[1].copy_(recv_hi)
+
+
+def torch_empty_like_cpu(t):
+    import torch
+
+    return torch.empty(t.shape, dtype=t.dtype, device="cpu")
+
+
+def collective_device(dist, device):
+    """Where collective operands live: the GPU for NCCL, the host for gloo
+    (the multi-process path run on one GPU in tests/test_gpu_multiproc.py)."""
+    return "cpu" if dist.get_backend() == "gloo" else device
 
 
 class _DevArray:
@@ -72,6 +92,7 @@ def reduce_rows(rows: list[dict], dist, device) -> list[dict]:
     import torch
 
     keys = ["dense_bytes", "compressed_bytes", "nnz", "zeroed"]
+    device = collective_device(dist, device)
     ints = torch.tensor([[r[k] for k in keys] for r in rows], dtype=torch.int64, device=device)
     mass = torch.tensor([r["global_mass"] for r in rows], dtype=torch.float64, device=device)
     dist.all_reduce(ints)
@@ -132,7 +153,13 @@ class ShardedSession:
             s_lo, s_hi, r_lo, r_hi = self.halo_tensors()
             exchange_halos(s_lo, s_hi, r_lo, r_hi, self.shard.rank, self.shard.world, self.dist)
             if self.swe:
-                self.dist.all_reduce(self.cfl_vmax_tensor(), op=self.dist.ReduceOp.MAX)
+                v = self.cfl_vmax_tensor()
+                if self.dist.get_backend() == "gloo":
+                    h = v.cpu()
+                    self.dist.all_reduce(h, op=self.dist.ReduceOp.MAX)
+                    v.copy_(h)
+                else:
+                    self.dist.all_reduce(v, op=self.dist.ReduceOp.MAX)
 
     def cfl_vmax_tensor(self):
         """SWE: the next step's max wave speed (int64 view of the non-negative
