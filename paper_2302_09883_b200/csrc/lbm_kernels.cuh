@@ -22,6 +22,10 @@
 
 namespace wg {
 
+#ifndef WG_LBM_SMEM_POPS
+#define WG_LBM_SMEM_POPS 0  // 3 measured no faster (C2 7.83 vs 7.86 GLUPS): the L2 scratch is not the bound
+#endif
+
 template <int N>
 struct LbmLayout {
     static constexpr int TP = N + 2;
@@ -30,10 +34,21 @@ struct LbmLayout {
     static constexpr int NT = ((SLOTS * N + 31) / 32) * 32;
     // 3 tiles + the scan buffer: 109.5 KB at N = 65, so two CTAs fit an SM
     // (the per-patch mass reductions reuse the tiles once a patch is done)
+    // the first SPOPS populations of the scratch live in shared memory (the
+    // rest in the CTA's L2-resident global scratch): 206 KB at N = 65
+    static constexpr int SPOPS = (N <= 65) ? WG_LBM_SMEM_POPS : 0;
     static constexpr size_t smem_bytes() {
-        return sizeof(double) * (size_t)(SLOTS * TILE) + sizeof(unsigned long long) * NT;
+        return sizeof(double) * (size_t)(SLOTS * TILE + SPOPS * N * N) + sizeof(unsigned long long) * NT;
     }
     static constexpr size_t scratch_doubles() { return (size_t)9 * N * N; }
+};
+
+// Population q of the per-patch staging (post-stream / post-collide field).
+struct LbmScratch {
+    double* sm;  // SPOPS populations in shared memory
+    double* gl;  // all 9 slots in global memory (the first SPOPS unused)
+    int spops, nn;
+    __device__ __forceinline__ double* pop(int q) const { return q < spops ? sm + (size_t)q * nn : gl + (size_t)q * nn; }
 };
 
 #ifndef WG_LBM_MIN_BLOCKS
@@ -44,7 +59,7 @@ struct LbmLayout {
 // into the scratch S; returns this thread's trapezoid mass partial of the
 // collided state.  Uniform: every thread of the CTA calls it.
 template <int N, int L>
-__device__ __forceinline__ double decode_stream_collide(const StepArgs& a, double* T, double* S, uint32_t p,
+__device__ __forceinline__ double decode_stream_collide(const StepArgs& a, double* T, const LbmScratch& S, uint32_t p,
                                                         const PatchPos& pp, int s, int li, bool lane_ok) {
     using Lay = LbmLayout<N>;
     constexpr int TP = Lay::TP, NT = Lay::NT, NN = N * N;
@@ -93,7 +108,7 @@ __device__ __forceinline__ double decode_stream_collide(const StepArgs& a, doubl
         if (lane_ok) {  // pull streaming f_q(x) <- f_q(x - c_q), ghost ring included
 #endif
             const int cx = lbm_cx(q), cy = lbm_cy(q);
-            double* Sq = S + (size_t)q * NN;
+            double* Sq = S.pop(q);
             const int j = li;
 #pragma unroll 5
             for (int i = 0; i < N; ++i) Sq[i * N + j] = T[(i + 1 - cx) * TP + (j + 1 - cy)];
@@ -112,8 +127,8 @@ __device__ __forceinline__ double decode_stream_collide(const StepArgs& a, doubl
         double f0[9], f1[9];
 #pragma unroll
         for (int q = 0; q < 9; ++q) {
-            f0[q] = S[(size_t)q * NN + c0];
-            f1[q] = two ? S[(size_t)q * NN + c1] : 1.0;
+            f0[q] = S.pop(q)[c0];
+            f1[q] = two ? S.pop(q)[c1] : 1.0;
         }
         lbm_collide(f0, a.omega);
         lbm_collide(f1, a.omega);
@@ -122,10 +137,10 @@ __device__ __forceinline__ double decode_stream_collide(const StepArgs& a, doubl
         const double w1 = ((i1 == 0 || i1 == N - 1) ? 0.5 : 1.0) * ((j1 == 0 || j1 == N - 1) ? 0.5 : 1.0);
 #pragma unroll
         for (int q = 0; q < 9; ++q) {
-            S[(size_t)q * NN + c0] = f0[q];
+            S.pop(q)[c0] = f0[q];
             mfv += w0 * f0[q];
             if (two) {
-                S[(size_t)q * NN + c1] = f1[q];
+                S.pop(q)[c1] = f1[q];
                 mfv += w1 * f1[q];
             }
         }
@@ -157,7 +172,8 @@ __global__ void __launch_bounds__(LbmLayout<N>::NT, WG_LBM_MIN_BLOCKS) k_lbm_ste
     const bool lane_ok = t < Lay::SLOTS * N;
     const ShardGeom& g = a.g;
     double* T = tiles + (lane_ok ? s : 0) * TILE;
-    double* S = a.scratch + (size_t)blockIdx.x * Lay::scratch_doubles();
+    const LbmScratch S{reinterpret_cast<double*>(inc + NT), a.scratch + (size_t)blockIdx.x * Lay::scratch_doubles(),
+                       Lay::SPOPS, NN};
 
     if (MODE == MODE_DECODE) {
         for (uint32_t p = blockIdx.x; p < g.npatch; p += gridDim.x) {
@@ -201,7 +217,7 @@ __global__ void __launch_bounds__(LbmLayout<N>::NT, WG_LBM_MIN_BLOCKS) k_lbm_ste
                 const double ux = a.ic_delta * a.ic_u0 * sin(2.0 * 3.141592653589793 * (Y + 0.25));
                 const double usq = ux * ux + uy * uy;
 #pragma unroll
-                for (int q = 0; q < 9; ++q) S[(size_t)q * NN + c] = lbm_feq(q, 1.0, lbm_cu(q, ux, uy), usq);
+                for (int q = 0; q < 9; ++q) S.pop(q)[c] = lbm_feq(q, 1.0, lbm_cu(q, ux, uy), usq);
             }
             __syncthreads();
         } else {
@@ -235,7 +251,7 @@ __global__ void __launch_bounds__(LbmLayout<N>::NT, WG_LBM_MIN_BLOCKS) k_lbm_ste
                 if (lane_ok) {
                     const int j = li;
 #pragma unroll
-                    for (int i = 0; i < N; ++i) v[i] = S[(size_t)q * NN + i * N + j];
+                    for (int i = 0; i < N; ++i) v[i] = S.pop(q)[i * N + j];
                     fwd_col_to_tile<N, L>(T, j, v);
                 }
                 __syncthreads();
@@ -318,7 +334,7 @@ __global__ void __launch_bounds__(LbmLayout<N>::NT, WG_LBM_MIN_BLOCKS) k_lbm_ste
                     double* d = slot_ok[s] ? reinterpret_cast<double*>(a.store_out + slot_off[s]) : nullptr;
 #pragma unroll 5
                     for (int i = 0; i < N; ++i) {
-                        const double x = S[(size_t)q * NN + i * N + j];
+                        const double x = S.pop(q)[i * N + j];
                         T[(i + 1) * Lay::TP + j + 1] = x;
                         if (d) d[i * N + j] = x;
                     }
