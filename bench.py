@@ -70,6 +70,19 @@ WORKLOADS = {
 }
 
 B_ALG = {"transport": 16, "swe": 48, "lbm": 144}  # bytes per cell-update, SURVEY §8d
+# fp64 flops per cell-update, SURVEY §8d's count (transport ~49, D2Q9 ~430);
+# SWE: the exact Riemann solves dominate (4 per cell, a few Newton iterations)
+FLOPS_EST = {"transport": 49, "lbm": 430}
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 def run_config(w: dict, steps: int) -> api.RunConfig:
@@ -207,7 +220,7 @@ def bench_reference(args, w: dict):
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (reference initial state)", "config": config_json(args, w),
         "compression_ratio": statistics.fmean(r["ratio"] for r in rows),
-        "cpu_baseline": {"value": mlups, "unit": "MLUPS", "cores": cores, "kind": kind,
+        "cpu_baseline": {"value": mlups, "unit": "MLUPS", "cores": cores, "kind": kind, "cpu": cpu_model(),
                          "sample": f"{len(rows)} steps of the full {w['nx'] - 1}^2 workload, run() of the "
                                    f"{'reference headers (oracle/_ref)' if kind == 'reference' else 'C port'}"},
         "e2e": {"value": mlups, "unit": "MLUPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -365,6 +378,7 @@ def bench_b200(args, w: dict):
                      "avg_launch_ms": launch_ms, "peak_source": pk["source"],
                      "step_share": main_max / tot_ms if tot_ms else None},
         "e2e": e2e,
+        "compute_ceiling": compute_ceiling(lib, w, value / world),  # per GPU
         "gpu_launches": args.steps,  # one fused kernel launch per step (k_*_step<STEP>)
         "clocks": clocks.summary(),
         "device_bytes": info.device_bytes,
@@ -376,12 +390,26 @@ def bench_b200(args, w: dict):
         _, s0, _, _, _ = cpu_run(w, 3, os.cpu_count() or 1)
         cpu_steps = args.cpu_steps or int(max(3, min(2000, 12.0 / max(s0 / 3, 1e-6))))
         mlups, secs, kind, cores, crow = cpu_run(w, cpu_steps, os.cpu_count() or 1)
-        line["cpu_baseline"] = {"value": mlups, "unit": "MLUPS", "cores": cores, "kind": kind,
+        line["cpu_baseline"] = {"value": mlups, "unit": "MLUPS", "cores": cores, "kind": kind, "cpu": cpu_model(),
                                 "sample": f"{len(crow)} steps of the full {w['nx'] - 1}^2 workload ({secs:.1f} s)"}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def compute_ceiling(lib, w, value_mlups):
+    """The fp64 ceiling next to the HBM roofline: measured DFMA
+    throughput of this GPU and, with SURVEY's flop count per cell-update,
+    the compute-bound cell rate and this run's fraction of it."""
+    t = C.c_double()
+    lib.check(lib.wg_dev_fp64_probe(1 << 16, C.byref(t)))
+    out = {"fp64_tflops_measured": t.value, "probe": "8 independent DFMA chains/thread, 8 CTAs x 256 per SM"}
+    fl = FLOPS_EST.get(w["scheme"])
+    if fl:
+        ceil = t.value * 1e12 / fl / 1e6
+        out.update({"flops_per_cell_estimate": fl, "ceiling_mlups": ceil, "frac": value_mlups / ceil})
+    return out
 
 
 def e2e_run(lib, cfg, shard, stream, host, args, dt, dist, copies=1):

@@ -278,6 +278,10 @@ wg_status wg_session_step(wg_session* s, double dt);
 wg_status wg_session_save(wg_session* s, const char* path);
 wg_status wg_session_load(wg_session* s, const char* path);
 
+/* Measured fp64 FMA throughput of the current device in TFLOP/s (2 flops
+ * per DFMA; SURVEY §8d's compute ceiling, reported next to the roofline). */
+wg_status wg_dev_fp64_probe(uint64_t iters, double* tflops);
+
 /* SWE, world > 1: the max wave speed the NEXT step's dt is computed from
  * (IEEE bits of a non-negative double, so an int64 MAX is the double max).
  * Multi-GPU callers all-reduce it with MAX after every upload and step —

@@ -227,6 +227,7 @@ _PROTOS = {
     "wg_session_sync": (i32, [vp]),
     "wg_session_profile": (i32, [vp, i32]),
     "wg_session_profile_read": (i32, [vp, dp, P(u64)]),
+    "wg_dev_fp64_probe": (i32, [u64, dp]),
     "wg_dev_dwt2d": (i32, [vp, vp, u64, u64, i32, u64, vp]),
     "wg_dev_idwt2d": (i32, [vp, vp, u64, u64, i32, u64, vp]),
 }

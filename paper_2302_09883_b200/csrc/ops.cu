@@ -677,4 +677,45 @@ wg_status wg_lbm_step(const wg_grid_desc* d, const double* cur, double* next, do
     });
 }
 
+// fp64 issue ceiling of this GPU (SURVEY §8d "measure the fp64 compute
+// ceiling with a microbenchmark"): 8 independent DFMA chains per thread,
+// enough CTAs to fill every SM; *tflops = 2 * FMAs / second.
+__global__ void k_fp64_probe(double* sink, uint64_t iters, double a, double b) {
+    double x[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) x[k] = threadIdx.x * 1e-9 + k;
+    for (uint64_t i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) x[k] = __fma_rn(x[k], a, b);
+    }
+    double s = 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s += x[k];
+    if (s == 12345.678) sink[0] = s;  // keeps the chains live
+}
+
+wg_status wg_dev_fp64_probe(uint64_t iters, double* tflops) {
+    return guard([&] {
+        int sms = 0, dev = 0;
+        WG_CUDA(cudaGetDevice(&dev));
+        WG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        const int blocks = sms * 8, threads = 256;
+        DevBuf<double> sink(1);
+        cudaEvent_t e0, e1;
+        WG_CUDA(cudaEventCreate(&e0));
+        WG_CUDA(cudaEventCreate(&e1));
+        k_fp64_probe<<<blocks, threads>>>(sink.p, iters / 10 + 1, 0.999999, 1e-7);  // warm-up
+        WG_CUDA(cudaEventRecord(e0));
+        k_fp64_probe<<<blocks, threads>>>(sink.p, iters, 0.999999, 1e-7);
+        WG_CUDA(cudaEventRecord(e1));
+        WG_CUDA(cudaEventSynchronize(e1));
+        WG_LAUNCH_CHECK("fp64 probe");
+        float ms = 0.f;
+        WG_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        *tflops = 2.0 * 8.0 * (double)iters * blocks * threads / (ms * 1e-3) / 1e12;
+    });
+}
+
 }  // extern "C"
