@@ -148,9 +148,11 @@ __device__ __forceinline__ bool decode_row(double* T, int li, const DirEntry e,
         return true;
     }
     if (raw) {
-        const double* d = reinterpret_cast<const double*>(base) + (size_t)li * N;
+        // a raw block fills the whole tile interior; thread li copies COLUMN
+        // li so that consecutive threads read consecutive addresses
+        const double* d = reinterpret_cast<const double*>(base) + li;
 #pragma unroll 8
-        for (int j = 0; j < N; ++j) rowp[j] = d[j];
+        for (int i = 0; i < N; ++i) T[(i + 1) * TP + li + 1] = d[(size_t)i * N];
     } else {
         const double* v = reinterpret_cast<const double*>(base);
         const uint32_t* col = reinterpret_cast<const uint32_t*>(base + 8ull * e.nnz);
