@@ -26,6 +26,7 @@ struct KernelSet {
 // Each returns false when (n, levels) has no instantiation.
 bool select_transport_kernels(uint64_t n, int levels, bool half_lines, KernelSet& out);  // kt_transport.cu
 bool select_lbm_kernels(uint64_t n, int levels, bool half_lines, KernelSet& out);        // kt_lbm.cu
+bool select_lbm_group_kernels(int levels, KernelSet& out);                              // kt_lbm_group.cu
 bool select_swe_kernels(uint64_t n, int levels, KernelSet& out);                         // kt_swe*.cu
 bool select_swe65_kernels(int levels, KernelSet& out);                                  // kt_swe65.cu
 

@@ -22,16 +22,20 @@ namespace wg {
 
 constexpr int kGL = 8;  // lanes per line
 
-__device__ __forceinline__ double seg_up(double x, int d) { return __shfl_up_sync(0xffffffffu, x, d, kGL); }
-__device__ __forceinline__ double seg_down(double x, int d) { return __shfl_down_sync(0xffffffffu, x, d, kGL); }
-__device__ __forceinline__ double seg_idx(double x, int src) { return __shfl_sync(0xffffffffu, x, src, kGL); }
+// m: the lanes taking part (the caller's 8-lane segment, or the full warp)
+__device__ __forceinline__ double seg_up(unsigned m, double x, int d) { return __shfl_up_sync(m, x, d, kGL); }
+__device__ __forceinline__ double seg_down(unsigned m, double x, int d) { return __shfl_down_sync(m, x, d, kGL); }
+__device__ __forceinline__ double seg_idx(unsigned m, double x, int src) { return __shfl_sync(m, x, src, kGL); }
+
+// The 8-lane segment of the calling lane as a shuffle mask.
+__device__ __forceinline__ unsigned seg_mask() { return 0xFFu << (threadIdx.x & 24); }
 
 __device__ __forceinline__ double lift_wr(int k, int half) { return (k == 0 || k == half - 1) ? 0.5 : 0.25; }
 
 // Forward L-level transform.  x: the lane's E + 1 elements; r: lane in the
 // segment (0..7).  All 32 lanes of the warp must call it (shuffles).
 template <int N, int L>
-__device__ __forceinline__ void dwt_line_grp(double (&x)[(N - 1) / kGL + 1], int r) {
+__device__ __forceinline__ void dwt_line_grp(double (&x)[(N - 1) / kGL + 1], int r, unsigned m = 0xffffffffu) {
     constexpr int E = (N - 1) / kGL;
 #pragma unroll
     for (int l = 1; l <= L; ++l) {
@@ -48,25 +52,25 @@ __device__ __forceinline__ void dwt_line_grp(double (&x)[(N - 1) / kGL + 1], int
                 x[e] = x[e] + lift_upd(lift_wr(k - 1, half), x[e - s], lift_wr(k, half), x[e + s]);
             }
             // the shared boundary elements: the detail across the boundary
-            const double dl = seg_up(x[E - s], 1), dr = seg_down(x[s], 1);
+            const double dl = seg_up(m, x[E - s], 1), dr = seg_down(m, x[s], 1);
             const int k0 = (E * r) / (2 * s), k1 = (E * r + E) / (2 * s);
             if (r > 0) x[0] = x[0] + lift_upd(lift_wr(k0 - 1, half), dl, lift_wr(k0, half), x[s]);
             if (r < kGL - 1) x[E] = x[E] + lift_upd(lift_wr(k1 - 1, half), x[E - s], lift_wr(k1, half), dr);
         } else {
             const int t = s / E;  // lane stride; y_j = lane j's x[0], y_8 = lane 7's x[E]
-            const double last = seg_idx(x[E], kGL - 1);
+            const double last = seg_idx(m, x[E], kGL - 1);
             {
-                const double yl = seg_up(x[0], t), yr0 = seg_down(x[0], t);
+                const double yl = seg_up(m, x[0], t), yr0 = seg_down(m, x[0], t);
                 const double yr = (r + t == kGL) ? last : yr0;
                 if ((r % (2 * t)) == t) x[0] = lift_pred_fwd(x[0], yl, yr);
             }
             {
-                const double dl = seg_up(x[0], t), dr = seg_down(x[0], t);
+                const double dl = seg_up(m, x[0], t), dr = seg_down(m, x[0], t);
                 const int k = r / (2 * t);
                 if (r > 0 && (r % (2 * t)) == 0 && r + t < kGL)
                     x[0] = x[0] + lift_upd(lift_wr(k - 1, half), dl, lift_wr(k, half), dr);
             }
-            const double nxt = seg_down(x[0], 1);
+            const double nxt = seg_down(m, x[0], 1);
             if (r < kGL - 1) x[E] = nxt;
         }
     }
@@ -74,14 +78,14 @@ __device__ __forceinline__ void dwt_line_grp(double (&x)[(N - 1) / kGL + 1], int
 
 // Inverse L-level transform (in place, interleaved order).
 template <int N, int L>
-__device__ __forceinline__ void idwt_line_grp(double (&x)[(N - 1) / kGL + 1], int r) {
+__device__ __forceinline__ void idwt_line_grp(double (&x)[(N - 1) / kGL + 1], int r, unsigned m = 0xffffffffu) {
     constexpr int E = (N - 1) / kGL;
 #pragma unroll
     for (int l = L; l >= 1; --l) {
         const int s = 1 << (l - 1);
         const int half = ((N - 1) / s) / 2;
         if (s < E) {
-            const double dl = seg_up(x[E - s], 1), dr = seg_down(x[s], 1);
+            const double dl = seg_up(m, x[E - s], 1), dr = seg_down(m, x[s], 1);
             const int k0 = (E * r) / (2 * s), k1 = (E * r + E) / (2 * s);
             if (r > 0) x[0] = x[0] - lift_upd(lift_wr(k0 - 1, half), dl, lift_wr(k0, half), x[s]);
             if (r < kGL - 1) x[E] = x[E] - lift_upd(lift_wr(k1 - 1, half), x[E - s], lift_wr(k1, half), dr);
@@ -95,18 +99,18 @@ __device__ __forceinline__ void idwt_line_grp(double (&x)[(N - 1) / kGL + 1], in
         } else {
             const int t = s / E;
             {
-                const double dl = seg_up(x[0], t), dr = seg_down(x[0], t);
+                const double dl = seg_up(m, x[0], t), dr = seg_down(m, x[0], t);
                 const int k = r / (2 * t);
                 if (r > 0 && (r % (2 * t)) == 0 && r + t < kGL)
                     x[0] = x[0] - lift_upd(lift_wr(k - 1, half), dl, lift_wr(k, half), dr);
             }
             {
-                const double last = seg_idx(x[E], kGL - 1);
-                const double yl = seg_up(x[0], t), yr0 = seg_down(x[0], t);
+                const double last = seg_idx(m, x[E], kGL - 1);
+                const double yl = seg_up(m, x[0], t), yr0 = seg_down(m, x[0], t);
                 const double yr = (r + t == kGL) ? last : yr0;
                 if ((r % (2 * t)) == t) x[0] = lift_pred_inv(x[0], yl, yr);
             }
-            const double nxt = seg_down(x[0], 1);
+            const double nxt = seg_down(m, x[0], 1);
             if (r < kGL - 1) x[E] = nxt;
         }
     }
