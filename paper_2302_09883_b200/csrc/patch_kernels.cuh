@@ -76,11 +76,14 @@ __device__ __forceinline__ void decode_and_fv(const StepArgs& a, double* T, bool
     }
 }
 
+// CTAs per SM the register allocation targets: 2 (spilling ~1 KB) measured
+// best for 33-point patches (88 vs 86 GLUPS at 4096^2), 1 (no spills) for
+// 65-point patches (75 vs 73)
 #ifndef WG_MIN_BLOCKS
-#define WG_MIN_BLOCKS 2
+#define WG_MIN_BLOCKS(N) ((N) >= 65 ? 1 : 2)
 #endif
 template <int N, int L, int P, int MODE>
-__global__ void __launch_bounds__(Layout<N, P>::NT, WG_MIN_BLOCKS)
+__global__ void __launch_bounds__(Layout<N, P>::NT, WG_MIN_BLOCKS(N))
     k_patch_step(const __grid_constant__ StepArgs a) {
     using Lay = Layout<N, P>;
     constexpr int TP = Lay::TP, TILE = Lay::TILE, NT = Lay::NT;
