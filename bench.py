@@ -75,6 +75,12 @@ B_ALG = {"transport": 16, "swe": 48, "lbm": 144}  # bytes per cell-update, SURVE
 FLOPS_EST = {"transport": 49, "lbm": 430}
 
 
+def data_label(w: dict) -> str:
+    return {"lbm": "synthetic (shear-layer D2Q9 initial state)",
+            "swe": "synthetic (reference dam-break initial state, pipeline.hpp:144-155)"}.get(
+                w["scheme"], "synthetic (reference initial state, exact_transport at t=0)")
+
+
 def cpu_model() -> str:
     try:
         for line in open("/proc/cpuinfo"):
@@ -217,8 +223,8 @@ def bench_reference(args, w: dict):
     line = {
         "impl": "reference", "metric": METRIC, "value": mlups, "unit": "MLUPS", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * secs / len(rows),
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (reference initial state)", "config": config_json(args, w),
+        "higher_is_better": True, "scaling": w.get("scaling", "weak"), "vs_baseline": None, "dtype": "f64",
+        "data": data_label(w), "config": config_json(args, w),
         "compression_ratio": statistics.fmean(r["ratio"] for r in rows),
         "cpu_baseline": {"value": mlups, "unit": "MLUPS", "cores": cores, "kind": kind, "cpu": cpu_model(),
                          "sample": f"{len(rows)} steps of the full {w['nx'] - 1}^2 workload, run() of the "
@@ -364,9 +370,7 @@ def bench_b200(args, w: dict):
         "metric": METRIC, "value": value, "unit": "MLUPS", "n_gpus": world, "steps": args.steps,
         "warmup": warm_steps, "ms_per_step": tot_ms / args.steps, "higher_is_better": True,
         "scaling": "weak" if weak else "strong", "vs_baseline": None, "dtype": "f64",
-        "data": {"lbm": "synthetic (shear-layer D2Q9 initial state)",
-                 "swe": "synthetic (reference dam-break initial state, pipeline.hpp:144-155)"}.get(
-                     w["scheme"], "synthetic (reference initial state)"),
+        "data": data_label(w),
         "config": config_json(args, w),
         "compression_ratio": statistics.fmean(r["ratio"] for r in timed_rows),
         "compressed_bytes_per_step": statistics.fmean(r["compressed_bytes"] for r in timed_rows),
