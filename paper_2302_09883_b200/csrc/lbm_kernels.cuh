@@ -71,11 +71,7 @@ __device__ __forceinline__ double decode_stream_collide(const StepArgs& a, doubl
     double* TR = T + (rs - s) * (Lay::TILE);
     for (int rd = 0; rd < 3; ++rd) {
         const int q = 3 * rd + s;
-#ifdef WG_ABL_NO_DECODE
-        if (false) {
-#else
         if (lane_ok) {
-#endif
 #ifdef WG_BOUNDS_CHECK
             {
                 const DirEntry e = a.dir_in[(size_t)p * 9 + 3 * rd + rs];
@@ -91,22 +87,14 @@ __device__ __forceinline__ double decode_stream_collide(const StepArgs& a, doubl
         // (threads past the 3 slots have q = 9..11: they must not read — the
         // last patch's q = 9 lies past the end of the directory)
         const bool raw_in = lane_ok && (a.dir_in[(size_t)p * 9 + q].flags & (DIR_RAW | DIR_DEAD)) != 0;
-#ifdef WG_ABL_NO_DECODE
-        if (false) {
-#else
         if (lane_ok && !raw_in) {
-#endif
             double v[N];
             decode_col<N, L>(T, li, false, v);
             store_col<N>(T, li, v);
         }
         __syncthreads();
         WG_PHASE_MARK(rd == 0 ? 0 : 12);
-#ifdef WG_ABL_NO_STREAM
-        if (false) {
-#else
         if (lane_ok) {  // pull streaming f_q(x) <- f_q(x - c_q), ghost ring included
-#endif
             const int cx = lbm_cx(q), cy = lbm_cy(q);
             double* Sq = S.pop(q);
             const int j = li;
@@ -118,9 +106,6 @@ __device__ __forceinline__ double decode_stream_collide(const StepArgs& a, doubl
     }
     double mfv = 0.0;
     // two cells per iteration: 18 independent scratch loads in flight
-#ifdef WG_ABL_NO_COLLIDE
-    if (false)
-#endif
     for (int c0 = threadIdx.x; c0 < NN; c0 += 2 * NT) {
         const int c1 = c0 + NT;
         const bool two = c1 < NN;
