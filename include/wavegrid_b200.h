@@ -305,6 +305,11 @@ wg_status wg_session_metrics(wg_session* s, wg_metrics_row* rows,
  * session stream: the per-step device->host result read of the e2e path). */
 wg_status wg_session_last_row(wg_session* s, wg_metrics_row* row);
 
+/* The same read enqueued on the session stream without synchronising: the
+ * row lands in `row` (page-locked host memory) once the stream reaches it
+ * (after wg_session_sync).  The per-step result read of a pipelined loop. */
+wg_status wg_session_last_row_async(wg_session* s, wg_metrics_row* row);
+
 /* Decode the current state into a host grid buffer (logical cells). */
 wg_status wg_session_download(wg_session* s, double* host_grid);
 

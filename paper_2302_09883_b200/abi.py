@@ -222,6 +222,7 @@ _PROTOS = {
     "wg_session_load": (i32, [vp, C.c_char_p]),
     "wg_session_metrics": (i32, [vp, P(MetricsRowC), u64, P(u64)]),
     "wg_session_last_row": (i32, [vp, P(MetricsRowC)]),
+    "wg_session_last_row_async": (i32, [vp, vp]),
     "wg_session_download": (i32, [vp, dp]),
     "wg_session_patch_csr": (i32, [vp, u64, u32, dp, P(u32), P(u32), P(u64), P(i32)]),
     "wg_session_sync": (i32, [vp]),

@@ -54,18 +54,20 @@ namespace {
 // ---- upload: raw store + edge lines from a grid buffer (one thread per
 // logical element: consecutive threads read consecutive addresses, which
 // matters when the source is page-locked host memory read over the bus) ----
-__global__ void k_upload(const double* grid, uint32_t N, ShardGeom g, unsigned char* store, DirEntry* dir,
-                         EdgeSet e) {
+// grid holds patches [p0, p0 + count) (a chunk of the shard's grid buffer).
+__global__ void k_upload(const double* grid, uint32_t N, ShardGeom g, uint32_t p0, uint32_t count,
+                         unsigned char* store, DirEntry* dir, EdgeSet e) {
     const uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     const uint64_t per = (uint64_t)N * N;
-    if (t >= (uint64_t)g.npatch * g.m * per) return;
-    const uint64_t pq = t / per;  // patch * m + q
+    if (t >= (uint64_t)count * g.m * per) return;
+    const uint64_t lq = t / per;                   // local patch * m + q
+    const uint64_t pq = (uint64_t)p0 * g.m + lq;  // patch * m + q
     const uint32_t i = (uint32_t)((t % per) / N), j = (uint32_t)(t % N);
     const uint32_t p = (uint32_t)(pq / g.m), q = (uint32_t)(pq % g.m);
     const uint64_t TP = N + 2, tcount = TP * TP;
     const uint64_t block = round16(per * 8);
     const uint64_t off = pq * block;
-    const double x = grid[pq * tcount + (i + 1) * TP + j + 1];
+    const double x = grid[lq * tcount + (i + 1) * TP + j + 1];
     reinterpret_cast<double*>(store + off)[(uint64_t)i * N + j] = x;
     if (i == 0 && j == 0) dir[pq] = DirEntry{off, 0u, DIR_RAW};
     const uint32_t ar = p / g.P1, b = p % g.P1;
@@ -128,6 +130,8 @@ __global__ void k_swe_vmax(const double* grid, uint32_t N, uint64_t npatch, doub
     if ((threadIdx.x & 31) == 0) atomicMax(vmax_bits, (unsigned long long)__double_as_longlong(v));
 }
 
+__global__ void k_set_u64(unsigned long long* p, unsigned long long v) { *p = v; }
+
 __global__ void k_swe_clock_reset(double* td, unsigned long long* vmax_bits, unsigned long long* steps) {
     td[0] = 0.0;
     td[1] = 0.0;
@@ -169,6 +173,10 @@ struct Session {
     // SWE device clock: [t, last dt] (f64), vmax bits [2], steps done (u64)
     unsigned long long* swe = nullptr;
     unsigned long long* phase = nullptr;  // WG_PHASE_TIMING builds only
+    // pinned-host upload pipeline (created on first use)
+    double* stage = nullptr;
+    cudaStream_t copy_stream = nullptr;
+    cudaEvent_t stage_ev[4] = {};
     uint64_t launched = 0;  // SWE step launches (steps past t_end are no-ops)
     uint64_t row0 = 0;      // step count at upload/load: rows[k] holds step row0 + k + 1
 
@@ -228,6 +236,14 @@ struct Session {
         swe = nullptr;
         cudaFree(phase);
         phase = nullptr;
+        if (copy_stream) {
+            cudaStreamSynchronize(copy_stream);
+            for (auto& ev : stage_ev) cudaEventDestroy(ev);
+            cudaStreamDestroy(copy_stream);
+            copy_stream = nullptr;
+        }
+        cudaFree(stage);
+        stage = nullptr;
         partials = nullptr;
         done = nullptr;
         bump = nullptr;
@@ -249,6 +265,10 @@ struct Session {
     }
 
     bool is_swe() const { return cfg.scheme == WG_SCHEME_SWE; }
+    // patches per staging chunk of a pinned-host upload (16 MB of grid buffer)
+    uint32_t stage_chunk() const {
+        return (uint32_t)std::max<uint64_t>(1, (16ull << 20) / ((uint64_t)sg.m * geo.tcount * 8));
+    }
     double* swe_td() const { return reinterpret_cast<double*>(swe); }
 
     uint64_t halo_doubles() const { return (uint64_t)sg.P1 * sg.me * N; }
@@ -345,6 +365,10 @@ struct Session {
         WG_CUDA(cudaMemsetAsync(phase, 0, 32 * sizeof(unsigned long long), stream));
 #endif
         grow_rows(1024);
+        // the pinned-host upload pipeline (allocated here, outside any timed upload)
+        stage = dalloc<double>(2 * (uint64_t)stage_chunk() * sg.m * geo.tcount);
+        WG_CUDA(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking));
+        for (auto& ev : stage_ev) WG_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
     }
 
     void grow_rows(uint64_t need) {
@@ -368,29 +392,59 @@ struct Session {
         row_cap = nc;
     }
 
-    void upload_dev(const double* dgrid) {
+    // The raw initial store from a grid buffer in device memory, or (pinned
+    // != nullptr) streamed from page-locked host memory: chunks of patches
+    // copied by the DMA engine on a second stream while the previous chunk
+    // is being stored (double-buffered staging).
+    void upload_dev(const double* dgrid, const double* pinned = nullptr) {
         const uint64_t raw_block = round16((uint64_t)N * N * 8);
         const uint64_t need = (uint64_t)sg.npatch * sg.m * raw_block;
         if (need > cap)
             raise(WG_OUT_OF_MEMORY, "initial state does not fit the compressed-store budget");
         cur = 0;
-        const uint64_t threads = (uint64_t)sg.npatch * sg.m * N * N;
-        k_upload<<<(unsigned)((threads + 255) / 256), 256, 0, stream>>>(dgrid, N, sg, store[cur], dir[cur],
-                                                                         edges[cur]);
-        WG_LAUNCH_CHECK("upload");
-        const unsigned long long used = need;
-        WG_CUDA(cudaMemcpyAsync(bump + cur, &used, sizeof used, cudaMemcpyHostToDevice, stream));
+        if (is_swe()) WG_CUDA(cudaMemsetAsync(swe + 2, 0, sizeof(unsigned long long), stream));
+        const uint64_t per = (uint64_t)sg.m * geo.tcount;  // doubles per patch in the grid buffer
+        auto store_chunk = [&](const double* src, uint32_t p0, uint32_t cnt) {
+            const uint64_t threads = (uint64_t)cnt * sg.m * N * N;
+            k_upload<<<(unsigned)((threads + 255) / 256), 256, 0, stream>>>(src, N, sg, p0, cnt, store[cur], dir[cur],
+                                                                             edges[cur]);
+            WG_LAUNCH_CHECK("upload");
+            if (is_swe()) {
+                const uint64_t cells = (uint64_t)cnt * N * N;
+                k_swe_vmax<<<(unsigned)((cells + 255) / 256), 256, 0, stream>>>(src, N, cnt, cfg.gravity, swe + 2,
+                                                                                err);
+                WG_LAUNCH_CHECK("swe wave speed");
+            }
+        };
+        if (!pinned) {
+            store_chunk(dgrid, 0, sg.npatch);
+        } else {
+            const uint32_t chunk = stage_chunk();
+            const uint32_t nch = (sg.npatch + chunk - 1) / chunk;
+            cudaEvent_t* copied = stage_ev;
+            cudaEvent_t* consumed = stage_ev + 2;
+            WG_CUDA(cudaEventRecord(consumed[0], stream));  // earlier work on the session stream first
+            WG_CUDA(cudaEventRecord(consumed[1], stream));
+            for (uint32_t c = 0; c < nch; ++c) {
+                const int k = c & 1;
+                const uint32_t p0 = c * chunk, cnt = std::min<uint32_t>(chunk, sg.npatch - p0);
+                double* buf = stage + (uint64_t)k * chunk * per;
+                WG_CUDA(cudaStreamWaitEvent(copy_stream, consumed[k], 0));
+                WG_CUDA(cudaMemcpyAsync(buf, pinned + (uint64_t)p0 * per, (uint64_t)cnt * per * 8,
+                                        cudaMemcpyHostToDevice, copy_stream));
+                WG_CUDA(cudaEventRecord(copied[k], copy_stream));
+                WG_CUDA(cudaStreamWaitEvent(stream, copied[k], 0));
+                store_chunk(buf, p0, cnt);
+                WG_CUDA(cudaEventRecord(consumed[k], stream));
+            }
+        }
+        k_set_u64<<<1, 1, 0, stream>>>(bump + cur, need);  // no host round trip: steps queue behind
+        WG_LAUNCH_CHECK("upload bump");
         WG_CUDA(cudaMemsetAsync(bump + (1 - cur), 0, sizeof(unsigned long long), stream));
         if (is_swe()) {
-            WG_CUDA(cudaMemsetAsync(swe + 2, 0, sizeof(unsigned long long), stream));
-            const uint64_t cells = (uint64_t)sg.npatch * N * N;
-            k_swe_vmax<<<(unsigned)((cells + 255) / 256), 256, 0, stream>>>(dgrid, N, sg.npatch, cfg.gravity,
-                                                                            swe + 2, err);
-            WG_LAUNCH_CHECK("swe wave speed");
             k_swe_clock_reset<<<1, 1, 0, stream>>>(swe_td(), swe + 2, swe + 4);
             WG_LAUNCH_CHECK("swe clock");
         }
-        WG_CUDA(cudaStreamSynchronize(stream));  // `used` lives on this stack frame
         step = 0;
         launched = 0;
         row0 = 0;
@@ -398,12 +452,13 @@ struct Session {
     }
 
     void upload_host(const double* hgrid) {
-        // page-locked host memory is read by the upload kernel directly over
-        // the bus (UVA, no staging copy); pageable memory is staged
+        // page-locked host memory is streamed in chunks by the DMA engine
+        // (overlapped with storing the previous chunk); pageable memory is
+        // copied whole first
         cudaPointerAttributes at{};
         if (cudaPointerGetAttributes(&at, hgrid) == cudaSuccess && at.type == cudaMemoryTypeHost &&
             at.devicePointer) {
-            upload_dev(static_cast<const double*>(at.devicePointer));
+            upload_dev(nullptr, hgrid);
             return;
         }
         cudaGetLastError();  // clear a failed attribute query on pageable memory
@@ -411,6 +466,7 @@ struct Session {
         DevBuf<double> d(n);
         WG_CUDA(cudaMemcpyAsync(d.p, hgrid, n * sizeof(double), cudaMemcpyHostToDevice, stream));
         upload_dev(d.p);
+        WG_CUDA(cudaStreamSynchronize(stream));  // d dies with this scope
     }
 
     // Initial state generated and compressed on the device (no host grid):
@@ -991,6 +1047,16 @@ wg_status wg_session_last_row(wg_session* sp, wg_metrics_row* row) {
         WG_CUDA(cudaMemcpyAsync(row, s->rows + (s->step - 1 - s->row0), sizeof(wg_metrics_row), cudaMemcpyDeviceToHost,
                                 s->stream));
         s->sync();
+    });
+}
+
+wg_status wg_session_last_row_async(wg_session* sp, wg_metrics_row* row) {
+    return guard([&] {
+        Session* s = reinterpret_cast<Session*>(sp);
+        const uint64_t done = s->is_swe() ? s->launched : s->step;  // SWE: the last launch's row
+        if (done <= s->row0) raise(WG_LOGIC, "no step has run");
+        WG_CUDA(cudaMemcpyAsync(row, s->rows + (done - 1 - s->row0), sizeof(wg_metrics_row), cudaMemcpyDeviceToHost,
+                                s->stream));
     });
 }
 
