@@ -4,6 +4,17 @@
 #include "kt_common.cuh"
 #include "patch_kernels.cuh"
 
+// patches per CTA, measured at 4096^2: 65-point patches 3 per CTA (7 warps
+// at 1 CTA/SM: 97 GLUPS; 2 -> 74, 4 -> 67), 33-point patches 7 per CTA
+// (256 threads at 2 CTAs/SM: 113 GLUPS; 4 -> 91, 5 -> 105, 6 -> 103,
+// 8 -> 87, 12 -> 63)
+#ifndef WG_T65_P
+#define WG_T65_P 3
+#endif
+#ifndef WG_T33_P
+#define WG_T33_P 7
+#endif
+
 namespace wg {
 namespace {
 
@@ -34,9 +45,9 @@ bool select_transport_kernels(uint64_t n, int levels, bool half_lines, KernelSet
     switch (n) {
         case 9: return pick_level<FullT<7>::M, 9, kMaxLevels>(levels, k);
         case 17: return pick_level<FullT<15>::M, 17, kMaxLevels>(levels, k);
-        case 33: return pick_level<FullT<8>::M, 33, kMaxLevels>(levels, k);
+        case 33: return pick_level<FullT<WG_T33_P>::M, 33, kMaxLevels>(levels, k);
         case 65: return half_lines ? pick_level<HalfT, 65, 6>(levels, k)
-                                   : pick_level<FullT<2>::M, 65, kMaxLevels>(levels, k);
+                                   : pick_level<FullT<WG_T65_P>::M, 65, kMaxLevels>(levels, k);
         default: return false;
     }
 }
