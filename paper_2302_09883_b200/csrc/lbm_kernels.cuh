@@ -22,6 +22,10 @@
 
 namespace wg {
 
+#ifndef WG_LBM_EXTRA_WARPS
+#define WG_LBM_EXTRA_WARPS 1  // 256 threads: the cell phases (stream, collide) get a warp more (+1-2 %)
+#endif
+
 #ifndef WG_LBM_SMEM_POPS
 #define WG_LBM_SMEM_POPS 0  // 3 measured no faster (C2 7.83 vs 7.86 GLUPS): the L2 scratch is not the bound
 #endif
@@ -31,7 +35,7 @@ struct LbmLayout {
     static constexpr int TP = N + 2;
     static constexpr int TILE = TP * TP;
     static constexpr int SLOTS = 3;
-    static constexpr int NT = ((SLOTS * N + 31) / 32) * 32;
+    static constexpr int NT = ((SLOTS * N + 31) / 32) * 32 + 32 * WG_LBM_EXTRA_WARPS;
     // 3 tiles + the scan buffer: 109.5 KB at N = 65, so two CTAs fit an SM
     // (the per-patch mass reductions reuse the tiles once a patch is done)
     // the first SPOPS populations of the scratch live in shared memory (the

@@ -24,11 +24,17 @@
 
 namespace wg {
 
+// one warp beyond the 3 x 65 line threads: 256 threads at 2 CTAs/SM (the
+// cell-parallel Godunov phase gets them): 5.35 vs 4.84 GLUPS at C3
+#ifndef WG_SWE_EXTRA_WARPS
+#define WG_SWE_EXTRA_WARPS 1
+#endif
+
 template <int N>
 struct SweLayout {
     static constexpr int TP = N + 2;
     static constexpr int TILE = TP * TP;
-    static constexpr int NT = ((3 * N + 31) / 32) * 32;
+    static constexpr int NT = ((3 * N + 31) / 32) * 32 + 32 * WG_SWE_EXTRA_WARPS;  // extra warps: FV cells
     static constexpr size_t smem_bytes() {
         return sizeof(double) * (size_t)(3 * TILE) + sizeof(unsigned long long) * NT;
     }
