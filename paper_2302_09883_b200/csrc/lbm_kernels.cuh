@@ -22,6 +22,10 @@
 
 namespace wg {
 
+#ifndef WG_LBM_PREFETCH
+#define WG_LBM_PREFETCH 1
+#endif
+
 #ifndef WG_LBM_EXTRA_WARPS
 #define WG_LBM_EXTRA_WARPS 1  // 256 threads: the cell phases (stream, collide) get a warp more (+1-2 %)
 #endif
@@ -212,7 +216,7 @@ __global__ void __launch_bounds__(LbmLayout<N>::NT, WG_LBM_MIN_BLOCKS) k_lbm_ste
         } else {
             mfv = decode_stream_collide<N, L>(a, T, S, p, pp, s, li, lane_ok);
         }
-        if (MODE != MODE_INIT && pn < g.npatch && lane_ok) {  // warm L2 with the next patch's inputs
+        if (WG_LBM_PREFETCH && MODE != MODE_INIT && pn < g.npatch && lane_ok) {  // warm L2 with the next patch's inputs
             for (int q = s; q < 9; q += 3) prefetch_block<N>(a, next_dir[q], li, N);
             prefetch_edges<N>(a, pn, t, Lay::SLOTS * N);
         }
