@@ -24,13 +24,15 @@ struct KernelSet {
 };
 
 // Each returns false when (n, levels) has no instantiation.
-bool select_transport_kernels(uint64_t n, int levels, bool half_lines, KernelSet& out);  // kt_transport.cu
+// small_grid: fewer patches than the CTAs of a full wave at the default
+// patches-per-CTA: one patch per CTA spreads them over more SMs
+bool select_transport_kernels(uint64_t n, int levels, bool half_lines, bool small_grid, KernelSet& out);  // kt_transport.cu
 bool select_lbm_kernels(uint64_t n, int levels, bool half_lines, KernelSet& out);        // kt_lbm.cu
 bool select_lbm_group_kernels(int levels, KernelSet& out);                              // kt_lbm_group.cu
 bool select_swe_kernels(uint64_t n, int levels, KernelSet& out);                         // kt_swe*.cu
 bool select_swe65_kernels(int levels, KernelSet& out);                                  // kt_swe65.cu
 
 // Raises WG_INVALID_ARGUMENT when unsupported (session.cu).
-KernelSet select_kernels(int scheme, uint64_t n, int levels);
+KernelSet select_kernels(int scheme, uint64_t n, int levels, uint64_t npatch);
 
 }  // namespace wg

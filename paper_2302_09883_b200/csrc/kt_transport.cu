@@ -41,7 +41,8 @@ struct HalfT {
 
 }  // namespace
 
-bool select_transport_kernels(uint64_t n, int levels, bool half_lines, KernelSet& k) {
+bool select_transport_kernels(uint64_t n, int levels, bool half_lines, bool small_grid, KernelSet& k) {
+    if (small_grid && n == 33) return pick_level<FullT<1>::M, 33, kMaxLevels>(levels, k);
     switch (n) {
         case 9: return pick_level<FullT<7>::M, 9, kMaxLevels>(levels, k);
         case 17: return pick_level<FullT<15>::M, 17, kMaxLevels>(levels, k);

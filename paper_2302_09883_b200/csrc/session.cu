@@ -29,7 +29,7 @@ namespace {
 // ---- kernel table: kernel_table.h (one translation unit per scheme) ----------
 }  // namespace
 
-KernelSet select_kernels(int scheme, uint64_t n, int levels) {
+KernelSet select_kernels(int scheme, uint64_t n, int levels, uint64_t npatch) {
     KernelSet k{};
     const bool half = std::getenv("WG_HALF_LINES") != nullptr;  // opt-in 65-point half-line variants
     bool ok = false;
@@ -41,7 +41,11 @@ KernelSet select_kernels(int scheme, uint64_t n, int levels) {
         ok = select_swe_kernels(n, levels, k);
         what = "SWE";
     } else {
-        ok = select_transport_kernels(n, levels, half, k);
+        int sms = 148, dev = 0;
+        if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        // C1-sized grids (64 patches of 33 points): one patch per CTA (more SMs busy)
+        const bool small = n == 33 && npatch < 2ull * sms;
+        ok = select_transport_kernels(n, levels, half, small, k);
     }
     if (!ok)
         raise(WG_INVALID_ARGUMENT, std::string("device session (") + what + "): patch side " + std::to_string(n) +
@@ -310,7 +314,7 @@ struct Session {
         sg.world = shard.world;
         sg.npatch = sg.R * sg.P1;
         sg.row0 = (uint32_t)shard.row_begin;
-        ks = select_kernels(cfg.scheme, N, levels);
+        ks = select_kernels(cfg.scheme, N, levels, (uint64_t)(shard.row_end - shard.row_begin) * geo.splits[1]);
         sg.me = ks.edges3 ? 3u : sg.m;
         {
             int per_sm = 0, sms = 0;
