@@ -153,7 +153,11 @@ typedef struct wg_run_config { /* RunConfig + SimConfig, pipeline.hpp:23-38, sol
     uint64_t splits[2];       /* SimConfig::splits                           */
     double cfl, t_end, alpha, beta, gravity, domain_length;
     int32_t threshold_mode;   /* ThresholdSpec::mode (default capped)        */
-    int32_t codec;            /* 1 = CSR (Codec::csr); LZ is out of scope    */
+    int32_t codec;            /* 1 = Codec::csr; 2 = Codec::lz (device session:
+                                 the store stays CSR — both codecs are
+                                 lossless — and every step's compressed_bytes
+                                 and ratio are the exact lz_encode sizes,
+                                 codec.hpp:81-244; transport and D2Q9)       */
     double c, threshold_alpha;/* ThresholdSpec::c, ::alpha                    */
     int32_t no_compression;
     int32_t strict;

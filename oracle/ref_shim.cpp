@@ -185,8 +185,8 @@ RunConfig to_run_config(const wg_run_config* c) {
     rc.sim.domain_length = c->domain_length;
     rc.levels = c->levels;
     rc.spec = ThresholdSpec{to_mode(c->threshold_mode), c->c, c->threshold_alpha};
-    if (c->codec != 1) throw std::invalid_argument("only Codec::csr is on the hot path");
-    rc.codec = Codec::csr;
+    if (c->codec != 1 && c->codec != 2) throw std::invalid_argument("unknown codec");
+    rc.codec = c->codec == 2 ? Codec::lz : Codec::csr;  // chunk_size: the RunConfig default (64 KiB)
     rc.no_compression = c->no_compression != 0;
     rc.strict = c->strict != 0;
     rc.threads = c->threads ? c->threads : 1;
@@ -246,8 +246,8 @@ RunResult run_lbm(const wg_run_config* c) {
                 std::size_t zeroed = 0;
                 for (auto& cs : coeffs) zeroed += apply_threshold(cs, spec);
                 for (std::size_t q = 0; q < m; ++q) comps[q] = std::move(coeffs[q].values);
-                const CompressedPatch enc = encode_patch(
-                    comps, plan.dims, static_cast<std::uint32_t>(c->levels), Codec::csr);
+                const CompressedPatch enc = encode_patch(comps, plan.dims, static_cast<std::uint32_t>(c->levels),
+                                                         c->codec == 2 ? Codec::lz : Codec::csr);
                 auto decoded = decode_patch(enc);
                 std::size_t nnz = 0;
                 for (const auto& d : decoded)

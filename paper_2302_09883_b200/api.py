@@ -381,6 +381,7 @@ class RunConfig:
     store_budget_bytes: int = 0
     tile_rows: int = 1
     metrics_path: str = ""       # RunConfig::metrics_path: CSV of the rows (pipeline.hpp:162-166)
+    codec: str = "csr"           # RunConfig::codec: "csr" or "lz" (codec.hpp:250)
 
     def to_c(self) -> abi.RunConfigC:
         c = abi.RunConfigC()
@@ -391,7 +392,7 @@ class RunConfig:
         c.cfl, c.t_end, c.alpha, c.beta = self.cfl, self.t_end, self.alpha, self.beta
         c.gravity, c.domain_length = self.gravity, self.domain_length
         c.threshold_mode = abi.threshold_mode(self.spec.mode)
-        c.codec = 1
+        c.codec = {"csr": 1, "lz": 2}[self.codec]
         c.c, c.threshold_alpha = self.spec.c, self.spec.alpha
         c.no_compression = int(self.no_compression)
         c.strict = int(self.strict)

@@ -21,6 +21,7 @@ struct KernelSet {
     size_t scratch_doubles;  // per CTA
     bool edges3;             // D2Q9 edge lines hold only the 3 crossing populations
     bool decode_l2;          // decode with decode_out == nullptr runs the transport l2 pass
+    void (*main_lz)(StepArgs) = nullptr;  // MODE_STEP_LZ (Codec::lz metrics); null if unsupported
 };
 
 // Each returns false when (n, levels) has no instantiation.

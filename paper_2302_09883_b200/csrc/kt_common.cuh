@@ -8,7 +8,7 @@
 namespace wg {
 
 inline void kt_set_smem(const KernelSet& k) {
-    for (auto f : {k.main, k.decode, k.init})
+    for (auto f : {k.main, k.decode, k.init, k.main_lz})
         if (f) WG_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k.smem));
 }
 

@@ -15,7 +15,8 @@ struct FullL {
     static KernelSet make() {
         using Lay = LbmLayout<N>;
         return KernelSet{k_lbm_step<N, L, MODE_STEP>, k_lbm_step<N, L, MODE_DECODE>, k_lbm_step<N, L, MODE_INIT>,
-                         1, Lay::NT, Lay::smem_bytes(), true, Lay::scratch_doubles(), true, false};
+                         1, Lay::NT, Lay::smem_bytes(), true, Lay::scratch_doubles(), true, false,
+                         k_lbm_step<N, L, MODE_STEP_LZ>};
     }
 };
 

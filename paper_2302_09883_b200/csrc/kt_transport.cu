@@ -25,7 +25,7 @@ struct FullT {
         static KernelSet make() {
             using Lay = Layout<N, P>;
             return KernelSet{k_patch_step<N, L, P, MODE_STEP>, k_patch_step<N, L, P, MODE_DECODE>, nullptr, P,
-                             Lay::NT, Lay::smem_bytes(), false, 0, false, true};
+                             Lay::NT, Lay::smem_bytes(), false, 0, false, true, k_patch_step<N, L, P, MODE_STEP_LZ>};
         }
     };
 };

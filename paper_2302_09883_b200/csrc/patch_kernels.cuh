@@ -179,7 +179,10 @@ __global__ void __launch_bounds__(Layout<N, P>::NT, WG_MIN_BLOCKS(N))
                 __syncthreads();
                 WG_PHASE_MARK(4);
                 // ---- ROW phase: forward DWT along dim 1, threshold, count --
-                if (valid) fwd_row_threshold<N, L>(T, li, a.thr, v, nz, zr);
+                if (valid)
+                    fwd_row_threshold<N, L>(T, li, a.thr, v, nz, zr,
+                                            MODE == MODE_STEP_LZ ? a.lz_dense + (size_t)p * N * N + (size_t)li * N
+                                                                 : nullptr);
                 cta_inclusive_scan<NT>(((unsigned long long)zr << 32) | nz, inc);
                 WG_PHASE_MARK(5);
             } else {

@@ -98,6 +98,7 @@ struct StepArgs {
     unsigned long long* swe_steps;   // steps completed on the device
     double t_end, cfl_dx, dx, gravity;
     unsigned long long* phase;       // WG_PHASE_TIMING builds: per-phase cycle sums [32]
+    double* lz_dense;                // Codec::lz: thresholded coefficient arrays [npatch*m][n*n] (else null)
     // transport l2_error diagnostic every step (pipeline.hpp:275-276)
     int l2_on;
     uint64_t l2_nx;
@@ -105,7 +106,9 @@ struct StepArgs {
     double thr[(kMaxLevels + 1) * (kMaxLevels + 1)];     // T[band_i][band_j]
 };
 
-enum { MODE_STEP = 0, MODE_INIT = 1, MODE_DECODE = 2 };
+// MODE_STEP_LZ: a step that also stages the thresholded coefficient arrays
+// for the Codec::lz sizes (a separate instantiation: no cost to MODE_STEP)
+enum { MODE_STEP = 0, MODE_INIT = 1, MODE_DECODE = 2, MODE_STEP_LZ = 3 };
 
 struct PatchPos {
     int ar;       // local patch row
@@ -237,9 +240,13 @@ __device__ __forceinline__ void fwd_col_to_tile(double* T, int j, double (&v)[N]
 // threshold (threshold.hpp:51-86: samples untouched, strict <, v != 0),
 // count kept and zeroed coefficients.  -0.0 becomes +0.0 like the CSR
 // round trip of pipeline.hpp:234-237.
+// dense_row (Codec::lz, else null): row i of the block's coefficient array
+// as apply_threshold leaves it (threshold.hpp:78-82: a killed value becomes
+// +0.0, every other value — -0.0 included — is kept), for the LZ coder.
 template <int N, int L>
 __device__ __forceinline__ void fwd_row_threshold(const double* T, int i, const double* thr,
-                                                  double (&v)[N], unsigned& nz, unsigned& zr) {
+                                                  double (&v)[N], unsigned& nz, unsigned& zr,
+                                                  double* dense_row = nullptr) {
     constexpr int TP = N + 2;
 #pragma unroll
     for (int jj = 0; jj < N; ++jj) v[jj] = T[(i + 1) * TP + jj + 1];
@@ -250,6 +257,13 @@ __device__ __forceinline__ void fwd_row_threshold(const double* T, int i, const 
     for (int bj = 0; bj <= L; ++bj) trow[bj] = thr[bi * (L + 1) + bj];
     nz = 0;
     zr = 0;
+    if (dense_row) {  // Codec::lz only: one branch per row on the default path
+#pragma unroll
+        for (int r = 0; r < N; ++r) {
+            const double x = v[r];
+            dense_row[corner_pos<N, L>(r)] = (x != 0.0 && fabs(x) < trow[band_of_r<N, L>(r)]) ? 0.0 : x;
+        }
+    }
 #pragma unroll
     for (int r = 0; r < N; ++r) {
         const double x = v[r];

@@ -134,6 +134,101 @@ __global__ void k_swe_vmax(const double* grid, uint32_t N, uint64_t npatch, doub
     if ((threadIdx.x & 31) == 0) atomicMax(vmax_bits, (unsigned long long)__double_as_longlong(v));
 }
 
+// ---- Codec::lz metrics (codec.hpp:81-244): the byte size of lz_encode of
+// every block's coefficient array, computed exactly like lz_encode_chunk's
+// greedy parse (13-bit hash table, 4-byte minimum match, offsets < 65536,
+// the match extension compares 8 bytes at a time but stops at the same
+// first differing byte) without materialising the stream. ------------------
+__device__ __forceinline__ uint64_t lz_load8(const unsigned char* p) {
+    const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+    const uint64_t* w = reinterpret_cast<const uint64_t*>(a & ~uintptr_t(7));
+    const unsigned sh = (unsigned)(a & 7) * 8;
+    const uint64_t lo = __ldg(w);
+    return sh ? (lo >> sh) | (__ldg(w + 1) << (64 - sh)) : lo;  // the buffer has 8 B of tail padding
+}
+
+// One warp per chunk: the parse itself is sequential (every lane follows it
+// in lock-step), the table is cleared and every match is extended 256 bytes
+// at a time by the 32 lanes (ballot: the first differing byte).
+__device__ uint32_t lz_chunk_size_warp(const unsigned char* in, uint32_t n, int* table) {
+    const int lane = threadIdx.x & 31;
+    for (int k = lane; k < 8192; k += 32) table[k] = -1;
+    __syncwarp();
+    uint32_t anchor = 0, pos = 0, out = 0;
+    auto ext = [](uint32_t len) { return len / 255 + 1; };  // lz_put_length bytes
+    while (n >= 4 && pos + 4 <= n) {
+        const uint32_t v = (uint32_t)lz_load8(in + pos);
+        const uint32_t h = (v * 2654435761u) >> 19;
+        const int cand = table[h];
+        __syncwarp();
+        if (lane == 0) table[h] = (int)pos;
+        __syncwarp();
+        if (cand >= 0 && pos - (uint32_t)cand <= 65535u && (uint32_t)lz_load8(in + cand) == v) {
+            uint32_t len = 4;
+            for (;;) {
+                if (pos + len + 256 <= n) {
+                    const uint64_t d = lz_load8(in + cand + len + 8 * lane) ^ lz_load8(in + pos + len + 8 * lane);
+                    const unsigned m = __ballot_sync(0xffffffffu, d != 0);
+                    if (!m) {
+                        len += 256;
+                        continue;
+                    }
+                    const int f = __ffs(m) - 1;
+                    const uint64_t df = __shfl_sync(0xffffffffu, d, f);
+                    len += 8 * f + (uint32_t)(__ffsll((long long)df) - 1) / 8;
+                    break;
+                }
+                while (pos + len < n && in[cand + len] == in[pos + len]) ++len;  // the tail (< 256 B)
+                break;
+            }
+            const uint32_t lit = pos - anchor, ml = len - 4;
+            out += 1 + (lit >= 15 ? ext(lit - 15) : 0) + lit + 2 + (ml >= 15 ? ext(ml - 15) : 0);
+            pos += len;
+            anchor = pos;
+            continue;
+        }
+        ++pos;
+    }
+    if (anchor < n) {  // the terminal literal-only sequence
+        const uint32_t lit = n - anchor;
+        out += 1 + (lit >= 15 ? ext(lit - 15) : 0) + lit;
+    }
+    return out;
+}
+
+// sizes[b] = LzStream::byte_size of block b (chunks of 64 KiB: 8 + payload
+// each); one warp per block, a hash table per warp.
+__global__ void k_lz_sizes(const double* dense, uint64_t nblocks, uint32_t nn, int* tables, uint32_t* sizes) {
+    const uint64_t wid = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) / 32;
+    const uint64_t nw = (uint64_t)gridDim.x * blockDim.x / 32;
+    int* table = tables + wid * 8192;
+    for (uint64_t b = wid; b < nblocks; b += nw) {
+        const unsigned char* in = reinterpret_cast<const unsigned char*>(dense + b * nn);
+        const uint32_t bytes = nn * 8;
+        uint32_t total = 0;
+        for (uint32_t off = 0; off < bytes; off += 65536u) {
+            const uint32_t len = min(65536u, bytes - off);
+            total += 8 + lz_chunk_size_warp(in + off, len, table);
+        }
+        if ((threadIdx.x & 31) == 0) sizes[b] = total;
+    }
+}
+
+// The step's row: compressed_bytes = sum of the LZ sizes (fixed order), ratio.
+__global__ void k_lz_finalize(const uint32_t* sizes, uint64_t nblocks, wg_metrics_row* row) {
+    __shared__ unsigned long long part[256];
+    unsigned long long s = 0;
+    for (uint64_t b = threadIdx.x; b < nblocks; b += blockDim.x) s += sizes[b];
+    part[threadIdx.x] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long tot = 0;
+        for (int k = 0; k < 256; ++k) tot += part[k];
+        row->compressed_bytes = tot;
+        row->ratio = tot > 0 ? (double)row->dense_bytes / (double)tot : 1.0;  // pipeline.hpp:270-272
+    }
+}
+
 __global__ void k_set_u64(unsigned long long* p, unsigned long long v) { *p = v; }
 
 __global__ void k_swe_clock_reset(double* td, unsigned long long* vmax_bits, unsigned long long* steps) {
@@ -177,6 +272,11 @@ struct Session {
     // SWE device clock: [t, last dt] (f64), vmax bits [2], steps done (u64)
     unsigned long long* swe = nullptr;
     unsigned long long* phase = nullptr;  // WG_PHASE_TIMING builds only
+    // Codec::lz metrics staging
+    double* lz_dense = nullptr;
+    uint32_t* lz_sizes = nullptr;
+    int* lz_tables = nullptr;
+    uint32_t lz_threads = 0;
     // pinned-host upload pipeline (created on first use)
     double* stage = nullptr;
     cudaStream_t copy_stream = nullptr;
@@ -248,6 +348,12 @@ struct Session {
         }
         cudaFree(stage);
         stage = nullptr;
+        cudaFree(lz_dense);
+        cudaFree(lz_sizes);
+        cudaFree(lz_tables);
+        lz_dense = nullptr;
+        lz_sizes = nullptr;
+        lz_tables = nullptr;
         partials = nullptr;
         done = nullptr;
         bump = nullptr;
@@ -279,7 +385,9 @@ struct Session {
 
     void create(const wg_run_config& c, const wg_shard* sh, void* strm) {
         cfg = c;
-        if (cfg.codec != 1) raise(WG_INVALID_ARGUMENT, "only Codec::csr is on the hot path");
+        if (cfg.codec != 1 && cfg.codec != 2) raise(WG_INVALID_ARGUMENT, "unknown codec");
+        if (cfg.codec == 2 && cfg.scheme == WG_SCHEME_SWE)
+            raise(WG_INVALID_ARGUMENT, "Codec::lz metrics: transport and D2Q9 sessions only");
         if (cfg.scheme != WG_SCHEME_LBM_D2Q9) sim_validate(cfg);
         if (cfg.scheme == WG_SCHEME_LBM_D2Q9 && cfg.lbm_tau <= 0.5)
             raise(WG_INVALID_ARGUMENT, "LBM: tau must exceed 1/2");
@@ -369,6 +477,16 @@ struct Session {
         WG_CUDA(cudaMemsetAsync(phase, 0, 32 * sizeof(unsigned long long), stream));
 #endif
         grow_rows(1024);
+        if (cfg.codec == 2 && !cfg.no_compression) {  // Codec::lz metrics (the store itself stays CSR)
+            if (!ks.main_lz) raise(WG_INVALID_ARGUMENT, "Codec::lz metrics: not available for this kernel variant");
+            const uint64_t nb = (uint64_t)sg.npatch * sg.m;
+            if (nb * N * N * 8 > (8ull << 30))
+                raise(WG_INVALID_ARGUMENT, "Codec::lz metrics: grid too large for the coefficient staging");
+            lz_dense = dalloc<double>(nb * N * N + 1);  // + 8 B tail padding for the word loads
+            lz_sizes = dalloc<uint32_t>(nb);
+            lz_threads = (uint32_t)((std::min<uint64_t>(nb, 4096) + 1) / 2 * 2);  // warps, 2 per CTA of 64
+            lz_tables = dalloc<int>((uint64_t)lz_threads * 8192);
+        }
         // the pinned-host upload pipeline (allocated here, outside any timed upload)
         stage = dalloc<double>(2 * (uint64_t)stage_chunk() * sg.m * geo.tcount);
         WG_CUDA(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking));
@@ -521,6 +639,7 @@ struct Session {
         a.thr_any = (cfg.c > 0.0 && levels > 0) ? 1 : 0;
         a.dense_bytes = (uint64_t)sg.npatch * 8ull * N * N * sg.m;
         a.phase = phase;
+        a.lz_dense = lz_dense;
         if (is_swe()) {
             a.swe_td = swe_td();
             a.swe_vmax = swe + 2;
@@ -558,11 +677,18 @@ struct Session {
             e1 = take_event();
             WG_CUDA(cudaEventRecord(e0, stream));
         }
-        ks.main<<<grid, ks.threads, ks.smem, stream>>>(a);
+        (lz_dense ? ks.main_lz : ks.main)<<<grid, ks.threads, ks.smem, stream>>>(a);
         WG_LAUNCH_CHECK("fused step");
         if (profiling) {
             WG_CUDA(cudaEventRecord(e1, stream));
             ev_main.emplace_back(e0, e1);
+        }
+        if (lz_dense) {  // Codec::lz: the step's compressed_bytes/ratio from the LZ stream sizes
+            k_lz_sizes<<<lz_threads / 2, 64, 0, stream>>>(lz_dense, (uint64_t)sg.npatch * sg.m, N * N,
+                                                                  lz_tables, lz_sizes);
+            WG_LAUNCH_CHECK("lz sizes");
+            k_lz_finalize<<<1, 256, 0, stream>>>(lz_sizes, (uint64_t)sg.npatch * sg.m, a.row_out);
+            WG_LAUNCH_CHECK("lz finalize");
         }
         if (ks.decode_l2 && cfg.compute_l2 && geo.tiles == 1) {
             // l2_error(assemble(grid, 0), exact_transport(t), cfg) of the new
