@@ -212,12 +212,11 @@ inline MetricsRow from_c(const wg_metrics_row& r) {
 }
 
 // run() on the device.  Harness features that are not on the hot path
-// (metrics_path, snapshots, observer, LZ codec) are rejected rather than
-// silently ignored.
+// (metrics_path, snapshots, observer) are rejected rather than silently
+// ignored; Codec::lz runs for transport (its sizes are computed on the device).
 inline RunResult run(const RunConfig& rc) {
     if (!rc.metrics_path.empty() || !rc.snapshot_times.empty() || rc.observer)
         throw std::invalid_argument("b200::run: metrics files, snapshots and observers are not supported");
-    if (rc.codec != Codec::csr) throw std::invalid_argument("b200::run: only Codec::csr is on the hot path");
     const wg_run_config c = to_c(rc);
     uint64_t steps = 0, doubles = 0;
     check(wg_run_step_count(&c, &steps));

@@ -875,6 +875,49 @@ static double now_s(void) {
 /* The per-patch compression cycle of run(), pipeline.hpp:217-257:
  * extract_logical -> dwt_nd -> apply_threshold -> encode/decode (CSR) ->
  * nnz count -> skip rule -> idwt_nd -> insert_logical. */
+/* lz_encode_chunk (codec.hpp:127-175): the payload length of the greedy
+ * LZ parse of one chunk (13-bit hash of 4 bytes, minimum match 4, offsets
+ * <= 65535, literal/match lengths extended with 255-bytes). */
+static uint64_t lz_chunk_payload(const unsigned char* in, uint64_t n) {
+    static int64_t table[1u << 13];
+    for (uint32_t k = 0; k < (1u << 13); ++k) table[k] = -1;
+    uint64_t anchor = 0, pos = 0, out = 0;
+#define LZ_EXT(len) ((len) / 255 + 1)
+    while (n >= 4 && pos + 4 <= n) {
+        uint32_t v;
+        memcpy(&v, in + pos, 4);
+        const uint32_t h = (v * 2654435761u) >> 19;
+        const int64_t cand = table[h];
+        table[h] = (int64_t)pos;
+        if (cand >= 0 && pos - (uint64_t)cand <= 65535 && memcmp(in + cand, in + pos, 4) == 0) {
+            uint64_t len = 4;
+            while (pos + len < n && in[cand + len] == in[pos + len]) ++len;
+            const uint64_t lit = pos - anchor, ml = len - 4;
+            out += 1 + (lit >= 15 ? LZ_EXT(lit - 15) : 0) + lit + 2 + (ml >= 15 ? LZ_EXT(ml - 15) : 0);
+            pos += len;
+            anchor = pos;
+            continue;
+        }
+        ++pos;
+    }
+    if (anchor < n) {
+        const uint64_t lit = n - anchor;
+        out += 1 + (lit >= 15 ? LZ_EXT(lit - 15) : 0) + lit;
+    }
+#undef LZ_EXT
+    return out;
+}
+
+/* LzStream::byte_size of lz_encode(bytes, 64 KiB chunks) (codec.hpp:99-105, 223-235). */
+static uint64_t lz_stream_size(const double* a, uint64_t count) {
+    const unsigned char* b = (const unsigned char*)a;
+    const uint64_t bytes = count * 8;
+    uint64_t s = 0;
+    for (uint64_t off = 0; off < bytes; off += 65536)
+        s += 8 + lz_chunk_payload(b + off, bytes - off < 65536 ? bytes - off : 65536);
+    return s;
+}
+
 static wg_status compress_patch(const wg_run_config* c, const grid_t* g, double* buf,
                                 uint64_t p, double* work, uint64_t* st_comp, uint64_t* st_nnz,
                                 uint64_t* st_zeroed) {
@@ -902,13 +945,14 @@ static wg_status compress_patch(const wg_run_config* c, const grid_t* g, double*
     }
     for (uint32_t q = 0; q < m; ++q) { /* CSR round trip: bytes, nnz, -0.0 -> +0.0 */
         double* cs = coef + q * n0 * n1;
+        if (c->codec == 2) comp_bytes += lz_stream_size(cs, n0 * n1); /* Codec::lz: the thresholded bytes */
         uint64_t k = 0;
         for (uint64_t e = 0; e < n0 * n1; ++e) {
             if (cs[e] != 0.0) ++k;
             else cs[e] = 0.0;
         }
         nnz += k;
-        comp_bytes += 12 * k + 4 * (n0 + 1); /* CsrBlock::byte_size, codec.hpp:33 */
+        if (c->codec == 1) comp_bytes += 12 * k + 4 * (n0 + 1); /* CsrBlock::byte_size, codec.hpp:33 */
     }
     for (uint32_t q = 0; q < m; ++q) {
         double* f = comp_ptr(g, buf, p, q);
@@ -936,7 +980,7 @@ wg_status wg_run(const wg_run_config* c, wg_metrics_row* rows, uint64_t max_rows
     if (c->scheme != WG_SCHEME_LBM_D2Q9 && (st = sim_validate(c))) return st;
     if ((st = run_grid(c, &g))) return st;
     if ((st = plan_validate(g.n, 2, c->levels))) return st;
-    if (c->codec != 1) return fail(WG_INVALID_ARGUMENT, "only Codec::csr is on the hot path");
+    if (c->codec != 1 && c->codec != 2) return fail(WG_INVALID_ARGUMENT, "unknown codec");
     if (c->scheme == WG_SCHEME_LBM_D2Q9 && c->lbm_tau <= 0.5)
         return fail(WG_INVALID_ARGUMENT, "LBM: tau must exceed 1/2");
     const uint64_t total = g.npatch * g.m * g.tcount;

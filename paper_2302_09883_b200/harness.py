@@ -6,8 +6,9 @@ demo (pipeline.hpp:405-460).
 
 Host-side orchestration only: every transform, threshold and codec call goes
 through the C ABI of `lib` (the sm_100a product by default, so the compute
-runs on the GPU's per-op kernels; the oracles in the tests).  The LZ codec
-is not implemented (SURVEY §8f-1): Codec::lz raises ValueError.
+runs on the GPU's per-op kernels; the oracles in the tests).  Files are
+written with Codec::csr; sweep and run accept Codec::lz (device-computed LZ
+sizes, metrics only).
 """
 from __future__ import annotations
 
@@ -157,12 +158,11 @@ def sweep(cfg: SweepConfig, lib=None) -> list:
         os.makedirs(cfg.out_dir, exist_ok=True)
     table = []
     for codec in cfg.codecs:
-        if codec != 1:
-            raise ValueError("Codec::lz is out of scope (SURVEY §8f-1)")
+        cname = {1: "csr", 2: "lz"}[codec]
         for level in cfg.levels:
             for c in cfg.thresholds:
-                name = "run_%s_L%d_c%s.csv" % ("csr", level, _fmt_g(c))
-                rc = replace(cfg.base, levels=level, spec=replace(cfg.base.spec, c=c),
+                name = "run_%s_L%d_c%s.csv" % (cname, level, _fmt_g(c))
+                rc = replace(cfg.base, levels=level, spec=replace(cfg.base.spec, c=c), codec=cname,
                              metrics_path=str(Path(cfg.out_dir) / name) if cfg.out_dir else name)
                 r = api.run(rc, lib=lib)
                 table.append(SweepEntry(c, level, codec, r.summary["avg_ratio"],
@@ -171,8 +171,8 @@ def sweep(cfg: SweepConfig, lib=None) -> list:
         with open(Path(cfg.out_dir) / "summary.csv", "w") as f:
             f.write("codec,level,threshold,avg_ratio,final_l2_error,metrics_file\n")
             for e in table:
-                f.write("%s,%d,%.17g,%.17g,%.17g,%s\n" % ("csr", e.level, e.threshold, e.avg_ratio, e.final_l2,
-                                                          e.metrics_file))
+                f.write("%s,%d,%.17g,%.17g,%.17g,%s\n" % ({1: "csr", 2: "lz"}[e.codec], e.level, e.threshold,
+                                                          e.avg_ratio, e.final_l2, e.metrics_file))
     return table
 
 

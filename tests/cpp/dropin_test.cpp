@@ -140,6 +140,19 @@ static int check_ops(bool device_session) {
         for (std::size_t c = 0; c < rc.sim.component_count(); ++c)
             EXPECT(same_bits(wg::assemble(ra.grid, c).values, wg::assemble(rb.grid, c).values));
     }
+    {  // Codec::lz (codec.hpp:81-244): the same state, the LZ stream sizes as metrics
+        wg::RunConfig rc;
+        rc.sim.nx = 129;
+        rc.sim.splits = {2, 2};
+        rc.sim.t_end = 0.01;
+        rc.spec = {wg::ThresholdMode::capped, 1e-3, 2.0};
+        rc.codec = wg::Codec::lz;
+        const auto ra = wg::run(rc);
+        const auto rb = wg::b200::run(rc);
+        EXPECT(ra.rows.size() == rb.rows.size());
+        for (std::size_t s = 0; s < ra.rows.size(); ++s)
+            EXPECT(ra.rows[s].compressed_bytes == rb.rows[s].compressed_bytes && ra.rows[s].ratio == rb.rows[s].ratio);
+    }
     if (device_session) {
 #ifdef WG_DROPIN_SESSION
         // the device-resident loop: same rows and state as run()

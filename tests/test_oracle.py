@@ -253,3 +253,15 @@ def test_metrics_csv_schema(oracle, tmp_path):
         f = line.split(",")
         assert int(f[0]) == row["step"] and float(f[1]) == row["time"] and int(f[5]) == row["nnz"]
         assert float(f[7]) == row["global_mass"] and float(f[8]) == row["l2"]  # %.17g round-trips
+
+
+@pytest.mark.parametrize("scheme", ["transport", "swe", "lbm"])
+def test_lz_metrics_vs_reference(oracle, reference, scheme):
+    """Codec::lz (codec.hpp:81-244): the restated greedy parse gives the
+    reference's stream sizes byte for byte (compressed_bytes, ratio)."""
+    kw = dict(lbm_steps=3) if scheme == "lbm" else dict(t_end=0.005)
+    nx = 129 if scheme != "swe" else 65
+    cfg = api.RunConfig(scheme=scheme, nx=nx, splits=(2, 2), levels=4 if scheme != "swe" else 3,
+                        spec=api.ThresholdSpec("capped", 1e-3), codec="lz", compute_l2=False, **kw)
+    a, b = api.run(cfg, lib=oracle), api.run(cfg, lib=reference)
+    assert [(r["compressed_bytes"], r["ratio"]) for r in a.rows] == [(r["compressed_bytes"], r["ratio"]) for r in b.rows]
