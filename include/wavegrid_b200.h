@@ -157,7 +157,7 @@ typedef struct wg_run_config { /* RunConfig + SimConfig, pipeline.hpp:23-38, sol
                                  the store stays CSR — both codecs are
                                  lossless — and every step's compressed_bytes
                                  and ratio are the exact lz_encode sizes,
-                                 codec.hpp:81-244; transport and D2Q9)       */
+                                 codec.hpp:81-244)                           */
     double c, threshold_alpha;/* ThresholdSpec::c, ::alpha                    */
     int32_t no_compression;
     int32_t strict;

@@ -213,7 +213,7 @@ inline MetricsRow from_c(const wg_metrics_row& r) {
 
 // run() on the device.  Harness features that are not on the hot path
 // (metrics_path, snapshots, observer) are rejected rather than silently
-// ignored; Codec::lz runs for transport (its sizes are computed on the device).
+// ignored; Codec::lz runs too (its stream sizes are computed on the device).
 inline RunResult run(const RunConfig& rc) {
     if (!rc.metrics_path.empty() || !rc.snapshot_times.empty() || rc.observer)
         throw std::invalid_argument("b200::run: metrics files, snapshots and observers are not supported");

@@ -9,7 +9,8 @@ struct SweK65 {
     static KernelSet make() {
         using Lay = SweLayout<N>;
         return KernelSet{k_swe_step<N, L, MODE_STEP>, k_swe_step<N, L, MODE_DECODE>, nullptr, 1, Lay::NT,
-                         Lay::smem_bytes(), true, Lay::scratch_doubles(), false, false};
+                         Lay::smem_bytes(), true, Lay::scratch_doubles(), false, false,
+                         k_swe_step<N, L, MODE_STEP_LZ>};
     }
 };
 

@@ -215,6 +215,28 @@ __global__ void k_lz_sizes(const double* dense, uint64_t nblocks, uint32_t nn, i
 }
 
 // The step's row: compressed_bytes = sum of the LZ sizes (fixed order), ratio.
+// SWE (device clock): only a live launch advanced the step counter; its row
+// is rows_at[k - 1] (rows_at = the row buffer shifted by the session's row0)
+// and `done` remembers the last row finalized, so a no-op launch changes nothing.
+__global__ void k_lz_finalize_swe(const uint32_t* sizes, uint64_t nblocks, wg_metrics_row* rows_at,
+                                  const unsigned long long* steps, unsigned long long* done) {
+    const unsigned long long k = *steps;
+    if (k <= *done) return;  // uniform: the launch was a no-op
+    __shared__ unsigned long long part[256];
+    unsigned long long s = 0;
+    for (uint64_t b = threadIdx.x; b < nblocks; b += blockDim.x) s += sizes[b];
+    part[threadIdx.x] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long tot = 0;
+        for (int i = 0; i < 256; ++i) tot += part[i];
+        wg_metrics_row* row = rows_at + (k - 1);
+        row->compressed_bytes = tot;
+        row->ratio = tot > 0 ? (double)row->dense_bytes / (double)tot : 1.0;
+        *done = k;
+    }
+}
+
 __global__ void k_lz_finalize(const uint32_t* sizes, uint64_t nblocks, wg_metrics_row* row) {
     __shared__ unsigned long long part[256];
     unsigned long long s = 0;
@@ -275,6 +297,7 @@ struct Session {
     // Codec::lz metrics staging
     double* lz_dense = nullptr;
     uint32_t* lz_sizes = nullptr;
+    unsigned long long* lz_done = nullptr;  // SWE: the last row given its LZ sizes
     int* lz_tables = nullptr;
     uint32_t lz_threads = 0;
     // pinned-host upload pipeline (created on first use)
@@ -350,6 +373,8 @@ struct Session {
         stage = nullptr;
         cudaFree(lz_dense);
         cudaFree(lz_sizes);
+        cudaFree(lz_done);
+        lz_done = nullptr;
         cudaFree(lz_tables);
         lz_dense = nullptr;
         lz_sizes = nullptr;
@@ -386,8 +411,7 @@ struct Session {
     void create(const wg_run_config& c, const wg_shard* sh, void* strm) {
         cfg = c;
         if (cfg.codec != 1 && cfg.codec != 2) raise(WG_INVALID_ARGUMENT, "unknown codec");
-        if (cfg.codec == 2 && cfg.scheme == WG_SCHEME_SWE)
-            raise(WG_INVALID_ARGUMENT, "Codec::lz metrics: transport and D2Q9 sessions only");
+
         if (cfg.scheme != WG_SCHEME_LBM_D2Q9) sim_validate(cfg);
         if (cfg.scheme == WG_SCHEME_LBM_D2Q9 && cfg.lbm_tau <= 0.5)
             raise(WG_INVALID_ARGUMENT, "LBM: tau must exceed 1/2");
@@ -484,6 +508,8 @@ struct Session {
                 raise(WG_INVALID_ARGUMENT, "Codec::lz metrics: grid too large for the coefficient staging");
             lz_dense = dalloc<double>(nb * N * N + 1);  // + 8 B tail padding for the word loads
             lz_sizes = dalloc<uint32_t>(nb);
+            lz_done = dalloc<unsigned long long>(1);
+            WG_CUDA(cudaMemsetAsync(lz_done, 0, sizeof(unsigned long long), stream));
             lz_threads = (uint32_t)((std::min<uint64_t>(nb, 4096) + 1) / 2 * 2);  // warps, 2 per CTA of 64
             lz_tables = dalloc<int>((uint64_t)lz_threads * 8192);
         }
@@ -567,6 +593,7 @@ struct Session {
             k_swe_clock_reset<<<1, 1, 0, stream>>>(swe_td(), swe + 2, swe + 4);
             WG_LAUNCH_CHECK("swe clock");
         }
+        if (lz_done) k_set_u64<<<1, 1, 0, stream>>>(lz_done, 0ull);
         step = 0;
         launched = 0;
         row0 = 0;
@@ -723,8 +750,15 @@ struct Session {
             e1 = take_event();
             WG_CUDA(cudaEventRecord(e0, stream));
         }
-        ks.main<<<grid, ks.threads, ks.smem, stream>>>(a);
+        (lz_dense ? ks.main_lz : ks.main)<<<grid, ks.threads, ks.smem, stream>>>(a);
         WG_LAUNCH_CHECK("fused swe step");
+        if (lz_dense) {
+            const uint64_t nb = (uint64_t)sg.npatch * sg.m;
+            k_lz_sizes<<<lz_threads / 2, 64, 0, stream>>>(lz_dense, nb, N * N, lz_tables, lz_sizes);
+            WG_LAUNCH_CHECK("lz sizes");
+            k_lz_finalize_swe<<<1, 256, 0, stream>>>(lz_sizes, nb, rows - row0, swe + 4, lz_done);
+            WG_LAUNCH_CHECK("lz finalize");
+        }
         if (profiling) {
             WG_CUDA(cudaEventRecord(e1, stream));
             ev_main.emplace_back(e0, e1);
@@ -1052,6 +1086,7 @@ struct Session {
             c[2 + (h.step & 1)] = h.swe_vmax_bits;
             WG_CUDA(cudaMemcpyAsync(swe, c, sizeof c, cudaMemcpyHostToDevice, stream));
         }
+        if (lz_done) k_set_u64<<<1, 1, 0, stream>>>(lz_done, h.step);
         sync();
     }
 

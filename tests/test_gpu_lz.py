@@ -21,6 +21,8 @@ pytestmark = pytest.mark.gpu
      ("transport", 129, (4, 4), 3, "constant", 1e-2, 5),
      ("transport", 65, (8, 8), 2, "accumulation", 5e-2, 4),
      ("transport", 129, (2, 2), 4, "capped", 0.0, 3),   # nothing zeroed: skip rule, raw patches
+     ("swe", 65, (2, 2), 3, "constant", 5e-4, 8),      # device clock: rows of live steps only
+     ("swe", 129, (4, 4), 4, "constant", 1e-3, 5),
      ("lbm", 129, (2, 2), 4, "capped", 1e-3, 4),
      ("lbm", 129, (4, 4), 5, "capped", 1e-5, 3)],
 )
@@ -28,6 +30,9 @@ def test_lz_metrics_match_reference(product, reference, scheme, nx, splits, leve
     if scheme == "lbm":
         cfg = api.RunConfig(scheme="lbm", nx=nx, splits=splits, levels=levels, lbm_steps=steps,
                             spec=api.ThresholdSpec(mode, c), codec="lz")
+    elif scheme == "swe":
+        cfg = api.RunConfig(scheme="swe", nx=nx, splits=splits, levels=levels, spec=api.ThresholdSpec(mode, c),
+                            codec="lz", t_end=steps * 0.45 / (nx - 1) / 4.5)
     else:
         cfg = api.RunConfig(scheme="transport", nx=nx, splits=splits, levels=levels,
                             spec=api.ThresholdSpec(mode, c), codec="lz", compute_l2=False)
