@@ -156,38 +156,56 @@ __device__ uint32_t lz_chunk_size_warp(const unsigned char* in, uint32_t n, int*
     __syncwarp();
     uint32_t anchor = 0, pos = 0, out = 0;
     auto ext = [](uint32_t len) { return len / 255 + 1; };  // lz_put_length bytes
+    // 32 candidate positions per iteration, one per lane: each lane sees the
+    // table as the sequential parse would after inserting the positions of
+    // the lower lanes (the latest lower lane with the same hash, else the
+    // table), the lowest lane with a match ends the window, and only the
+    // positions up to it are inserted (latest position per hash).
     while (n >= 4 && pos + 4 <= n) {
-        const uint32_t v = (uint32_t)lz_load8(in + pos);
+        const uint32_t w = pos + lane;
+        const bool act = w + 4 <= n;
+        const uint32_t v = act ? (uint32_t)lz_load8(in + w) : 0u;
         const uint32_t h = (v * 2654435761u) >> 19;
-        const int cand = table[h];
+        const unsigned actm = __ballot_sync(0xffffffffu, act);
+        const unsigned peers = __match_any_sync(0xffffffffu, act ? h : 0xFFFFFFFFu) & actm;
+        const unsigned lower = peers & ((1u << lane) - 1u);
+        const int cand = !act ? -1 : lower ? (int)(pos + 31 - __clz(lower)) : table[h];
+        const bool hit = act && cand >= 0 && w - (uint32_t)cand <= 65535u && (uint32_t)lz_load8(in + cand) == v;
+        const unsigned hits = __ballot_sync(0xffffffffu, hit);
+        const int first = hits ? __ffs(hits) - 1 : 31;
+        const unsigned upto = (first == 31) ? actm : (actm & ((2u << first) - 1u));
+        // insert the processed positions: per hash the latest one wins
+        const unsigned later = peers & upto & ~((2u << lane) - 1u);
         __syncwarp();
-        if (lane == 0) table[h] = (int)pos;
+        if (((upto >> lane) & 1u) && !later) table[h] = (int)w;
         __syncwarp();
-        if (cand >= 0 && pos - (uint32_t)cand <= 65535u && (uint32_t)lz_load8(in + cand) == v) {
-            uint32_t len = 4;
-            for (;;) {
-                if (pos + len + 256 <= n) {
-                    const uint64_t d = lz_load8(in + cand + len + 8 * lane) ^ lz_load8(in + pos + len + 8 * lane);
-                    const unsigned m = __ballot_sync(0xffffffffu, d != 0);
-                    if (!m) {
-                        len += 256;
-                        continue;
-                    }
-                    const int f = __ffs(m) - 1;
-                    const uint64_t df = __shfl_sync(0xffffffffu, d, f);
-                    len += 8 * f + (uint32_t)(__ffsll((long long)df) - 1) / 8;
-                    break;
-                }
-                while (pos + len < n && in[cand + len] == in[pos + len]) ++len;  // the tail (< 256 B)
-                break;
-            }
-            const uint32_t lit = pos - anchor, ml = len - 4;
-            out += 1 + (lit >= 15 ? ext(lit - 15) : 0) + lit + 2 + (ml >= 15 ? ext(ml - 15) : 0);
-            pos += len;
-            anchor = pos;
+        if (!hits) {
+            pos += __popc(actm);  // all literals
             continue;
         }
-        ++pos;
+        const uint32_t mpos = pos + first;
+        const int mc = __shfl_sync(0xffffffffu, cand, first);
+        uint32_t len = 4;
+        for (;;) {
+            if (mpos + len + 256 <= n) {
+                const uint64_t d = lz_load8(in + mc + len + 8 * lane) ^ lz_load8(in + mpos + len + 8 * lane);
+                const unsigned m = __ballot_sync(0xffffffffu, d != 0);
+                if (!m) {
+                    len += 256;
+                    continue;
+                }
+                const int f = __ffs(m) - 1;
+                const uint64_t df = __shfl_sync(0xffffffffu, d, f);
+                len += 8 * f + (uint32_t)(__ffsll((long long)df) - 1) / 8;
+                break;
+            }
+            while (mpos + len < n && in[mc + len] == in[mpos + len]) ++len;  // the tail (< 256 B)
+            break;
+        }
+        const uint32_t lit = mpos - anchor, ml = len - 4;
+        out += 1 + (lit >= 15 ? ext(lit - 15) : 0) + lit + 2 + (ml >= 15 ? ext(ml - 15) : 0);
+        pos = mpos + len;
+        anchor = pos;
     }
     if (anchor < n) {  // the terminal literal-only sequence
         const uint32_t lit = n - anchor;
