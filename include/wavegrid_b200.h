@@ -311,7 +311,9 @@ wg_status wg_session_last_row(wg_session* s, wg_metrics_row* row);
 
 /* The same read enqueued on the session stream without synchronising: the
  * row lands in `row` (page-locked host memory) once the stream reaches it
- * (after wg_session_sync).  The per-step result read of a pipelined loop. */
+ * (after wg_session_sync).  The per-step result read of a pipelined loop.
+ * SWE: the row of the last launch — undefined if that launch was a no-op
+ * (t_end already reached); wg_session_metrics reports the live steps. */
 wg_status wg_session_last_row_async(wg_session* s, wg_metrics_row* row);
 
 /* Decode the current state into a host grid buffer (logical cells). */

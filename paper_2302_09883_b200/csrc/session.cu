@@ -187,6 +187,27 @@ __device__ uint32_t lz_chunk_size_warp(const unsigned char* in, uint32_t n, int*
         const int mc = __shfl_sync(0xffffffffu, cand, first);
         uint32_t len = 4;
         for (;;) {
+            if (mpos + len + 1024 <= n) {  // 1 KiB per round: 4 independent word pairs per lane in flight
+                uint64_t d[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    d[u] = lz_load8(in + mc + len + 256 * u + 8 * lane) ^ lz_load8(in + mpos + len + 256 * u + 8 * lane);
+                bool stop = false;
+#pragma unroll
+                for (int u = 0; u < 4 && !stop; ++u) {
+                    const unsigned m = __ballot_sync(0xffffffffu, d[u] != 0);
+                    if (!m) {
+                        len += 256;
+                        continue;
+                    }
+                    const int f = __ffs(m) - 1;
+                    const uint64_t df = __shfl_sync(0xffffffffu, d[u], f);
+                    len += 8 * f + (uint32_t)(__ffsll((long long)df) - 1) / 8;
+                    stop = true;
+                }
+                if (stop) break;
+                continue;
+            }
             if (mpos + len + 256 <= n) {
                 const uint64_t d = lz_load8(in + mc + len + 8 * lane) ^ lz_load8(in + mpos + len + 8 * lane);
                 const unsigned m = __ballot_sync(0xffffffffu, d != 0);
