@@ -388,7 +388,9 @@ def bench_b200(args, w: dict):
                      "step_share": main_max / tot_ms if tot_ms else None},
         "e2e": e2e,
         "compute_ceiling": compute_ceiling(lib, w, value / world),  # per GPU
-        "gpu_launches": args.steps,  # one fused kernel launch per step (k_*_step<STEP>)
+        # one fused kernel launch per step (k_*_step<STEP>); Codec::lz adds the
+        # LZ-size pass and its reduction (k_lz_sizes, k_lz_finalize)
+        "gpu_launches": args.steps * (3 if w.get("codec") == "lz" else 1),
         "clocks": clocks.summary(),
         "device_bytes": info.device_bytes,
         "device_mem_used_bytes": mem_used,
