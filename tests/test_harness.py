@@ -63,3 +63,13 @@ def test_demo_discontinuous(oracle, tmp_path):
     keep = harness.demo_discontinuous("", 0.0, lib=oracle)
     assert keep.mass_after == pytest.approx(keep.mass_before, rel=1e-12)
     assert (tmp_path / "report.txt").exists() and (tmp_path / "original.wgrd").exists()
+
+
+def test_sweep_with_both_codecs(oracle, tmp_path):
+    """sweep over Codec::csr and Codec::lz (pipeline.hpp:360-401): the LZ
+    runs report their own (smaller) byte counts, same state."""
+    base = api.RunConfig(scheme="transport", nx=33, splits=(2, 2), levels=3, t_end=0.02,
+                         spec=api.ThresholdSpec("capped", 0.01))
+    table = harness.sweep(harness.SweepConfig(base, [0.01], [3], [1, 2], str(tmp_path)), lib=oracle)
+    assert [e.codec for e in table] == [1, 2] and table[0].avg_ratio != table[1].avg_ratio
+    assert (tmp_path / "run_lz_L3_c0.01.csv").exists()
