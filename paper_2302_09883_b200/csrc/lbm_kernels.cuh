@@ -252,9 +252,9 @@ __global__ void __launch_bounds__(LbmLayout<N>::NT, WG_LBM_MIN_BLOCKS) k_lbm_ste
                 unsigned nz = 0, zr = 0;
                 if (lane_ok)
                     fwd_row_threshold<N, L>(T, li, a.thr, v, nz, zr,
-                                            MODE == MODE_STEP_LZ ? a.lz_dense + ((size_t)p * 9 + q) * NN + (size_t)li * N
-                                                                 : nullptr);
+                                            MODE == MODE_STEP_LZ ? T + (li + 1) * TP + 1 : nullptr);
                 cta_inclusive_scan<NT>(((unsigned long long)zr << 32) | nz, inc);
+                if (MODE == MODE_STEP_LZ) tiles_to_dense<N, NT>(tiles, TILE, 3, a.lz_dense + ((size_t)p * 9 + 3 * rd) * NN);
                 if (t == 0) {
                     for (int sl = 0; sl < 3; ++sl) {
                         const int qq = 3 * rd + sl;

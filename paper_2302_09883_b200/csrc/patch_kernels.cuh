@@ -181,9 +181,11 @@ __global__ void __launch_bounds__(Layout<N, P>::NT, WG_MIN_BLOCKS(N))
                 // ---- ROW phase: forward DWT along dim 1, threshold, count --
                 if (valid)
                     fwd_row_threshold<N, L>(T, li, a.thr, v, nz, zr,
-                                            MODE == MODE_STEP_LZ ? a.lz_dense + (size_t)p * N * N + (size_t)li * N
-                                                                 : nullptr);
+                                            MODE == MODE_STEP_LZ ? T + (li + 1) * TP + 1 : nullptr);
                 cta_inclusive_scan<NT>(((unsigned long long)zr << 32) | nz, inc);
+                if (MODE == MODE_STEP_LZ)
+                    tiles_to_dense<N, NT>(tiles, TILE, (int)min((uint32_t)P, g.npatch - grp * P),
+                                          a.lz_dense + (size_t)grp * P * N * N);
                 WG_PHASE_MARK(5);
             } else {
                 __syncthreads();

@@ -240,9 +240,12 @@ __device__ __forceinline__ void fwd_col_to_tile(double* T, int j, double (&v)[N]
 // threshold (threshold.hpp:51-86: samples untouched, strict <, v != 0),
 // count kept and zeroed coefficients.  -0.0 becomes +0.0 like the CSR
 // round trip of pipeline.hpp:234-237.
-// dense_row (Codec::lz, else null): row i of the block's coefficient array
-// as apply_threshold leaves it (threshold.hpp:78-82: a killed value becomes
-// +0.0, every other value — -0.0 included — is kept), for the LZ coder.
+// dense_row (Codec::lz, else null): where row i of the block's coefficient
+// array goes, in corner order, as apply_threshold leaves it
+// (threshold.hpp:78-82: a killed value becomes +0.0, every other value —
+// -0.0 included — is kept), for the LZ coder.  The kernels pass the tile's
+// own row i (read into v above, free until the reconstruction) and copy the
+// tiles out coalesced with tiles_to_dense.
 template <int N, int L>
 __device__ __forceinline__ void fwd_row_threshold(const double* T, int i, const double* thr,
                                                   double (&v)[N], unsigned& nz, unsigned& zr,
@@ -273,6 +276,18 @@ __device__ __forceinline__ void fwd_row_threshold(const double* T, int i, const 
         const bool keep = nzx && !kill;
         v[r] = keep ? x : 0.0;
         nz += keep ? 1u : 0u;
+    }
+}
+
+// Codec::lz staging: the interiors of `count` consecutive tiles (the
+// coefficient arrays fwd_row_threshold left there) to dense[count][N*N],
+// coalesced.  Between the row phase's scan barrier and the next barrier.
+template <int N, int NT>
+__device__ __forceinline__ void tiles_to_dense(const double* tiles, int tile_stride, int count, double* dense) {
+    constexpr int TP = N + 2, NN = N * N;
+    for (int k = threadIdx.x; k < count * NN; k += NT) {
+        const int s = k / NN, r = k - s * NN, i = r / N, j = r - i * N;
+        dense[k] = tiles[s * tile_stride + (i + 1) * TP + j + 1];
     }
 }
 

@@ -150,9 +150,10 @@ __device__ __forceinline__ uint64_t lz_load8(const unsigned char* p) {
 // One warp per chunk: the parse itself is sequential (every lane follows it
 // in lock-step), the table is cleared and every match is extended 256 bytes
 // at a time by the 32 lanes (ballot: the first differing byte).
-__device__ uint32_t lz_chunk_size_warp(const unsigned char* in, uint32_t n, int* table) {
+__device__ uint32_t lz_chunk_size_warp(const unsigned char* in, uint32_t n, unsigned short* table) {
     const int lane = threadIdx.x & 31;
-    for (int k = lane; k < 8192; k += 32) table[k] = -1;
+    // chunk positions are < 65536 - 3, so 16-bit entries with 0xFFFF as "empty"
+    for (int k = lane; k < 8192 / 8; k += 32) reinterpret_cast<uint4*>(table)[k] = make_uint4(~0u, ~0u, ~0u, ~0u);
     __syncwarp();
     uint32_t anchor = 0, pos = 0, out = 0;
     auto ext = [](uint32_t len) { return len / 255 + 1; };  // lz_put_length bytes
@@ -169,7 +170,8 @@ __device__ uint32_t lz_chunk_size_warp(const unsigned char* in, uint32_t n, int*
         const unsigned actm = __ballot_sync(0xffffffffu, act);
         const unsigned peers = __match_any_sync(0xffffffffu, act ? h : 0xFFFFFFFFu) & actm;
         const unsigned lower = peers & ((1u << lane) - 1u);
-        const int cand = !act ? -1 : lower ? (int)(pos + 31 - __clz(lower)) : table[h];
+        const unsigned short t = act && !lower ? table[h] : (unsigned short)0xFFFFu;
+        const int cand = !act ? -1 : lower ? (int)(pos + 31 - __clz(lower)) : (t == 0xFFFFu ? -1 : (int)t);
         const bool hit = act && cand >= 0 && w - (uint32_t)cand <= 65535u && (uint32_t)lz_load8(in + cand) == v;
         const unsigned hits = __ballot_sync(0xffffffffu, hit);
         const int first = hits ? __ffs(hits) - 1 : 31;
@@ -177,7 +179,7 @@ __device__ uint32_t lz_chunk_size_warp(const unsigned char* in, uint32_t n, int*
         // insert the processed positions: per hash the latest one wins
         const unsigned later = peers & upto & ~((2u << lane) - 1u);
         __syncwarp();
-        if (((upto >> lane) & 1u) && !later) table[h] = (int)w;
+        if (((upto >> lane) & 1u) && !later) table[h] = (unsigned short)w;
         __syncwarp();
         if (!hits) {
             pos += __popc(actm);  // all literals
@@ -235,59 +237,55 @@ __device__ uint32_t lz_chunk_size_warp(const unsigned char* in, uint32_t n, int*
     return out;
 }
 
-// sizes[b] = LzStream::byte_size of block b (chunks of 64 KiB: 8 + payload
-// each); one warp per block, a hash table per warp.
-__global__ void k_lz_sizes(const double* dense, uint64_t nblocks, uint32_t nn, int* tables, uint32_t* sizes) {
+// The step's LZ row: the sizes are summed by atomics (integers: any order
+// gives the same sum) and the last warp writes compressed_bytes and ratio
+// (pipeline.hpp:270-272).  SWE (device clock): a launch is live only if the
+// step kernel before it advanced the step counter; its row is rows_at[k - 1]
+// and state[0] remembers the last row finalized, so a no-op launch changes
+// nothing.
+struct LzFinal {
+    unsigned long long* state;  // [0] last SWE row done, [1] running sum, [2] warps done (both back to 0 after)
+    wg_metrics_row* row;        // the step's row (transport, D2Q9)
+    wg_metrics_row* rows_at;    // SWE: the row buffer shifted by the session's row0
+    const unsigned long long* steps;  // SWE: the device step counter, else null
+};
+
+// LzStream::byte_size of every block (chunks of 64 KiB: 8 + payload each):
+// one warp per block, a 16 KiB shared-memory hash table per warp, the block
+// read through L2 (it was written by the step kernel just before).
+constexpr int kLzWarps = 2;  // per CTA: 32 KiB of tables, 7 CTAs (14 warps) per SM
+__global__ void __launch_bounds__(32 * kLzWarps) k_lz_sizes(const double* dense, uint64_t nblocks, uint32_t nn,
+                                                            LzFinal f) {
+    __shared__ __align__(16) unsigned short tables[kLzWarps][8192];
+    unsigned long long k = 0;
+    if (f.steps) {
+        k = *f.steps;
+        if (k <= f.state[0]) return;  // uniform: the step launch was a no-op
+    }
     const uint64_t wid = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) / 32;
     const uint64_t nw = (uint64_t)gridDim.x * blockDim.x / 32;
-    int* table = tables + wid * 8192;
+    unsigned short* table = tables[threadIdx.x / 32];
+    unsigned long long sum = 0;
     for (uint64_t b = wid; b < nblocks; b += nw) {
         const unsigned char* in = reinterpret_cast<const unsigned char*>(dense + b * nn);
         const uint32_t bytes = nn * 8;
-        uint32_t total = 0;
         for (uint32_t off = 0; off < bytes; off += 65536u) {
             const uint32_t len = min(65536u, bytes - off);
-            total += 8 + lz_chunk_size_warp(in + off, len, table);
+            sum += 8 + lz_chunk_size_warp(in + off, len, table);
         }
-        if ((threadIdx.x & 31) == 0) sizes[b] = total;
     }
-}
-
-// The step's row: compressed_bytes = sum of the LZ sizes (fixed order), ratio.
-// SWE (device clock): only a live launch advanced the step counter; its row
-// is rows_at[k - 1] (rows_at = the row buffer shifted by the session's row0)
-// and `done` remembers the last row finalized, so a no-op launch changes nothing.
-__global__ void k_lz_finalize_swe(const uint32_t* sizes, uint64_t nblocks, wg_metrics_row* rows_at,
-                                  const unsigned long long* steps, unsigned long long* done) {
-    const unsigned long long k = *steps;
-    if (k <= *done) return;  // uniform: the launch was a no-op
-    __shared__ unsigned long long part[256];
-    unsigned long long s = 0;
-    for (uint64_t b = threadIdx.x; b < nblocks; b += blockDim.x) s += sizes[b];
-    part[threadIdx.x] = s;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        unsigned long long tot = 0;
-        for (int i = 0; i < 256; ++i) tot += part[i];
-        wg_metrics_row* row = rows_at + (k - 1);
-        row->compressed_bytes = tot;
-        row->ratio = tot > 0 ? (double)row->dense_bytes / (double)tot : 1.0;
-        *done = k;
-    }
-}
-
-__global__ void k_lz_finalize(const uint32_t* sizes, uint64_t nblocks, wg_metrics_row* row) {
-    __shared__ unsigned long long part[256];
-    unsigned long long s = 0;
-    for (uint64_t b = threadIdx.x; b < nblocks; b += blockDim.x) s += sizes[b];
-    part[threadIdx.x] = s;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        unsigned long long tot = 0;
-        for (int k = 0; k < 256; ++k) tot += part[k];
-        row->compressed_bytes = tot;
-        row->ratio = tot > 0 ? (double)row->dense_bytes / (double)tot : 1.0;  // pipeline.hpp:270-272
-    }
+    if ((threadIdx.x & 31) != 0) return;
+    atomicAdd(&f.state[1], sum);
+    __threadfence();
+    if (atomicAdd(&f.state[2], 1ull) != nw - 1) return;
+    __threadfence();
+    const unsigned long long tot = atomicAdd(&f.state[1], 0ull);
+    wg_metrics_row* row = f.steps ? f.rows_at + (k - 1) : f.row;
+    row->compressed_bytes = tot;
+    row->ratio = tot > 0 ? (double)row->dense_bytes / (double)tot : 1.0;
+    f.state[1] = 0;
+    f.state[2] = 0;
+    if (f.steps) f.state[0] = k;
 }
 
 __global__ void k_set_u64(unsigned long long* p, unsigned long long v) { *p = v; }
@@ -335,10 +333,8 @@ struct Session {
     unsigned long long* phase = nullptr;  // WG_PHASE_TIMING builds only
     // Codec::lz metrics staging
     double* lz_dense = nullptr;
-    uint32_t* lz_sizes = nullptr;
-    unsigned long long* lz_done = nullptr;  // SWE: the last row given its LZ sizes
-    int* lz_tables = nullptr;
-    uint32_t lz_threads = 0;
+    unsigned long long* lz_done = nullptr;  // LzFinal::state
+    uint32_t lz_ctas = 0;
     // pinned-host upload pipeline (created on first use)
     double* stage = nullptr;
     cudaStream_t copy_stream = nullptr;
@@ -411,13 +407,9 @@ struct Session {
         cudaFree(stage);
         stage = nullptr;
         cudaFree(lz_dense);
-        cudaFree(lz_sizes);
         cudaFree(lz_done);
         lz_done = nullptr;
-        cudaFree(lz_tables);
         lz_dense = nullptr;
-        lz_sizes = nullptr;
-        lz_tables = nullptr;
         partials = nullptr;
         done = nullptr;
         bump = nullptr;
@@ -546,11 +538,13 @@ struct Session {
             if (nb * N * N * 8 > (8ull << 30))
                 raise(WG_INVALID_ARGUMENT, "Codec::lz metrics: grid too large for the coefficient staging");
             lz_dense = dalloc<double>(nb * N * N + 1);  // + 8 B tail padding for the word loads
-            lz_sizes = dalloc<uint32_t>(nb);
-            lz_done = dalloc<unsigned long long>(1);
-            WG_CUDA(cudaMemsetAsync(lz_done, 0, sizeof(unsigned long long), stream));
-            lz_threads = (uint32_t)((std::min<uint64_t>(nb, 4096) + 1) / 2 * 2);  // warps, 2 per CTA of 64
-            lz_tables = dalloc<int>((uint64_t)lz_threads * 8192);
+            lz_done = dalloc<unsigned long long>(3);
+            WG_CUDA(cudaMemsetAsync(lz_done, 0, 3 * sizeof(unsigned long long), stream));
+            int lz_per_sm = 0, lz_sms = 0;
+            WG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&lz_per_sm, k_lz_sizes, 32 * kLzWarps, 0));
+            WG_CUDA(cudaDeviceGetAttribute(&lz_sms, cudaDevAttrMultiProcessorCount, shard.device));
+            lz_ctas = (uint32_t)std::min<uint64_t>((nb + kLzWarps - 1) / kLzWarps,
+                                                   (uint64_t)std::max(lz_per_sm, 1) * lz_sms);
         }
         // the pinned-host upload pipeline (allocated here, outside any timed upload)
         stage = dalloc<double>(2 * (uint64_t)stage_chunk() * sg.m * geo.tcount);
@@ -750,11 +744,9 @@ struct Session {
             ev_main.emplace_back(e0, e1);
         }
         if (lz_dense) {  // Codec::lz: the step's compressed_bytes/ratio from the LZ stream sizes
-            k_lz_sizes<<<lz_threads / 2, 64, 0, stream>>>(lz_dense, (uint64_t)sg.npatch * sg.m, N * N,
-                                                                  lz_tables, lz_sizes);
+            k_lz_sizes<<<lz_ctas, 32 * kLzWarps, 0, stream>>>(lz_dense, (uint64_t)sg.npatch * sg.m, N * N,
+                                                               LzFinal{lz_done, a.row_out, nullptr, nullptr});
             WG_LAUNCH_CHECK("lz sizes");
-            k_lz_finalize<<<1, 256, 0, stream>>>(lz_sizes, (uint64_t)sg.npatch * sg.m, a.row_out);
-            WG_LAUNCH_CHECK("lz finalize");
         }
         if (ks.decode_l2 && cfg.compute_l2 && geo.tiles == 1) {
             // l2_error(assemble(grid, 0), exact_transport(t), cfg) of the new
@@ -793,10 +785,9 @@ struct Session {
         WG_LAUNCH_CHECK("fused swe step");
         if (lz_dense) {
             const uint64_t nb = (uint64_t)sg.npatch * sg.m;
-            k_lz_sizes<<<lz_threads / 2, 64, 0, stream>>>(lz_dense, nb, N * N, lz_tables, lz_sizes);
+            k_lz_sizes<<<lz_ctas, 32 * kLzWarps, 0, stream>>>(lz_dense, nb, N * N,
+                                                               LzFinal{lz_done, nullptr, rows - row0, swe + 4});
             WG_LAUNCH_CHECK("lz sizes");
-            k_lz_finalize_swe<<<1, 256, 0, stream>>>(lz_sizes, nb, rows - row0, swe + 4, lz_done);
-            WG_LAUNCH_CHECK("lz finalize");
         }
         if (profiling) {
             WG_CUDA(cudaEventRecord(e1, stream));

@@ -164,10 +164,9 @@ __global__ void __launch_bounds__(SweLayout<N>::NT, WG_SWE_MIN_BLOCKS) k_swe_ste
             WG_PHASE_MARK(4);
             unsigned nz = 0, zr = 0;
             if (lane_ok)
-                fwd_row_threshold<N, L>(T, li, a.thr, v, nz, zr,
-                                        MODE == MODE_STEP_LZ ? a.lz_dense + ((size_t)p * 3 + s) * NN + (size_t)li * N
-                                                             : nullptr);
+                fwd_row_threshold<N, L>(T, li, a.thr, v, nz, zr, MODE == MODE_STEP_LZ ? T + (li + 1) * TP + 1 : nullptr);
             cta_inclusive_scan<NT>(((unsigned long long)zr << 32) | nz, inc);
+            if (MODE == MODE_STEP_LZ) tiles_to_dense<N, NT>(tiles, TILE, 3, a.lz_dense + (size_t)p * 3 * NN);
             if (t == 0) {
                 for (int sl = 0; sl < 3; ++sl) {
                     const unsigned long long base = sl == 0 ? 0ull : inc[sl * N - 1];
