@@ -26,6 +26,9 @@ namespace wg {
 #define WG_LBM_PREFETCH 1
 #endif
 
+#ifndef WG_LBM_CELLS
+#define WG_LBM_CELLS 2  // cells per collide iteration
+#endif
 #ifndef WG_LBM_EXTRA_WARPS
 #define WG_LBM_EXTRA_WARPS 1  // 256 threads: the cell phases (stream, collide) get a warp more (+1-2 %)
 #endif
@@ -113,30 +116,34 @@ __device__ __forceinline__ double decode_stream_collide(const StepArgs& a, doubl
         WG_PHASE_MARK(1);
     }
     double mfv = 0.0;
-    // two cells per iteration: 18 independent scratch loads in flight
-    for (int c0 = threadIdx.x; c0 < NN; c0 += 2 * NT) {
-        const int c1 = c0 + NT;
-        const bool two = c1 < NN;
-        double f0[9], f1[9];
+    // WG_LBM_CELLS cells per iteration: 9 x that many independent scratch loads in flight
+    constexpr int K = WG_LBM_CELLS;
+    for (int c0 = threadIdx.x; c0 < NN; c0 += K * NT) {
+        double f[K][9];
 #pragma unroll
-        for (int q = 0; q < 9; ++q) {
-            f0[q] = S.pop(q)[c0];
-            f1[q] = two ? S.pop(q)[c1] : 1.0;
+        for (int u = 0; u < K; ++u) {
+            const int c = c0 + u * NT;
+#pragma unroll
+            for (int q = 0; q < 9; ++q) f[u][q] = c < NN ? S.pop(q)[c] : 1.0;
         }
-        lbm_collide(f0, a.omega);
-        lbm_collide(f1, a.omega);
-        const int i0 = c0 / N, j0 = c0 - i0 * N, i1 = c1 / N, j1 = c1 - i1 * N;
-        const double w0 = ((i0 == 0 || i0 == N - 1) ? 0.5 : 1.0) * ((j0 == 0 || j0 == N - 1) ? 0.5 : 1.0);
-        const double w1 = ((i1 == 0 || i1 == N - 1) ? 0.5 : 1.0) * ((j1 == 0 || j1 == N - 1) ? 0.5 : 1.0);
 #pragma unroll
-        for (int q = 0; q < 9; ++q) {
-            S.pop(q)[c0] = f0[q];
-            mfv += w0 * f0[q];
-            if (two) {
-                S.pop(q)[c1] = f1[q];
-                mfv += w1 * f1[q];
+        for (int u = 0; u < K; ++u) lbm_collide(f[u], a.omega);
+        double w[K];
+#pragma unroll
+        for (int u = 0; u < K; ++u) {
+            const int c = c0 + u * NT, i = c / N, j = c - i * N;
+            w[u] = ((i == 0 || i == N - 1) ? 0.5 : 1.0) * ((j == 0 || j == N - 1) ? 0.5 : 1.0);
+        }
+#pragma unroll
+        for (int q = 0; q < 9; ++q)
+#pragma unroll
+            for (int u = 0; u < K; ++u) {
+                const int c = c0 + u * NT;
+                if (c < NN) {
+                    S.pop(q)[c] = f[u][q];
+                    mfv += w[u] * f[u][q];
+                }
             }
-        }
     }
     __syncthreads();
     WG_PHASE_MARK(2);
