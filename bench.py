@@ -389,7 +389,7 @@ def bench_b200(args, w: dict):
         "e2e": e2e,
         "compute_ceiling": compute_ceiling(lib, w, value / world),  # per GPU
         # one fused kernel launch per step (k_*_step<STEP>); Codec::lz adds the
-        # LZ-size pass and its reduction (k_lz_sizes, k_lz_finalize)
+        # LZ-size pass (k_lz_sizes, which also writes the step's row)
         "gpu_launches": args.steps * (2 if w.get("codec") == "lz" else 1),
         "clocks": clocks.summary(),
         "device_bytes": info.device_bytes,
