@@ -247,6 +247,10 @@ def config_json(args, w):
             "parallelism": f"patch-row shards x{args.gpus}"
                            + (" (weak: one periodic copy of the grid per rank)" if w.get("scaling", "weak") == "weak" else
                               " (strong: the grid split over the ranks)"),
+            "halo_exchange": ("none (one shard)" if args.gpus == 1 else
+                              "in-kernel NVLink peer stores (WG_PEER_HALOS=1)"
+                              if os.environ.get("WG_PEER_HALOS") == "1" and w["scheme"] != "swe"
+                              else "NCCL point-to-point between steps"),
             "l2": "flushed between timed steps (256 MiB write)"}
 
 
@@ -306,6 +310,7 @@ def bench_b200(args, w: dict):
         del full
 
     sess = ShardedSession(lib, cfg, shard, stream.cuda_stream, dist if world > 1 else None)
+    maybe_peer_halos(sess, cfg, dist, world)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{local}")
     try:
         if device_init:
@@ -432,6 +437,7 @@ def e2e_run(lib, cfg, shard, stream, host, args, dt, dist, copies=1):
     from paper_2302_09883_b200.distributed import ShardedSession, collective_device
 
     sess = ShardedSession(lib, cfg, shard, stream.cuda_stream, dist)
+    maybe_peer_halos(sess, cfg, dist, shard.world)
     row_buf = torch.empty(args.steps * C.sizeof(abi.MetricsRowC), dtype=torch.uint8, pin_memory=True)
     try:
         if dist:
@@ -466,6 +472,19 @@ def e2e_run(lib, cfg, shard, stream, host, args, dt, dist, copies=1):
             "h2d_bytes_per_step": host.nbytes / args.steps, "d2h_bytes_per_step": C.sizeof(abi.MetricsRowC),
             "note": "initial state uploaded once inside the timed region (bytes amortised per step); "
                     "every step's metrics row read back (async D2H into page-locked memory)"}
+
+
+def peer_halos_wanted(cfg, dist, world: int) -> bool:
+    """WG_PEER_HALOS=1 (opt-in until validated on a multi-GPU box): the step
+    kernels store the halo lines into the neighbours' halo slots over NVLink
+    (CUDA IPC), instead of an NCCL exchange between steps."""
+    return (world > 1 and os.environ.get("WG_PEER_HALOS") == "1" and cfg.scheme != "swe"
+            and dist is not None and dist.get_backend() == "nccl")
+
+
+def maybe_peer_halos(sess, cfg, dist, world: int) -> None:
+    if peer_halos_wanted(cfg, dist, world):
+        sess.connect_peers()
 
 
 def traffic_from_profiles(workload: str):

@@ -300,6 +300,30 @@ wg_status wg_session_cfl_vmax(wg_session* s, unsigned long long** vmax_bits);
 wg_status wg_session_halo(wg_session* s, double** send_lo, double** send_hi,
                           double** recv_lo, double** recv_hi);
 
+/* Peer halo mode (multi-GPU over NVLink, transport and D2Q9; replaces the
+ * host-driven exchange of the blocks above — the halo exchange of
+ * sync_ghosts, patchgrid.hpp:131-201, across shards).  The step kernel
+ * stores the halo lines straight into the ring neighbours' halo slots; a
+ * step waits (on the device, bounded: WG_LOGIC after 10 s) until both
+ * neighbours delivered the same generation of edge lines and announces its
+ * own when complete, so no host exchange or NCCL call sits between steps.
+ *   export: this session's two edge allocations, its 2 flag words, its rows;
+ *   attach: the neighbours' exports, mapped into this process (the same
+ *     pointers in one process, or wg_ipc_open of wg_ipc_handle across
+ *     processes); above = rank - 1, below = rank + 1 (mod world);
+ *   push: after upload / load (every rank, after a barrier): the current
+ *     halo lines to the neighbours. */
+wg_status wg_session_peer_export(wg_session* s, void** edge_mem0, void** edge_mem1, void** flags,
+                                 uint32_t* rows);
+wg_status wg_session_peer_attach(wg_session* s, void* above_mem0, void* above_mem1, void* above_flags,
+                                 uint32_t above_rows, void* below_mem0, void* below_mem1,
+                                 void* below_flags, uint32_t below_rows);
+wg_status wg_session_peer_push(wg_session* s);
+/* CUDA IPC of a device allocation (64-byte handle) for the peer mode. */
+wg_status wg_ipc_handle(void* dev_ptr, unsigned char out[64]);
+wg_status wg_ipc_open(const unsigned char in[64], void** dev_ptr);
+wg_status wg_ipc_close(void* dev_ptr);
+
 /* Per-step metrics rows accumulated on the device since upload (nsteps rows;
  * this shard's partial sums — multi-GPU callers all-reduce them). */
 wg_status wg_session_metrics(wg_session* s, wg_metrics_row* rows,

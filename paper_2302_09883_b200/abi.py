@@ -218,6 +218,12 @@ _PROTOS = {
     "wg_session_step": (i32, [vp, f64]),
     "wg_session_halo": (i32, [vp, P(vp), P(vp), P(vp), P(vp)]),
     "wg_session_cfl_vmax": (i32, [vp, P(vp)]),
+    "wg_session_peer_export": (i32, [vp, P(vp), P(vp), P(vp), P(C.c_uint32)]),
+    "wg_session_peer_attach": (i32, [vp, vp, vp, vp, C.c_uint32, vp, vp, vp, C.c_uint32]),
+    "wg_session_peer_push": (i32, [vp]),
+    "wg_ipc_handle": (i32, [vp, C.c_char_p]),
+    "wg_ipc_open": (i32, [C.c_char_p, P(vp)]),
+    "wg_ipc_close": (i32, [vp]),
     "wg_session_save": (i32, [vp, C.c_char_p]),
     "wg_session_load": (i32, [vp, C.c_char_p]),
     "wg_session_metrics": (i32, [vp, P(MetricsRowC), u64, P(u64)]),
@@ -234,7 +240,7 @@ _PROTOS = {
 }
 
 #: the symbols every implementation of the ABI exports
-HOST_SYMBOLS = [k for k in _PROTOS if not (k.startswith("wg_session") or k.startswith("wg_dev"))]
+HOST_SYMBOLS = [k for k in _PROTOS if not k.startswith(("wg_session", "wg_dev", "wg_ipc"))]
 #: the symbols only the device product exports
 DEVICE_SYMBOLS = [k for k in _PROTOS if k not in HOST_SYMBOLS]
 

@@ -134,6 +134,21 @@ __device__ __forceinline__ size_t edge_ix(uint32_t slot, uint32_t b, uint32_t q,
     return (((size_t)slot * g.P1 + b) * g.me + q) * (size_t)N;
 }
 
+// Edge-line stores of the row edges: the halo lines (owned slot 1 of rowlo,
+// owned slot R of rowhi) also go straight into the ring neighbours' halo
+// slots when peers are attached (EdgeSet::peer_lo / peer_hi), so the step
+// kernel itself performs the halo exchange over NVLink.
+__device__ __forceinline__ void put_rowlo(const EdgeSet& e, const ShardGeom& g, uint32_t slot, uint32_t b, uint32_t q,
+                                          int N, int j, double x) {
+    e.rowlo[edge_ix(slot, b, q, g, N) + j] = x;
+    if (slot == 1 && e.peer_lo) e.peer_lo[edge_ix(0, b, q, g, N) + j] = x;
+}
+__device__ __forceinline__ void put_rowhi(const EdgeSet& e, const ShardGeom& g, uint32_t slot, uint32_t b, uint32_t q,
+                                          int N, int j, double x) {
+    e.rowhi[edge_ix(slot, b, q, g, N) + j] = x;
+    if (slot == g.R && e.peer_hi) e.peer_hi[edge_ix(0, b, q, g, N) + j] = x;
+}
+
 // ROW phase of the decode: row li of component (p, q) from the store into
 // the tile (CSR scatter or raw copy), inverse transform along dim 1
 // (idwt_nd, wavelet.hpp:200-223 does the last dimension first).  Returns
@@ -331,9 +346,8 @@ __device__ __forceinline__ void inv_row_to_tile(double* T, int i, double (&v)[N]
 template <int N>
 __device__ __forceinline__ void write_edges(const EdgeSet& e, const PatchPos& pp, uint32_t q,
                                             const ShardGeom& g, int j, const double (&v)[N]) {
-    const size_t own = edge_ix((uint32_t)(pp.ar + 1), pp.b, q, g, N);
-    e.rowlo[own + j] = v[1];
-    e.rowhi[own + j] = v[N - 2];
+    put_rowlo(e, g, (uint32_t)(pp.ar + 1), pp.b, q, N, j, v[1]);
+    put_rowhi(e, g, (uint32_t)(pp.ar + 1), pp.b, q, N, j, v[N - 2]);
     const size_t oc = edge_ix((uint32_t)pp.ar, pp.b, q, g, N);
     if (j == 1) {
 #pragma unroll
@@ -369,8 +383,8 @@ template <int N>
 __device__ __forceinline__ void write_edges_lbm(const EdgeSet& e, const PatchPos& pp, int q, const ShardGeom& g,
                                                 int j, const double (&v)[N]) {
     const int cxq = lbm_cx(q), cyq = lbm_cy(q);
-    if (cxq == -1) e.rowlo[edge_ix((uint32_t)(pp.ar + 1), pp.b, lbm_slot_rowlo(q), g, N) + j] = v[1];
-    if (cxq == 1) e.rowhi[edge_ix((uint32_t)(pp.ar + 1), pp.b, lbm_slot_rowhi(q), g, N) + j] = v[N - 2];
+    if (cxq == -1) put_rowlo(e, g, (uint32_t)(pp.ar + 1), pp.b, lbm_slot_rowlo(q), N, j, v[1]);
+    if (cxq == 1) put_rowhi(e, g, (uint32_t)(pp.ar + 1), pp.b, lbm_slot_rowhi(q), N, j, v[N - 2]);
     if (cyq == -1 && j == 1) {
         double* d = e.collo + edge_ix((uint32_t)pp.ar, pp.b, lbm_slot_collo(q), g, N);
 #pragma unroll
@@ -391,9 +405,8 @@ __device__ __forceinline__ void write_edges_lbm_tile(const EdgeSet& e, const Pat
                                                      int li, const double* T) {
     constexpr int TP = N + 2;
     const int cxq = lbm_cx(q), cyq = lbm_cy(q);
-    if (cxq == -1) e.rowlo[edge_ix((uint32_t)(pp.ar + 1), pp.b, lbm_slot_rowlo(q), g, N) + li] = T[2 * TP + li + 1];
-    if (cxq == 1)
-        e.rowhi[edge_ix((uint32_t)(pp.ar + 1), pp.b, lbm_slot_rowhi(q), g, N) + li] = T[(N - 1) * TP + li + 1];
+    if (cxq == -1) put_rowlo(e, g, (uint32_t)(pp.ar + 1), pp.b, lbm_slot_rowlo(q), N, li, T[2 * TP + li + 1]);
+    if (cxq == 1) put_rowhi(e, g, (uint32_t)(pp.ar + 1), pp.b, lbm_slot_rowhi(q), N, li, T[(N - 1) * TP + li + 1]);
     if (cyq == -1) e.collo[edge_ix((uint32_t)pp.ar, pp.b, lbm_slot_collo(q), g, N) + li] = T[(li + 1) * TP + 2];
     if (cyq == 1) e.colhi[edge_ix((uint32_t)pp.ar, pp.b, lbm_slot_colhi(q), g, N) + li] = T[(li + 1) * TP + N - 1];
 }
@@ -634,7 +647,11 @@ __device__ __forceinline__ void finalize_step(const StepArgs& a, const StepParti
     if (threadIdx.x == 0) {
         a.partials[blockIdx.x] = mine;
         if (clk) atomicMax(a.swe_vmax + ((clk->k + 1) & 1), (unsigned long long)__double_as_longlong(cta_vmax));
-        __threadfence();
+        // (cumulative over the CTA's stores, the kernels end their patch
+        // loops with a barrier): peer halo lines reach the neighbours before
+        // the step is complete
+        if (a.eout.peer_lo) __threadfence_system();
+        else __threadfence();
         const unsigned prev = atomicAdd(a.done, 1u);
         am_last = prev == gridDim.x - 1;
     }

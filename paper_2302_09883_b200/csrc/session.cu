@@ -290,6 +290,34 @@ __global__ void __launch_bounds__(32 * kLzWarps) k_lz_sizes(const double* dense,
 
 __global__ void k_set_u64(unsigned long long* p, unsigned long long v) { *p = v; }
 
+// ---- peer halo mode (multi-GPU): the step kernels store the halo lines into
+// the ring neighbours' halo slots themselves (EdgeSet::peer_lo/peer_hi); a
+// step may start once both neighbours delivered the same generation of edge
+// lines, and announces its own when it is complete. -------------------------
+__global__ void k_peer_signal(unsigned long long* to_above, unsigned long long* to_below, unsigned long long gen) {
+    __threadfence_system();
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(to_above), "l"(gen) : "memory");
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(to_below), "l"(gen) : "memory");
+}
+
+// Bounded wait (10 s): a neighbour that never delivers becomes an error, not a hang.
+__global__ void k_peer_wait(const unsigned long long* flags, unsigned long long gen, unsigned* err) {
+    unsigned long long t0, t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    for (;;) {
+        unsigned long long a, b;
+        asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(a) : "l"(flags) : "memory");
+        asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(b) : "l"(flags + 1) : "memory");
+        if (a >= gen && b >= gen) return;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        if (t - t0 > 10000000000ull) {
+            atomicOr(err, ERR_PEER_TIMEOUT);
+            return;
+        }
+        __nanosleep(200);
+    }
+}
+
 __global__ void k_swe_clock_reset(double* td, unsigned long long* vmax_bits, unsigned long long* steps) {
     td[0] = 0.0;
     td[1] = 0.0;
@@ -317,6 +345,12 @@ struct Session {
     EdgeSet edges[2]{};
     double* edge_mem[2] = {nullptr, nullptr};
     StepPartial* partials = nullptr;     // per CTA of the step launch
+    // peer halo mode: [0] edge generation delivered by the above neighbour, [1] by the below one
+    unsigned long long* peer_flags = nullptr;
+    unsigned long long* sig_above = nullptr;  // the above neighbour's word [1]
+    unsigned long long* sig_below = nullptr;  // the below neighbour's word [0]
+    unsigned long long peer_gen = 0;          // edge generations this session delivered
+    bool peers = false;
     unsigned* done = nullptr;            // CTA completion counter
     double* scratch = nullptr;           // D2Q9 per-CTA staging (L2-resident)
     unsigned grid = 0;                   // launch grid of the step kernels
@@ -387,6 +421,8 @@ struct Session {
             edge_mem[k] = nullptr;
         }
         cudaFree(partials);
+        cudaFree(peer_flags);
+        peer_flags = nullptr;
         cudaFree(done);
         cudaFree(scratch);
         scratch = nullptr;
@@ -517,6 +553,8 @@ struct Session {
             edges[k].colhi = edge_mem[k] + 2 * rowline + colline;
         }
         partials = dalloc<StepPartial>(grid);
+        peer_flags = dalloc<unsigned long long>(2);
+        WG_CUDA(cudaMemsetAsync(peer_flags, 0, 2 * sizeof(unsigned long long), stream));
         done = dalloc<unsigned>(1);
         bump = dalloc<unsigned long long>(2);
         err = dalloc<unsigned>(1);
@@ -676,6 +714,44 @@ struct Session {
         sync();
     }
 
+    // Peer halo mode.  above_mem/below_mem: the neighbours' edge allocations
+    // (both buffer parities) and flag words, mapped into this process.
+    void peer_attach(double* const above_mem[2], uint32_t above_rows, unsigned long long* above_flags,
+                     double* const below_mem[2], uint32_t below_rows, unsigned long long* below_flags) {
+        if (is_swe()) raise(WG_INVALID_ARGUMENT, "peer halos: transport and D2Q9 sessions only (SWE all-reduces its CFL speed)");
+        if (sg.R == 0) raise(WG_INVALID_ARGUMENT, "peer halos: empty shard");
+        const uint64_t line = halo_doubles();
+        for (int k = 0; k < 2; ++k) {
+            if (!above_mem[k] || !below_mem[k]) raise(WG_INVALID_ARGUMENT, "peer halos: null edge allocation");
+            edges[k].peer_lo = above_mem[k] + (uint64_t)(above_rows + 1) * line;  // above's rowlo slot R+1
+            edges[k].peer_hi = below_mem[k] + (uint64_t)(below_rows + 2) * line;  // below's rowhi slot 0
+        }
+        sig_above = above_flags + 1;
+        sig_below = below_flags + 0;
+        peers = true;
+    }
+
+    void peer_signal() {
+        k_peer_signal<<<1, 1, 0, stream>>>(sig_above, sig_below, peer_gen + 1);
+        WG_LAUNCH_CHECK("peer signal");
+        ++peer_gen;
+    }
+
+    // The current edge lines' halo rows to the neighbours (after upload /
+    // load, which build the edges locally), once both neighbours reached
+    // this session's generation.
+    void peer_push() {
+        if (!peers) raise(WG_INVALID_ARGUMENT, "peer halos: no peers attached");
+        k_peer_wait<<<1, 1, 0, stream>>>(peer_flags, peer_gen, err);
+        const EdgeSet& e = edges[cur];
+        const uint64_t line = halo_doubles();
+        WG_CUDA(cudaMemcpyAsync(e.peer_lo, e.rowlo + line, line * sizeof(double), cudaMemcpyDeviceToDevice, stream));
+        WG_CUDA(cudaMemcpyAsync(e.peer_hi, e.rowhi + (uint64_t)sg.R * line, line * sizeof(double),
+                                cudaMemcpyDeviceToDevice, stream));
+        peer_signal();
+        sync();
+    }
+
     StepArgs step_args(int src, int dst) const {
         StepArgs a{};
         a.store_in = store[src];
@@ -737,8 +813,10 @@ struct Session {
             e1 = take_event();
             WG_CUDA(cudaEventRecord(e0, stream));
         }
+        if (peers) k_peer_wait<<<1, 1, 0, stream>>>(peer_flags, peer_gen, err);
         (lz_dense ? ks.main_lz : ks.main)<<<grid, ks.threads, ks.smem, stream>>>(a);
         WG_LAUNCH_CHECK("fused step");
+        if (peers) peer_signal();
         if (profiling) {
             WG_CUDA(cudaEventRecord(e1, stream));
             ev_main.emplace_back(e0, e1);
@@ -1199,6 +1277,54 @@ wg_status wg_session_halo(wg_session* sp, double** send_lo, double** send_hi, do
         if (recv_lo) *recv_lo = e.rowhi;                         // slot 0: halo above
         if (recv_hi) *recv_hi = e.rowlo + (uint64_t)(s->sg.R + 1) * line;  // slot R+1: halo below
     });
+}
+
+wg_status wg_session_peer_export(wg_session* sp, void** edge_mem0, void** edge_mem1, void** flags, uint32_t* rows) {
+    return guard([&] {
+        Session* s = reinterpret_cast<Session*>(sp);
+        if (edge_mem0) *edge_mem0 = s->edge_mem[0];
+        if (edge_mem1) *edge_mem1 = s->edge_mem[1];
+        if (flags) *flags = s->peer_flags;
+        if (rows) *rows = s->sg.R;
+    });
+}
+
+wg_status wg_session_peer_attach(wg_session* sp, void* above_mem0, void* above_mem1, void* above_flags,
+                                 uint32_t above_rows, void* below_mem0, void* below_mem1, void* below_flags,
+                                 uint32_t below_rows) {
+    return guard([&] {
+        Session* s = reinterpret_cast<Session*>(sp);
+        double* const am[2] = {static_cast<double*>(above_mem0), static_cast<double*>(above_mem1)};
+        double* const bm[2] = {static_cast<double*>(below_mem0), static_cast<double*>(below_mem1)};
+        if (!above_flags || !below_flags) raise(WG_INVALID_ARGUMENT, "peer halos: null flag words");
+        s->peer_attach(am, above_rows, static_cast<unsigned long long*>(above_flags), bm, below_rows,
+                       static_cast<unsigned long long*>(below_flags));
+    });
+}
+
+wg_status wg_session_peer_push(wg_session* s) {
+    return guard([&] { reinterpret_cast<Session*>(s)->peer_push(); });
+}
+
+wg_status wg_ipc_handle(void* dev_ptr, unsigned char out[64]) {
+    return guard([&] {
+        cudaIpcMemHandle_t h;
+        WG_CUDA(cudaIpcGetMemHandle(&h, dev_ptr));
+        static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
+        std::memcpy(out, &h, 64);
+    });
+}
+
+wg_status wg_ipc_open(const unsigned char in[64], void** dev_ptr) {
+    return guard([&] {
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, in, 64);
+        WG_CUDA(cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess));
+    });
+}
+
+wg_status wg_ipc_close(void* dev_ptr) {
+    return guard([&] { WG_CUDA(cudaIpcCloseMemHandle(dev_ptr)); });
 }
 
 wg_status wg_session_cfl_vmax(wg_session* sp, unsigned long long** vmax_bits) {

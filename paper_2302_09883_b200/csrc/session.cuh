@@ -35,6 +35,14 @@ struct EdgeSet {
     double* rowhi;  // [(R+2) slots][P1][m][n]: logical row n-2
     double* collo;  // [R][P1][m][n]: logical column 1
     double* colhi;  // [R][P1][m][n]: logical column n-2
+    // peer halo mode (multi-GPU, opt-in): the ring neighbours' halo slots of
+    // the same buffer parity, mapped into this process (NVLink P2P / IPC).
+    // The line of owned slot 1 (rowlo) is also stored into peer_lo = the
+    // above neighbour's rowlo slot R_above + 1; the line of owned slot R
+    // (rowhi) into peer_hi = the below neighbour's rowhi slot 0.  Null: the
+    // halo blocks are exchanged by the host (NCCL) instead.
+    double* peer_lo;
+    double* peer_hi;
 };
 
 struct ShardGeom {

@@ -133,23 +133,79 @@ class ShardedSession:
         lib.check(lib.wg_session_info_get(self.handle, C.byref(self.info)))
         self._halo = None
         self.swe = cfg.scheme == "swe"
+        self.peer = False
+        self._ipc_opened: list[int] = []
+
+    # ---- peer halo mode (wg_session_peer_*): the step kernels store the halo
+    # lines into the neighbours' halo slots over NVLink, no exchange between
+    # steps.  Transport and D2Q9; opt-in (bench: WG_PEER_HALOS=1).
+    def peer_export(self) -> dict:
+        m0, m1, fl, rows = abi.vp(), abi.vp(), abi.vp(), C.c_uint32()
+        self.lib.check(self.lib.wg_session_peer_export(self.handle, C.byref(m0), C.byref(m1), C.byref(fl),
+                                                       C.byref(rows)))
+        return {"mem0": m0.value, "mem1": m1.value, "flags": fl.value, "rows": rows.value}
+
+    def peer_attach(self, above: dict, below: dict):
+        self.lib.check(self.lib.wg_session_peer_attach(
+            self.handle, abi.vp(above["mem0"]), abi.vp(above["mem1"]), abi.vp(above["flags"]), above["rows"],
+            abi.vp(below["mem0"]), abi.vp(below["mem1"]), abi.vp(below["flags"]), below["rows"]))
+        self.peer = True
+
+    def peer_push(self):
+        self.lib.check(self.lib.wg_session_peer_push(self.handle))
+
+    def connect_peers(self):
+        """Multi-process: map the ring neighbours' edge allocations and flag
+        words by CUDA IPC (handles all-gathered over the process group) and
+        attach them.  Collective: every rank calls it."""
+        exp = self.peer_export()
+        mine = {"rows": exp["rows"]}
+        for k in ("mem0", "mem1", "flags"):
+            buf = C.create_string_buffer(64)
+            self.lib.check(self.lib.wg_ipc_handle(abi.vp(exp[k]), buf))
+            mine[k] = buf.raw
+        allx = [None] * self.shard.world
+        self.dist.all_gather_object(allx, mine)
+        above_r, below_r = ring_neighbours(self.shard.rank, self.shard.world)
+        opened: dict[int, dict] = {}
+        for r in {above_r, below_r}:
+            d = {"rows": allx[r]["rows"]}
+            for k in ("mem0", "mem1", "flags"):
+                p = abi.vp()
+                self.lib.check(self.lib.wg_ipc_open(allx[r][k], C.byref(p)))
+                self._ipc_opened.append(p.value)
+                d[k] = p.value
+            opened[r] = d
+        self.peer_attach(opened[above_r], opened[below_r])
 
     def close(self):
         if self.handle:
             self.lib.wg_session_destroy(self.handle)
             self.handle = abi.vp()
+        for p in self._ipc_opened:
+            self.lib.wg_ipc_close(abi.vp(p))
+        self._ipc_opened = []
 
     def upload(self, host_grid: np.ndarray):
         self.lib.check(self.lib.wg_session_upload(self.handle, abi.dptr(host_grid)))
-        self._exchange()
+        self._initial_exchange()
 
     def init_device(self):
         """Initial state generated and compressed on the device (C4/C5)."""
         self.lib.check(self.lib.wg_session_init_device(self.handle))
-        self._exchange()
+        self._initial_exchange()
+
+    def _initial_exchange(self):
+        """After upload / init / load: the edges were rebuilt locally."""
+        if self.peer:
+            if self.dist is not None:
+                self.dist.barrier()  # every neighbour rebuilt its own edges first
+            self.peer_push()
+        else:
+            self._exchange()
 
     def _exchange(self):
-        if self.shard.world > 1:
+        if self.shard.world > 1 and not self.peer:
             s_lo, s_hi, r_lo, r_hi = self.halo_tensors()
             exchange_halos(s_lo, s_hi, r_lo, r_hi, self.shard.rank, self.shard.world, self.dist)
             if self.swe:
@@ -187,11 +243,11 @@ class ShardedSession:
     def load(self, path: str):
         """Resume from a checkpoint written by save() for the same shard."""
         self.lib.check(self.lib.wg_session_load(self.handle, str(path).encode()))
-        self._exchange()
+        self._initial_exchange()
 
     def step(self, dt: float = 1.0):
         self.lib.check(self.lib.wg_session_step(self.handle, dt))
-        self._exchange()  # the halo blocks move with the double buffer: re-fetched every step
+        self._exchange()  # the halo blocks move with the double buffer: re-fetched every step (host mode)
 
     def sync(self):
         self.lib.check(self.lib.wg_session_sync(self.handle))

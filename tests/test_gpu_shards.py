@@ -150,3 +150,82 @@ def test_swe_single_shard_session_matches_run(product, oracle_sq):
         assert np.array_equal(bits(la), bits(ref.grid.logical_view()))
     finally:
         one.close()
+
+
+class PeerShards(LocalShards):
+    """The same shards in peer halo mode: each session is attached to its
+    ring neighbours' edge allocations (plain device pointers here: one
+    process; CUDA IPC across processes), the step kernels store the halo
+    lines into the neighbours' halo slots themselves and the sessions
+    synchronise through the device flag words — no exchange between steps.
+    All shards run in order on one stream, so every device-side wait is
+    already satisfied when it is reached (no kernel waits on a kernel that
+    has not run)."""
+
+    def __init__(self, lib, cfg, world):
+        super().__init__(lib, cfg, world)
+        ex = [s.peer_export() for s in self.sessions]
+        for r, s in enumerate(self.sessions):
+            s.peer_attach(ex[(r - 1) % world], ex[(r + 1) % world])
+
+    def exchange(self):
+        pass  # the step kernels did it
+
+    def upload(self, grid: api.PatchGrid):
+        P1 = self.cfg.splits[1]
+        per = grid.data.size // grid.data.shape[0]
+        flat = grid.data.reshape(grid.data.shape[0], per)
+        self._keep = []
+        for s, (rb, re_) in zip(self.sessions, self.ranges):
+            part = np.ascontiguousarray(flat[rb * P1: re_ * P1]).reshape(-1)
+            self._keep.append(part)
+            self.lib.check(self.lib.wg_session_upload(s.handle, abi.dptr(part)))
+        for s in self.sessions:  # every shard built its own edges: now the halo rows
+            s.peer_push()
+
+
+@pytest.mark.parametrize(
+    "scheme,nx,splits,levels,c,world,steps,codec",
+    [("transport", 257, (8, 8), 4, 1e-3, 2, 6, "csr"),
+     ("transport", 257, (8, 8), 4, 1e-3, 3, 6, "csr"),   # uneven shards
+     ("lbm", 257, (8, 8), 4, 1e-3, 2, 5, "csr"),
+     ("lbm", 129, (4, 4), 4, 1e-3, 4, 5, "csr"),          # one patch row per shard
+     ("lbm", 129, (4, 4), 4, 1e-3, 2, 4, "lz")],
+)
+def test_peer_halos_equal_single(product, scheme, nx, splits, levels, c, world, steps, codec):
+    cfg = _cfg(scheme, nx, splits, levels, c, codec=codec)
+    g0 = api.initial_state(cfg, lib=product)
+    single = LocalShards(product, cfg, 1)
+    multi = PeerShards(product, cfg, world)
+    try:
+        single.upload(g0)
+        multi.upload(g0)
+        dt = cfg.cfl / (nx - 1) / 0.9
+        for _ in range(steps):
+            for s in single.sessions:
+                product.check(product.wg_session_step(s.handle, dt))
+            single.exchange()
+            for s in multi.sessions:
+                product.check(product.wg_session_step(s.handle, dt))
+        a, b = single.download(), multi.download()
+        for s in multi.sessions:
+            s.sync()  # device error word (a peer wait that timed out raises here)
+        assert np.array_equal(bits(a), bits(b)), f"{np.sum(a != b)} values differ"
+        r1, rn = single.rows()[0], multi.rows()
+        for k in range(steps):
+            for key in ("dense_bytes", "compressed_bytes", "nnz", "zeroed"):
+                assert r1[k][key] == sum(p[k][key] for p in rn), key
+    finally:
+        single.close()
+        multi.close()
+
+
+def test_peer_halos_reject_swe(product):
+    cfg = _cfg("swe", 129, (4, 4), 4, 5e-4, t_end=1.0)
+    two = LocalShards(product, cfg, 2)
+    try:
+        ex = [s.peer_export() for s in two.sessions]
+        with pytest.raises(ValueError):
+            two.sessions[0].peer_attach(ex[1], ex[1])
+    finally:
+        two.close()
