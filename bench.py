@@ -395,7 +395,8 @@ def bench_b200(args, w: dict):
         "compute_ceiling": compute_ceiling(lib, w, value / world),  # per GPU
         # one fused kernel launch per step (k_*_step<STEP>); Codec::lz adds the
         # LZ-size pass (k_lz_sizes, which also writes the step's row)
-        "gpu_launches": args.steps * (2 if w.get("codec") == "lz" else 1),
+        # (+ the device-side wait and signal of the peer halo mode)
+        "gpu_launches": args.steps * ((2 if w.get("codec") == "lz" else 1) + (2 if sess.peer else 0)),
         "clocks": clocks.summary(),
         "device_bytes": info.device_bytes,
         "device_mem_used_bytes": mem_used,
