@@ -53,3 +53,16 @@ def test_two_ranks_weak_scaling(workload):
     assert two["compression_ratio"] == pytest.approx(one["compression_ratio"], rel=1e-12)
     assert two["compressed_bytes_per_step"] == pytest.approx(2 * one["compressed_bytes_per_step"], rel=1e-12)
     assert two["mass_drift"] <= 1e-12
+
+
+@pytest.mark.parametrize("scheme", ["transport", "lbm"])
+def test_peer_halos_across_processes(scheme):
+    """Peer halo mode with real CUDA IPC between two processes (tests/peer_ipc_job.py)."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_port()), "tests/peer_ipc_job.py", scheme, "4"]
+    out = subprocess.run(cmd, cwd=REPO, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [x for x in out.stdout.splitlines() if x.startswith("{")]
+    assert len(lines) == 1, out.stdout
+    res = json.loads(lines[0])
+    assert res["peer"] and res["equal"], res
