@@ -41,6 +41,19 @@ struct SweLayout {
     static constexpr size_t scratch_doubles() { return (size_t)3 * N * N; }
 };
 
+// skip-rule patches (nothing zeroed, pipeline.hpp:243-249) keep a component
+// as CSR when its reconstruction equals the FV output bit for bit (and the
+// CSR block is at most 1/8 of the raw one, so a failed attempt stays inside
+// the pool's 1/8 slack): the flat regions of the dam
+// break then stay compressed instead of raw.  The stored state, metrics and
+// edges are identical either way (the next decode yields the same bits).
+// Measured at C3 (tools/ab_swe_exact.sh): DRAM 0.83 vs 1.90 GB per step, but
+// 5.21 vs 5.39 GLUPS (the flat CSR components now need inverse transforms in
+// a compute-bound kernel), so off by default; all GPU tests pass either way.
+#ifndef WG_SWE_EXACT_CSR
+#define WG_SWE_EXACT_CSR 0
+#endif
+
 #ifndef WG_SWE_MIN_BLOCKS
 #define WG_SWE_MIN_BLOCKS 2  // 2 CTAs per SM (spills in the lifting phases, +44% C3)
 #endif
@@ -55,6 +68,7 @@ __global__ void __launch_bounds__(SweLayout<N>::NT, WG_SWE_MIN_BLOCKS) k_swe_ste
     __shared__ uint64_t slot_off[3];
     __shared__ int slot_ok[3];
     __shared__ uint32_t comp_nnz[3];
+    __shared__ int slot_exact[3];
     __shared__ unsigned long long patch_bytes, patch_nnz, patch_zero;
     __shared__ ChunkState cs;
     __shared__ double wmax[NT / 32];
@@ -179,7 +193,10 @@ __global__ void __launch_bounds__(SweLayout<N>::NT, WG_SWE_MIN_BLOCKS) k_swe_ste
                 }
                 // skip rule decided before anything is written (pipeline.hpp:243)
                 for (int sl = 0; sl < 3; ++sl) {
-                    if (!cycle || patch_zero == 0) {
+                    slot_exact[sl] = 1;
+                    const bool exact_try = WG_SWE_EXACT_CSR && patch_zero == 0 &&
+                                           12ull * comp_nnz[sl] + 4ull * (N + 1) <= (uint64_t)NN;
+                    if (!cycle || (patch_zero == 0 && !exact_try)) {
                         slot_ok[sl] = 0;
                         continue;
                     }
@@ -207,8 +224,16 @@ __global__ void __launch_bounds__(SweLayout<N>::NT, WG_SWE_MIN_BLOCKS) k_swe_ste
             WG_PHASE_MARK(7);
             if (ok) {
                 decode_col<N, L>(T, li, false, v);
-                write_edges<N>(a.eout, pp, s, g, li, v);
-                if (s == 0) m += col_mass<N>(li, v);
+                if (!store_raw) {
+                    write_edges<N>(a.eout, pp, s, g, li, v);
+                    if (s == 0) m += col_mass<N>(li, v);
+                } else {  // skip rule: is the CSR form exact for this column?
+                    bool same = true;
+#pragma unroll
+                    for (int i = 0; i < N; ++i)
+                        same &= __double_as_longlong(v[i]) == __double_as_longlong(S[(size_t)s * NN + i * N + li]);
+                    if (!same) slot_exact[s] = 0;
+                }
             }
             __syncthreads();
             WG_PHASE_MARK(8);
@@ -231,6 +256,10 @@ __global__ void __launch_bounds__(SweLayout<N>::NT, WG_SWE_MIN_BLOCKS) k_swe_ste
         if (store_raw) {  // raw store of the FV output (skip rule / no_compression)
             if (t == 0) {
                 for (int sl = 0; sl < 3; ++sl) {
+                    if (a.compress && slot_ok[sl] && slot_exact[sl]) {  // exact CSR kept (its directory entry stands)
+                        slot_ok[sl] = 2;
+                        continue;
+                    }
                     const uint64_t off = chunk_alloc(a, cs, round16((uint64_t)NN * 8));
                     slot_ok[sl] = off != ~0ull;
                     slot_off[sl] = off;
@@ -243,7 +272,7 @@ __global__ void __launch_bounds__(SweLayout<N>::NT, WG_SWE_MIN_BLOCKS) k_swe_ste
                 double v[N];
 #pragma unroll
                 for (int i = 0; i < N; ++i) v[i] = S[(size_t)s * NN + i * N + li];
-                if (slot_ok[s]) {
+                if (slot_ok[s] == 1) {
                     double* d = reinterpret_cast<double*>(a.store_out + slot_off[s]);
 #pragma unroll
                     for (int i = 0; i < N; ++i) d[i * N + li] = v[i];
