@@ -22,14 +22,14 @@ struct KernelSet {
     bool edges3;             // D2Q9 edge lines hold only the 3 crossing populations
     bool decode_l2;          // decode with decode_out == nullptr runs the transport l2 pass
     void (*main_lz)(StepArgs) = nullptr;  // MODE_STEP_LZ (Codec::lz metrics); null if unsupported
+    int cluster = 1;                      // CTAs per patch (thread-block cluster size of every mode)
 };
 
 // Each returns false when (n, levels) has no instantiation.
 // small_grid: fewer patches than the CTAs of a full wave at the default
 // patches-per-CTA: one patch per CTA spreads them over more SMs
-bool select_transport_kernels(uint64_t n, int levels, bool half_lines, bool small_grid, KernelSet& out);  // kt_transport.cu
-bool select_lbm_kernels(uint64_t n, int levels, bool half_lines, KernelSet& out);        // kt_lbm.cu
-bool select_lbm_group_kernels(int levels, KernelSet& out);                              // kt_lbm_group.cu
+bool select_transport_kernels(uint64_t n, int levels, bool small_grid, KernelSet& out);  // kt_transport.cu
+bool select_lbm_kernels(uint64_t n, int levels, KernelSet& out);        // kt_lbm.cu
 bool select_swe_kernels(uint64_t n, int levels, KernelSet& out);                         // kt_swe*.cu
 bool select_swe65_kernels(int levels, KernelSet& out);                                  // kt_swe65.cu
 

@@ -15,6 +15,7 @@ inline void kt_set_smem(const KernelSet& k) {
 // Walk L = 0.. while 2^L <= N-1 (and L <= Lmax); Make<N, L>::make() builds the set.
 template <template <int, int> class Make, int N, int Lmax, int L = 0>
 bool pick_level(int levels, KernelSet& out) {
+    static_assert(L >= 0);
     if constexpr ((1 << L) <= N - 1 && L <= Lmax) {
         if (levels == L) {
             out = Make<N, L>::make();

@@ -1,6 +1,5 @@
-// kt_transport.cu — transport (1 component) step kernels: full-line
-// k_patch_step (P patches per CTA) and the opt-in half-line variant.
-#include "half_kernels.cuh"
+// kt_transport.cu — transport (1 component) step kernels: k_patch_step
+// (P patches per CTA).
 #include "kt_common.cuh"
 #include "patch_kernels.cuh"
 
@@ -30,25 +29,15 @@ struct FullT {
     };
 };
 
-template <int N, int L>
-struct HalfT {
-    static KernelSet make() {
-        using Lay = HLayout<N, 2>;
-        return KernelSet{k_patch_step_h<N, L, 2, MODE_STEP>, k_patch_step_h<N, L, 2, MODE_DECODE>, nullptr, 2,
-                         Lay::NT, Lay::smem_bytes(), false, 0, false, false};
-    }
-};
-
 }  // namespace
 
-bool select_transport_kernels(uint64_t n, int levels, bool half_lines, bool small_grid, KernelSet& k) {
+bool select_transport_kernels(uint64_t n, int levels, bool small_grid, KernelSet& k) {
     if (small_grid && n == 33) return pick_level<FullT<1>::M, 33, kMaxLevels>(levels, k);
     switch (n) {
         case 9: return pick_level<FullT<7>::M, 9, kMaxLevels>(levels, k);
         case 17: return pick_level<FullT<15>::M, 17, kMaxLevels>(levels, k);
         case 33: return pick_level<FullT<WG_T33_P>::M, 33, kMaxLevels>(levels, k);
-        case 65: return half_lines ? pick_level<HalfT, 65, 6>(levels, k)
-                                   : pick_level<FullT<WG_T65_P>::M, 65, kMaxLevels>(levels, k);
+        case 65: return pick_level<FullT<WG_T65_P>::M, 65, kMaxLevels>(levels, k);
         default: return false;
     }
 }

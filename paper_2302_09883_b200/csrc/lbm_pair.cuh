@@ -1,0 +1,857 @@
+// lbm_pair.cuh — the fused D2Q9 step: one patch per CTA PAIR (a 2-CTA
+// thread-block cluster), the whole uncompressed patch in shared memory.
+//
+// A 65^2 x 9 fp64 patch is 304 KB: more than one SM's shared memory, less
+// than two.  The pair splits it by population: rank 0 owns populations
+// 1..4, rank 1 owns 5..8, and both hold a replica of the rest population 0
+// (no streaming, no edges).  Every CTA therefore has 4 x 65 + 33 (or 32)
+// line jobs per pass — one per thread (10 warps) — and every phase except
+// the collide is CTA-local:
+//
+//   D0  wait for the patch's CSR blocks (cp.async.bulk into shared memory,
+//       issued while the previous patch was being processed; mbarrier)
+//   D1  decode rows: CSR scatter + inverse transform along dim 1 of the
+//       non-empty coefficient rows only (a row that decodes to nothing is
+//       never touched: the column pass reads it as +0.0 through a row mask)
+//   D2  decode columns: inverse transform along dim 0 from the masked rows
+//       (zero-detail levels skipped bit-exactly, lifting.cuh), ghost values
+//       from the neighbours' edge lines, pull streaming as a register shift
+//       -> the streamed population field in shared memory
+//   C   BGK collide of this CTA's column half of the patch: 9 populations per
+//       cell, the peer's 4 over distributed shared memory (DSMEM)
+//   F1  forward transform along dim 0 (columns), corner layout, in place
+//   F2  forward transform along dim 1 (rows) + threshold + nnz/zeroed counts
+//   S   CTA scan -> CSR row offsets; the pair exchanges its counts through
+//       a DSMEM mailbox (skip rule, pipeline.hpp:243-249, on the patch total)
+//   W   CSR rows written straight from registers; edge lines (the next
+//       step's ghost sources) by partial reconstruction: only the cones of
+//       logical rows/columns 1 and n-2 are inverse transformed; mass from the
+//       kept coefficients through the trapezoid functional of the inverse
+//       (details integrate to zero: the sample coefficients carry the mass)
+//
+// The reconstruction of the reference's compress cycle (insert_logical of
+// idwt_nd, pipeline.hpp:251-253) is not materialised: the next step decodes
+// the stored coefficients anyway, and the edge lines it needs are computed
+// bit-identically from the same lifting operations.  A patch whose cycle
+// zeroes nothing is re-derived (decode + collide again, deterministic) and
+// stored raw; its CSR blocks are never allocated.
+//
+// The D2Q9 scheme is NOT in the reference; its definition
+// is shared with oracle/ref_shim.cpp and oracle/wg_oracle.c.
+#pragma once
+
+#include <cooperative_groups.h>
+
+#include "patch_phases.cuh"
+
+namespace wg {
+
+namespace cg = cooperative_groups;
+
+// ---- PTX helpers: mbarrier, bulk async copy, cluster barriers ---------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect(unsigned long long* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WG_MBAR_WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WG_MBAR_WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+// global -> this CTA's shared memory, completion counted on bar (bytes and
+// both addresses 16-byte aligned)
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+// generic-proxy accesses of shared memory before later async-proxy writes
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void cluster_arrive() { asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory"); }
+__device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory"); }
+__device__ __forceinline__ void cluster_sync_all() {
+    cluster_arrive();
+    cluster_wait();
+}
+__device__ __forceinline__ unsigned cluster_rank() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+
+// ---- compile-time tables ----------------------------------------------------
+// 128-bit position set (N <= 65 < 128).
+struct Bits128 {
+    unsigned long long lo, hi;
+    __host__ __device__ constexpr bool has(int p) const { return p < 64 ? ((lo >> p) & 1ull) : ((hi >> (p - 64)) & 1ull); }
+    __host__ __device__ constexpr void set(int p) {
+        if (p < 64) lo |= 1ull << p;
+        else hi |= 1ull << (p - 64);
+    }
+};
+
+// Corner-layout positions of a line whose inverse transform feeds output
+// position `ii` (the dependency cone of idwt_line_reg, wavelet.hpp:118-130).
+template <int N, int L>
+__host__ __device__ constexpr Bits128 inverse_cone(int ii) {
+    Bits128 dep[N] = {};
+    for (int r = 0; r < N; ++r) dep[r].set(r);
+    for (int l = L; l >= 1; --l) {
+        const int s = 1 << (l - 1);
+        const int len = (N - 1) / s + 1;
+        const int half = (len - 1) / 2;
+        for (int k = 1; k < half; ++k) {
+            dep[2 * k * s].lo |= dep[(2 * k - 1) * s].lo | dep[(2 * k + 1) * s].lo;
+            dep[2 * k * s].hi |= dep[(2 * k - 1) * s].hi | dep[(2 * k + 1) * s].hi;
+        }
+        for (int k = 0; k < half; ++k) {
+            dep[(2 * k + 1) * s].lo |= dep[2 * k * s].lo | dep[(2 * k + 2) * s].lo;
+            dep[(2 * k + 1) * s].hi |= dep[2 * k * s].hi | dep[(2 * k + 2) * s].hi;
+        }
+    }
+    Bits128 out{};
+    for (int r = 0; r < N; ++r)
+        if (dep[ii].has(r)) out.set(corner_pos<N, L>(r));
+    return out;
+}
+
+// Output position II of the inverse line transform of a register line
+// (only the dependency cone of II survives dead-code elimination).
+template <int N, int L, int II>
+__device__ __forceinline__ double idwt_at(const double (&x)[N]) {
+    double y[N];
+#pragma unroll
+    for (int r = 0; r < N; ++r) y[r] = x[r];
+    idwt_line_reg<N, L>(y);
+    return y[II];
+}
+
+// Streamed column (pull streaming along dim 0: out[i] = v[i - cx], the
+// ghost value at the row that enters) stored with element stride S.
+template <int N, int S>
+__device__ __forceinline__ void store_streamed(double* dst, const double (&v)[N], int cx, double ghost) {
+    if (cx == 0) {
+#pragma unroll
+        for (int i = 0; i < N; ++i) dst[i * S] = v[i];
+    } else if (cx == 1) {
+        dst[0] = ghost;
+#pragma unroll
+        for (int i = 1; i < N; ++i) dst[i * S] = v[i - 1];
+    } else {
+#pragma unroll
+        for (int i = 0; i < N - 1; ++i) dst[i * S] = v[i + 1];
+        dst[(N - 1) * S] = ghost;
+    }
+}
+
+template <int N>
+struct PairLayout {
+    static constexpr int H0 = (N + 1) / 2;        // rank 0's half of population 0 (columns / rows)
+    static constexpr int JOBS = 4 * N + H0;       // line jobs of rank 0 (rank 1: one fewer)
+    static constexpr int NT = ((JOBS + 31) / 32) * 32;
+    static constexpr int NN = N * N;
+    static constexpr int BUFD = (NN + 1) & ~1;    // doubles per population buffer (16-byte multiple)
+    static constexpr int NBUF = 5;                // slot 0: population 0 replica, slots 1..4: own populations
+    static constexpr size_t kSmemMax = 232448;    // 227 KB per CTA (sm_100)
+    static constexpr size_t kStatic = 2048;       // static shared memory of the kernel (bound)
+    // + the scan array, the column-edge partials of the 4 own populations and
+    // the per-thread mass accumulators
+    static constexpr size_t fixed_bytes() {
+        return sizeof(double) * (size_t)NBUF * BUFD + 8ull * NT + sizeof(double) * 4 * (size_t)N +
+               sizeof(double) * 2 * (size_t)NT;
+    }
+    static constexpr size_t stage_bytes() {
+        const size_t room = kSmemMax - kStatic - fixed_bytes();
+        const size_t want = (size_t)5 * (12 * NN + 4 * (N + 1) + 16);  // every block dense-CSR
+        return ((want < room ? want : room) / 16) * 16;
+    }
+    static constexpr size_t smem_bytes() { return fixed_bytes() + stage_bytes(); }
+};
+
+enum : uint32_t { IN_CSR = 0, IN_RAW = 1, IN_DEAD = 2 };
+
+// Where a slot's input block of the current patch lives.
+struct SlotIn {
+    const double* v;         // CSR values (staged copy or global)
+    const uint32_t* col;
+    const uint32_t* ro;
+    const double* gv;        // the same block in global memory (re-derivation after the skip rule)
+    const uint32_t* gcol;
+    const uint32_t* gro;
+    const double* raw;       // IN_RAW: dense N x N block in global memory
+    uint32_t nnz, kind;
+};
+
+__host__ __device__ constexpr int pair_pop(int rank, int s) { return s == 0 ? 0 : (rank == 0 ? s : s + 4); }
+
+// ---- the kernel -------------------------------------------------------------
+template <int N, int L, int MODE>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<N>::NT, 1)
+    k_lbm_pair(const __grid_constant__ StepArgs a) {
+    using Lay = PairLayout<N>;
+    constexpr int NT = Lay::NT, NN = N * N, BUFD = Lay::BUFD, H0 = Lay::H0;
+    constexpr size_t STAGE = Lay::stage_bytes();
+    constexpr Bits128 CONE_LO = inverse_cone<N, L>(1), CONE_HI = inverse_cone<N, L>(N - 2);
+
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    double* bufs = reinterpret_cast<double*>(smem_raw);
+    unsigned long long* inc = reinterpret_cast<unsigned long long*>(bufs + Lay::NBUF * BUFD);
+    double* side = reinterpret_cast<double*>(inc + NT);  // [4][N] column-edge partials Y[r][1 or N-2]
+    double* acc_m = side + 4 * N;                // per-thread mass of the reconstruction
+    double* acc_f = acc_m + NT;                  // per-thread mass of the collided state
+    unsigned char* stage = reinterpret_cast<unsigned char*>(acc_f + NT);
+
+    __shared__ __align__(8) unsigned long long mbar;
+    __shared__ SlotIn slot_in[2][5];
+    __shared__ Bits128 rmask[5];               // non-empty coefficient rows per slot
+    __shared__ unsigned long long mail_tot[5];  // peer's per-slot (zeroed << 32 | nnz) totals
+    __shared__ unsigned long long mail_off0;    // population 0 block offset (rank 0 -> rank 1)
+    __shared__ int mail_ok0;
+    __shared__ unsigned long long slot_tot[5];
+    __shared__ uint64_t slot_off[5];
+    __shared__ int slot_ok[5];
+    __shared__ uint32_t slot_nnz[5];            // nnz of the block a slot writes into
+    __shared__ uint32_t slot_k0[5];             // entry offset of this CTA's rows inside the block
+    __shared__ int slot_top[5];                 // highest row holding a kept coefficient (-1: none)
+    __shared__ ChunkState cs;
+    __shared__ int skip_patch;
+    __shared__ PatchPos ppos;
+    __shared__ StepPartial part;                // this CTA's step sums (thread 0)
+    __shared__ uint32_t cur_p;                  // the patch in flight (state lives in shared
+    __shared__ int cur_it, cur_redo, cur_raw;   // memory: short register live ranges)
+    __shared__ double red_m[NT / 32], red_f[NT / 32];
+
+    const int t = threadIdx.x;
+    const ShardGeom& g = a.g;
+    const uint32_t npairs = gridDim.x / 2, pair = blockIdx.x / 2;
+
+    // thread -> line job: own slot s (1..4) line li, or population 0 (slot 0) line li of this CTA's half
+    struct Job {
+        int s, li, q, cx, cy;
+        bool on;
+    };
+    auto job_of = [&]() {
+        const unsigned rank = cluster_rank();
+        const int H = rank == 0 ? H0 : N - H0, lo = rank == 0 ? 0 : H0;
+        Job jb{0, 0, 0, 0, 0, false};
+        if (t < 4 * N) {
+            jb.s = 1 + t / N;
+            jb.li = t - (jb.s - 1) * N;
+            jb.on = true;
+        } else if (t < 4 * N + H) {
+            jb.li = lo + (t - 4 * N);
+            jb.on = true;
+        }
+        jb.q = pair_pop((int)rank, jb.s);
+        jb.cx = lbm_cx(jb.q);
+        jb.cy = lbm_cy(jb.q);
+        return jb;
+    };
+    auto jb_on_d2 = [&]() { return t < 4 * N + (cluster_rank() == 0 ? H0 : N - H0); };
+    auto half_lo = [&]() { return cluster_rank() == 0 ? 0 : H0; };
+    auto half_n = [&]() { return cluster_rank() == 0 ? H0 : N - H0; };
+    auto peer_of = [&]() { return cluster_rank() ^ 1u; };
+
+    // ---- input prefetch of patch p into descriptor set `par` (thread 0) ----
+    auto prefetch = [&](uint32_t p, int par) {
+        const int rank = (int)cluster_rank();
+        unsigned used = 0;
+        for (int sl = 0; sl < 5; ++sl) {
+            const int qq = pair_pop(rank, sl);
+            SlotIn d{};
+            DirEntry e{0, 0u, DIR_DEAD};
+            if (MODE != MODE_INIT) e = a.dir_in[(size_t)p * 9 + qq];
+            if (e.flags & DIR_DEAD) {
+                d.kind = IN_DEAD;
+            } else if (e.flags & DIR_RAW) {
+                d.kind = IN_RAW;
+                d.raw = reinterpret_cast<const double*>(a.store_in + e.off);
+            } else {
+                d.kind = IN_CSR;
+                d.nnz = e.nnz;
+                const unsigned char* gb = a.store_in + e.off;
+                d.gv = reinterpret_cast<const double*>(gb);
+                d.gcol = reinterpret_cast<const uint32_t*>(gb + 8ull * e.nnz);
+                d.gro = d.gcol + e.nnz;
+                const unsigned bytes = (unsigned)round16(12ull * e.nnz + 4ull * (N + 1));
+                if (used + bytes <= STAGE) {
+                    unsigned char* sb = stage + used;
+                    bulk_g2s(sb, gb, bytes, &mbar);
+                    used += bytes;
+                    d.v = reinterpret_cast<const double*>(sb);
+                    d.col = reinterpret_cast<const uint32_t*>(sb + 8ull * e.nnz);
+                    d.ro = d.col + e.nnz;
+                } else {  // does not fit the staging area: decoded from global memory
+                    d.v = d.gv;
+                    d.col = d.gcol;
+                    d.ro = d.gro;
+                }
+            }
+            slot_in[par][sl] = d;
+        }
+        mbar_arrive_expect(&mbar, used);
+    };
+
+    if (t == 0) {
+        mbar_init(&mbar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        cs.cur = cs.end = 0;
+        part = StepPartial{0, 0, 0, 0.0, 0.0, 0.0};
+    }
+    __syncthreads();
+    cluster_sync_all();  // the peer CTA runs before any DSMEM access
+    if (t == 0 && pair < g.npatch) prefetch(pair, 0);
+
+    unsigned phase = 0;
+    if (t == 0) {
+        cur_p = pair;
+        cur_it = 0;
+    }
+    __syncthreads();
+    for (;;) {
+        if (cur_p >= g.npatch) break;
+        // D0: inputs arrived; row masks of the stored blocks
+        mbar_wait(&mbar, phase);
+        phase ^= 1u;
+        if (t < 5) {
+            rmask[t] = Bits128{0ull, 0ull};
+            slot_top[t] = -1;
+        }
+        if (t == 0) {
+            ppos = patch_pos(cur_p, g);
+            cur_redo = 0;
+            cur_raw = 0;
+        }
+        acc_m[t] = 0.0;
+        acc_f[t] = 0.0;
+        __syncthreads();
+        WG_PHASE_MARK(-1);
+        const int par = cur_it & 1;
+        if (MODE != MODE_INIT) {
+            for (int k = t; k < 5 * N; k += NT) {
+                const int sl = k / N, r = k - sl * N;
+                const SlotIn& d = slot_in[par][sl];
+                const bool ne = d.kind == IN_CSR ? d.ro[r + 1] > d.ro[r] : d.kind == IN_RAW;
+                if (ne) {
+                    if (r < 64) atomicOr(&rmask[sl].lo, 1ull << r);
+                    else atomicOr(&rmask[sl].hi, 1ull << (r - 64));
+                }
+            }
+        }
+        __syncthreads();
+
+        // produce the post-collide state (D1, D2, C); pass 1 re-derives the
+        // state of a skip-rule patch after the transform overwrote it
+        for (;;) {
+            const int par = cur_it & 1;
+            if constexpr (MODE == MODE_INIT) {
+                // initial state generated on the device (CUDA libm, not bit-pinned
+                // to the host IC) for grids whose raw state exceeds the store
+                // budget; own populations fully, population 0 on the own half
+                const int N1 = N - 1, rank = (int)cluster_rank(), lo = half_lo(), H = half_n();
+                const PatchPos pp = ppos;
+                for (int c = t; c < NN; c += NT) {
+                    const int i = c / N, jj = c - i * N;
+                    const uint64_t gi = ((uint64_t)(g.row0 + pp.ar) * N1 + i) % a.ic_period,
+                                   gj = (uint64_t)pp.b * N1 + jj;
+                    const double X = (double)gi * a.ic_inv, Y = (double)gj * a.ic_inv;
+                    const double uy = X <= 0.5 ? a.ic_u0 * tanh(a.ic_kappa * (X - 0.25))
+                                               : a.ic_u0 * tanh(a.ic_kappa * (0.75 - X));
+                    const double ux = a.ic_delta * a.ic_u0 * sin(2.0 * 3.141592653589793 * (Y + 0.25));
+                    const double usq = ux * ux + uy * uy;
+#pragma unroll
+                    for (int sl = 0; sl < 5; ++sl) {
+                        const int qq = pair_pop(rank, sl);
+                        if (sl == 0 && (jj < lo || jj >= lo + H)) continue;
+                        bufs[(size_t)sl * BUFD + c] = lbm_feq(qq, 1.0, lbm_cu(qq, ux, uy), usq);
+                    }
+                }
+                __syncthreads();
+                if (t == 0 && !cur_redo && cur_p + npairs < g.npatch) prefetch(cur_p + npairs, par ^ 1);
+                cluster_sync_all();
+            } else {
+                // D1: decode rows (own slots: row li; population 0: every row,
+
+                // strided).  The pull-streaming shift along dim 1 commutes with
+                // the column transforms, so it is applied here: row r is stored
+                // shifted by cy (B[r][j] = Y[r][j - cy]) and every column thread
+                // of D2 then reads and writes only its own column.
+                {
+                    const Job jb = job_of();
+                    const bool redo = cur_redo != 0;
+                    auto decode_row = [&](double* Bs, const SlotIn& d, int r, int cy) {
+                        if (d.kind != IN_CSR) return;
+                        const double* vv = redo ? d.gv : d.v;
+                        const uint32_t* cc = redo ? d.gcol : d.col;
+                        const uint32_t* ro = redo ? d.gro : d.ro;
+                        const uint32_t k0 = ro[r], k1 = ro[r + 1];
+                        if (k0 == k1) return;
+                        WG_CHECK(k1 <= d.nnz && k0 < k1, 1);
+                        double* rowp = Bs + (size_t)r * N;
+                        const int z = z_of_top(N, L, (int)cc[k1 - 1]);
+                        const int top = z_top(N, z);
+                        for (int jj = 0; jj <= top; ++jj) rowp[jj] = 0.0;
+                        for (uint32_t k = k0; k < k1; ++k) {
+                            WG_CHECK(cc[k] < (uint32_t)N, 2);
+                            rowp[cc[k]] = vv[k];
+                        }
+                        with_z<L>(z, [&](auto ZC) {
+                            constexpr int Z = decltype(ZC)::value;
+                            double x[N];
+#pragma unroll
+                            for (int rr = 0; rr < N; ++rr)
+                                x[rr] = corner_pos<N, L>(rr) <= z_top(N, Z) ? rowp[corner_pos<N, L>(rr)] : 0.0;
+                            idwt_line_reg<N, L, Z>(x);
+                            store_streamed<N, 1>(rowp, x, (MODE == MODE_DECODE) ? 0 : cy, 0.0);
+                        });
+                    };
+                    if (jb.on) {
+                        double* Bs = bufs + (size_t)jb.s * BUFD;
+                        if (jb.s > 0) decode_row(Bs, slot_in[par][jb.s], jb.li, jb.cy);
+                        else
+                            for (int r = t - 4 * N; r < N; r += half_n()) decode_row(Bs, slot_in[par][0], r, 0);
+                    }
+                }
+                __syncthreads();
+                WG_PHASE_MARK(21);
+                // next patch's inputs: the staging area is free once D1 has run
+                // (the skip rule's re-derivation reads the global copies)
+                if (t == 0 && !cur_redo && cur_p + npairs < g.npatch) {
+                    fence_proxy_async();
+                    prefetch(cur_p + npairs, par ^ 1);
+                }
+                // D2: decode columns, ghosts, pull streaming along dim 0 (a
+                // register shift), or the MODE_DECODE output.  Thread j owns
+                // column j (already shifted along dim 1 by D1); the column that
+                // streams in from outside (jc = j - cy off the patch) is the
+                // neighbour's edge line.
+                if (jb_on_d2()) {
+                    const Job jb = job_of();
+                    const int j = jb.li, cx = jb.cx, cy = jb.cy, q = jb.q;
+                    double* const Bs = bufs + (size_t)jb.s * BUFD;
+                    const int jc = (MODE == MODE_DECODE) ? j : j - cy;
+                    const SlotIn& d = slot_in[par][jb.s];
+                    const PatchPos pp = ppos;
+                    double ghost = 0.0;
+                    if (MODE != MODE_DECODE && cx != 0) {
+                        // ghost value of the streamed-in row: L(-1, jc) (cx = +1) or L(N, jc) (cx = -1)
+                        const uint32_t bcol = jc < 0 ? pp.bl : (jc >= N ? pp.br : pp.b);
+                        const int pos = jc < 0 ? N - 2 : (jc >= N ? 1 : jc);
+                        ghost = cx == 1 ? a.ein.rowhi[edge_ix(pp.su, bcol, lbm_slot_rowhi(q), g, N) + pos]
+                                        : a.ein.rowlo[edge_ix(pp.sd, bcol, lbm_slot_rowlo(q), g, N) + pos];
+                    }
+                    auto emit = [&](const double (&v)[N]) {
+                        if (MODE == MODE_DECODE) {
+                            constexpr int TP = N + 2;
+                            double* out = a.decode_out + ((size_t)cur_p * 9 + q) * (size_t)TP * TP + TP + 1 + j;
+#pragma unroll
+                            for (int i = 0; i < N; ++i) out[i * TP] = v[i];
+                        } else {
+                            store_streamed<N, N>(Bs + j, v, cx, ghost);
+                        }
+                    };
+                    double v[N];
+                    if (jc < 0 || jc >= N) {  // a ghost column: the neighbour's edge line
+                        const double* gl = jc < 0 ? a.ein.colhi + edge_ix(pp.ar, pp.bl, lbm_slot_colhi(q), g, N)
+                                                  : a.ein.collo + edge_ix(pp.ar, pp.br, lbm_slot_collo(q), g, N);
+#pragma unroll
+                        for (int i = 0; i < N; ++i) v[i] = gl[i];
+                        emit(v);
+                    } else if (d.kind == IN_RAW) {
+#pragma unroll
+                        for (int i = 0; i < N; ++i) v[i] = d.raw[(size_t)i * N + jc];
+                        emit(v);
+                    } else if (d.kind == IN_DEAD) {
+#pragma unroll
+                        for (int i = 0; i < N; ++i) v[i] = 0.0;
+                        emit(v);
+                    } else {
+                        const Bits128 m = rmask[jb.s];
+                        int top = -1;
+                        if (m.hi) top = 64 + 63 - __clzll((long long)m.hi);
+                        else if (m.lo) top = 63 - __clzll((long long)m.lo);
+                        with_z<L>(z_of_top(N, L, top), [&](auto ZC) {
+                            constexpr int Z = decltype(ZC)::value;
+#pragma unroll
+                            for (int rr = 0; rr < N; ++rr) {
+                                const int cp = corner_pos<N, L>(rr);
+                                v[rr] = (cp <= z_top(N, Z) && m.has(cp)) ? Bs[(size_t)cp * N + j] : 0.0;
+                            }
+                            idwt_line_reg<N, L, Z>(v);
+                            emit(v);
+                        });
+                    }
+                }
+                if (MODE == MODE_DECODE) break;
+                __syncthreads();
+                WG_PHASE_MARK(22);
+                cluster_sync_all();  // both halves streamed
+                WG_PHASE_MARK(23);
+                // C: BGK collide of this CTA's column half (lbm_collide, physics.cuh)
+                {
+                    const unsigned rank = cluster_rank(), peer = rank ^ 1u;
+                    cg::cluster_group cluster = cg::this_cluster();
+                    const int lo = half_lo(), H = half_n();
+                    double* P[9];  // population pointers (the peer's populations through DSMEM)
+#pragma unroll
+                    for (int k = 0; k < 9; ++k) {
+                        const bool mine = k == 0 || (rank == 0 ? (k >= 1 && k <= 4) : (k >= 5));
+                        const int sl = k == 0 ? 0 : (k <= 4 ? k : k - 4);
+                        P[k] = mine ? bufs + (size_t)sl * BUFD : cluster.map_shared_rank(bufs + (size_t)sl * BUFD, peer);
+                    }
+                    constexpr int K = 2;
+                    const int cells = N * H;
+                    const bool redo = cur_redo != 0;
+                    double mfv = 0.0;
+                    for (int c0 = t; c0 < cells; c0 += K * NT) {
+                        double f[K][9];
+                        int o[K];
+                        double w[K];
+#pragma unroll
+                        for (int u = 0; u < K; ++u) {
+                            const int c = c0 + u * NT;
+                            const int cc = c < cells ? c : c0;
+                            const int i = cc / H, jj = lo + (cc - i * H);
+                            o[u] = i * N + jj;
+                            w[u] = ((i == 0 || i == N - 1) ? 0.5 : 1.0) * ((jj == 0 || jj == N - 1) ? 0.5 : 1.0);
+#pragma unroll
+                            for (int k = 0; k < 9; ++k) f[u][k] = P[k][o[u]];
+                        }
+#pragma unroll
+                        for (int u = 0; u < K; ++u) lbm_collide(f[u], a.omega);
+#pragma unroll
+                        for (int u = 0; u < K; ++u) {
+                            if (c0 + u * NT < cells) {
+#pragma unroll
+                                for (int k = 0; k < 9; ++k) {
+                                    P[k][o[u]] = f[u][k];
+                                    if (!redo) mfv += w[u] * f[u][k];
+                                }
+                            }
+                        }
+                    }
+                    acc_f[t] += mfv;
+                }
+                WG_PHASE_MARK(24);
+                cluster_sync_all();  // the peer's populations are written back
+                WG_PHASE_MARK(25);
+            }
+            if (cur_redo || !a.compress) {  // the collided state, to be stored raw
+                if (t == 0) cur_raw = 1;
+                break;
+            }
+
+            // F1: forward transform along dim 0 (columns), corner layout, in place;
+            // population 0's column half also into the peer's replica
+            {
+                const Job jb = job_of();
+                if (jb.on) {
+                    double* const Bs = bufs + (size_t)jb.s * BUFD;
+                    const int j = jb.li;
+                    double x[N];
+#pragma unroll
+                    for (int i = 0; i < N; ++i) x[i] = Bs[(size_t)i * N + j];
+                    dwt_line_reg<N, L>(x);
+#pragma unroll
+                    for (int rr = 0; rr < N; ++rr) Bs[(size_t)corner_pos<N, L>(rr) * N + j] = x[rr];
+                    if (jb.s == 0) {
+                        cg::cluster_group cluster = cg::this_cluster();
+                        double* const Bpeer0 = cluster.map_shared_rank(bufs, peer_of());
+#pragma unroll
+                        for (int rr = 0; rr < N; ++rr) Bpeer0[(size_t)corner_pos<N, L>(rr) * N + j] = x[rr];
+                    }
+                }
+            }
+            cluster_sync_all();  // population 0's replicas hold both column halves
+            WG_PHASE_MARK(26);
+            // F2: forward transform along dim 1 (rows) + threshold (threshold.hpp:51-86);
+            // the thresholded row is parked in its own buffer row across the barriers
+            unsigned long long cnt = 0;  // zeroed << 32 | nnz of this row
+            {
+                const Job jb = job_of();
+                if (jb.on) {
+                    double* const rowp = bufs + (size_t)jb.s * BUFD + (size_t)jb.li * N;
+                    const int r = jb.li;
+                    double x[N];
+#pragma unroll
+                    for (int jj = 0; jj < N; ++jj) x[jj] = rowp[jj];
+                    dwt_line_reg<N, L>(x);
+                    const int bi = band_of_pos(N, L, r);
+                    double trow[L + 1];
+#pragma unroll
+                    for (int bj = 0; bj <= L; ++bj) trow[bj] = a.thr[bi * (L + 1) + bj];
+                    if (MODE == MODE_STEP_LZ) {  // apply_threshold's output (-0.0 kept) for the LZ sizes
+                        double* lz = a.lz_dense + ((size_t)cur_p * 9 + jb.q) * NN + (size_t)r * N;
+#pragma unroll
+                        for (int rr = 0; rr < N; ++rr) {
+                            const double y = x[rr];
+                            lz[corner_pos<N, L>(rr)] = (y != 0.0 && fabs(y) < trow[band_of_r<N, L>(rr)]) ? 0.0 : y;
+                        }
+                    }
+                    // kept / zeroed flags as bit masks (one predicated OR each), counted by popc
+                    unsigned long long km[2] = {0ull, 0ull}, zm[2] = {0ull, 0ull};
+#pragma unroll
+                    for (int rr = 0; rr < N; ++rr) {
+                        const double y = x[rr];
+                        const bool nzx = y != 0.0;
+                        const bool kill = fabs(y) < trow[band_of_r<N, L>(rr)];
+                        const bool keep = nzx && !kill;
+                        if (keep) km[rr >> 6] |= 1ull << (rr & 63);
+                        if (nzx && kill) zm[rr >> 6] |= 1ull << (rr & 63);
+                        x[rr] = keep ? y : 0.0;
+                    }
+                    const unsigned nz = (unsigned)(__popcll(km[0]) + __popcll(km[1]));
+                    const unsigned zr = (unsigned)(__popcll(zm[0]) + __popcll(zm[1]));
+                    if (nz) atomicMax(&slot_top[jb.s], r);
+                    // mass of the reconstruction: sum_rc a_r a_c C[r][c] (trapezoid
+                    // functional of idwt_nd, host-computed exact dyadic values; for
+                    // conservative levels only the samples carry mass)
+                    const double ar = a.mass_a[r];
+                    if (ar != 0.0 && nz) {
+                        double acc = 0.0;
+#pragma unroll
+                        for (int rr = 0; rr < N; ++rr) acc += x[rr] * a.mass_a[corner_pos<N, L>(rr)];
+                        acc_m[t] = ar * acc;
+                    }
+                    // column edge line of the reconstruction (own populations):
+                    // Y[r][jj] = row inverse at jj = 1 (cy = -1) or N-2 (cy = +1)
+                    if (jb.s > 0 && jb.cy != 0) {
+                        double val = 0.0;
+                        if (nz) val = jb.cy == -1 ? idwt_at<N, L, 1>(x) : idwt_at<N, L, N - 2>(x);
+                        side[(size_t)(jb.s - 1) * N + r] = val;
+                    }
+#pragma unroll
+                    for (int rr = 0; rr < N; ++rr) rowp[rr] = x[rr];  // interleaved order
+                    cnt = ((unsigned long long)zr << 32) | nz;
+                }
+            }
+            WG_PHASE_MARK(27);
+            // S: CTA scan of the counts in job order, per-slot totals, mailbox
+            cta_inclusive_scan<NT>(cnt, inc);
+            if (t < 5) {
+                const int first = t == 0 ? 4 * N : (t - 1) * N;
+                const int n = t == 0 ? half_n() : N;
+                const unsigned long long before = first == 0 ? 0ull : inc[first - 1];
+                slot_tot[t] = inc[first + n - 1] - before;
+                cg::cluster_group cluster = cg::this_cluster();
+                cluster.map_shared_rank(mail_tot, peer_of())[t] = slot_tot[t];
+            }
+            cluster_sync_all();  // M1: the pair's counts exchanged
+            WG_PHASE_MARK(28);
+            const bool cycle = a.thr_any != 0;
+            if (t == 0) {
+                const unsigned rank = cluster_rank();
+                unsigned long long zero = 0, nnz_m = 0, zr_m = 0;
+                for (int sl = 0; sl < 5; ++sl) {
+                    zero += (slot_tot[sl] >> 32) + (mail_tot[sl] >> 32);
+                    nnz_m += slot_tot[sl] & 0xffffffffull;
+                    zr_m += slot_tot[sl] >> 32;
+                }
+                // bytes: 12 nnz of the own rows + the row offsets of the blocks
+                // this CTA allocates (population 0's by rank 0)
+                part.comp_bytes += 12ull * nnz_m + 4ull * (N + 1) * (rank == 0 ? 5 : 4);
+                part.nnz += nnz_m;
+                part.zeroed += zr_m;
+                skip_patch = (zero == 0) || !cycle;
+                if (!skip_patch) {
+                    for (int sl = (rank == 0 ? 0 : 1); sl < 5; ++sl) {
+                        const int qq = pair_pop((int)rank, sl);
+                        const uint32_t bnnz = (uint32_t)(slot_tot[sl] & 0xffffffffull) +
+                                              (sl == 0 ? (uint32_t)(mail_tot[0] & 0xffffffffull) : 0u);
+                        const uint64_t off = chunk_alloc(a, cs, round16(12ull * bnnz + 4ull * (N + 1)));
+                        slot_ok[sl] = off != ~0ull;
+                        slot_off[sl] = off;
+                        slot_nnz[sl] = bnnz;
+                        slot_k0[sl] = 0;
+                        a.dir_out[(size_t)cur_p * 9 + qq] = slot_ok[sl] ? DirEntry{off, bnnz, 0u} : DirEntry{0, 0u, DIR_DEAD};
+                    }
+                    cg::cluster_group cluster = cg::this_cluster();
+                    if (rank == 0) {
+                        *cluster.map_shared_rank(&mail_off0, peer_of()) = slot_off[0];
+                        *cluster.map_shared_rank(&mail_ok0, peer_of()) = slot_ok[0];
+                    } else {  // population 0: rank 0's rows come first in the block
+                        slot_nnz[0] = (uint32_t)(slot_tot[0] & 0xffffffffull) + (uint32_t)(mail_tot[0] & 0xffffffffull);
+                        slot_k0[0] = (uint32_t)(mail_tot[0] & 0xffffffffull);
+                    }
+                }
+            }
+            cluster_sync_all();  // M2: population 0's block offset delivered
+            WG_PHASE_MARK(29);
+            if (t == 0 && cluster_rank() == 1 && !skip_patch) {
+                slot_off[0] = mail_off0;
+                slot_ok[0] = mail_ok0;
+            }
+            __syncthreads();
+            if (!skip_patch) {
+                // W: CSR rows (csr_encode, codec.hpp:37-60) from the parked rows;
+                // the cone rows of the row edge line are inverse transformed in
+                // place (a thread only touches its own parked row)
+                const Job jb = job_of();
+                if (jb.on) {
+                    double* const rowp = bufs + (size_t)jb.s * BUFD + (size_t)jb.li * N;
+                    const int r = jb.li, s = jb.s;
+                    double x[N];
+#pragma unroll
+                    for (int rr = 0; rr < N; ++rr) x[rr] = rowp[rr];
+                    const unsigned nz = (unsigned)(cnt & 0xffffffffull);
+                    if (slot_ok[s]) {
+                        const int first = s == 0 ? 4 * N : (s - 1) * N;
+                        const unsigned long long before = first == 0 ? 0ull : inc[first - 1];
+                        const uint32_t k = (uint32_t)((inc[t] - before) & 0xffffffffull) - nz + slot_k0[s];
+                        WG_CHECK(slot_off[s] + 12ull * slot_nnz[s] + 4ull * (N + 1) <= a.cap_out &&
+                                     k + nz <= slot_nnz[s], 10);
+                        write_csr_row<N, L>(a.store_out + slot_off[s], slot_nnz[s], r, k, nz, x);
+                    }
+                    if (s > 0 && jb.cx != 0 && nz && (jb.cx == -1 ? CONE_LO : CONE_HI).has(r)) {
+                        idwt_line_reg<N, L>(x);
+#pragma unroll
+                        for (int jj = 0; jj < N; ++jj) rowp[jj] = x[jj];  // natural order: Y[r][.]
+                    }
+                }
+                __syncthreads();
+                WG_PHASE_MARK(30);
+                if (jb.on && jb.s > 0) {
+                    double* const Bs = bufs + (size_t)jb.s * BUFD;
+                    const int j = jb.li, cx = jb.cx, cy = jb.cy, q = jb.q;
+                    const PatchPos pp = ppos;
+                    if (cx != 0) {  // row line: column j of the cone rows, inverse at 1 / N-2
+                        double y[N];
+                        if (cx == -1) {
+#pragma unroll
+                            for (int rr = 0; rr < N; ++rr) {
+                                const int cp = corner_pos<N, L>(rr);
+                                y[rr] = CONE_LO.has(cp) ? Bs[(size_t)cp * N + j] : 0.0;
+                            }
+                            put_rowlo(a.eout, g, (uint32_t)(pp.ar + 1), pp.b, lbm_slot_rowlo(q), N, j,
+                                      idwt_at<N, L, 1>(y));
+                        } else {
+#pragma unroll
+                            for (int rr = 0; rr < N; ++rr) {
+                                const int cp = corner_pos<N, L>(rr);
+                                y[rr] = CONE_HI.has(cp) ? Bs[(size_t)cp * N + j] : 0.0;
+                            }
+                            put_rowhi(a.eout, g, (uint32_t)(pp.ar + 1), pp.b, lbm_slot_rowhi(q), N, j,
+                                      idwt_at<N, L, N - 2>(y));
+                        }
+                    }
+                    if (cy != 0 && j == 0) {  // column line: the column inverse of the partials
+                        // rows without kept coefficients hold +0.0 partials: the
+                        // zero-detail inverse variant of the top row applies
+                        double* dst = cy == -1 ? a.eout.collo + edge_ix((uint32_t)pp.ar, pp.b, lbm_slot_collo(q), g, N)
+                                               : a.eout.colhi + edge_ix((uint32_t)pp.ar, pp.b, lbm_slot_colhi(q), g, N);
+                        const double* src = side + (size_t)(jb.s - 1) * N;
+                        with_z<L>(z_of_top(N, L, slot_top[jb.s]), [&](auto ZC) {
+                            constexpr int Z = decltype(ZC)::value;
+                            double y[N];
+#pragma unroll
+                            for (int rr = 0; rr < N; ++rr)
+                                y[rr] = corner_pos<N, L>(rr) <= z_top(N, Z) ? src[corner_pos<N, L>(rr)] : 0.0;
+                            idwt_line_reg<N, L, Z>(y);
+#pragma unroll
+                            for (int i = 0; i < N; ++i) dst[i] = y[i];
+                        });
+                    }
+                }
+                break;
+            }
+            if (t == 0) cur_redo = 1;  // skip rule: the buffers hold the transform, re-derive the state
+            __syncthreads();
+        }
+        __syncthreads();  // cur_raw visible to every thread
+        if (MODE != MODE_DECODE && cur_raw) {
+            // skip rule / no compression: the collided state itself, stored raw
+            const unsigned rank = cluster_rank();
+            if (t == 0) {
+                for (int sl = (rank == 0 ? 0 : 1); sl < 5; ++sl) {
+                    const int qq = pair_pop((int)rank, sl);
+                    const uint64_t off = chunk_alloc(a, cs, round16((uint64_t)NN * 8));
+                    slot_ok[sl] = off != ~0ull;
+                    slot_off[sl] = off;
+                    a.dir_out[(size_t)cur_p * 9 + qq] = slot_ok[sl] ? DirEntry{off, 0u, DIR_RAW} : DirEntry{0, 0u, DIR_DEAD};
+                }
+                if (rank == 0) {
+                    cg::cluster_group cluster = cg::this_cluster();
+                    *cluster.map_shared_rank(&mail_off0, peer_of()) = slot_off[0];
+                    *cluster.map_shared_rank(&mail_ok0, peer_of()) = slot_ok[0];
+                }
+            }
+            cluster_sync_all();
+            if (t == 0 && rank == 1) {
+                slot_off[0] = mail_off0;
+                slot_ok[0] = mail_ok0;
+            }
+            __syncthreads();
+            double mass = 0.0;
+            const int lo = half_lo(), H = half_n();
+            for (int k = t; k < 5 * NN; k += NT) {
+                const int sl = k / NN, e = k - sl * NN, i = e / N, jj = e - i * N;
+                if (sl == 0 && (jj < lo || jj >= lo + H)) continue;  // population 0: own column half
+                const double xv = bufs[(size_t)sl * BUFD + e];
+                if (slot_ok[sl]) reinterpret_cast<double*>(a.store_out + slot_off[sl])[e] = xv;
+                mass += (((i == 0 || i == N - 1) ? 0.5 : 1.0) * ((jj == 0 || jj == N - 1) ? 0.5 : 1.0)) * xv;
+            }
+            acc_m[t] = mass;
+            const Job jb = job_of();
+            if (jb.on && jb.s > 0) {  // edge lines straight from the state
+                const double* Bs = bufs + (size_t)jb.s * BUFD;
+                const int li = jb.li, q = jb.q;
+                const PatchPos pp = ppos;
+                if (jb.cx == -1) put_rowlo(a.eout, g, (uint32_t)(pp.ar + 1), pp.b, lbm_slot_rowlo(q), N, li, Bs[(size_t)1 * N + li]);
+                if (jb.cx == 1) put_rowhi(a.eout, g, (uint32_t)(pp.ar + 1), pp.b, lbm_slot_rowhi(q), N, li, Bs[(size_t)(N - 2) * N + li]);
+                if (jb.cy == -1) a.eout.collo[edge_ix((uint32_t)pp.ar, pp.b, lbm_slot_collo(q), g, N) + li] = Bs[(size_t)li * N + 1];
+                if (jb.cy == 1) a.eout.colhi[edge_ix((uint32_t)pp.ar, pp.b, lbm_slot_colhi(q), g, N) + li] = Bs[(size_t)li * N + N - 2];
+            }
+        }
+        // per-patch sums (fixed association: warps in order)
+        if (MODE != MODE_DECODE) {
+            __syncthreads();
+            double mm = acc_m[t], mf = acc_f[t];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                mm += __shfl_xor_sync(0xffffffffu, mm, o);
+                mf += __shfl_xor_sync(0xffffffffu, mf, o);
+            }
+            if ((t & 31) == 0) {
+                red_m[t >> 5] = mm;
+                red_f[t >> 5] = mf;
+            }
+            __syncthreads();
+            if (t == 0) {
+                double sm = 0.0, sf = 0.0;
+                for (int w = 0; w < NT / 32; ++w) {
+                    sm += red_m[w];
+                    sf += red_f[w];
+                }
+                part.mass += sm;
+                part.mass_fv += sf;
+            }
+        }
+        __syncthreads();  // buffers and descriptors free for the next patch
+        WG_PHASE_MARK(31);
+        if (t == 0) {
+            cur_p += npairs;
+            ++cur_it;
+        }
+        __syncthreads();
+    }
+    cluster_sync_all();  // no DSMEM access of an exited peer
+    if (MODE == MODE_DECODE) return;
+    __syncthreads();
+    finalize_step(a, part);
+}
+
+}  // namespace wg

@@ -16,6 +16,7 @@
 namespace wg {
 
 constexpr int kMaxLevels = 8;
+constexpr int kMaxN = 65;  // largest patch side of the device session
 
 // ---- optional phase timing (tuning builds only: -DWG_PHASE_TIMING) ---------
 // Thread 0 of every CTA adds the cycles since its previous mark (i.e. the
@@ -104,6 +105,10 @@ struct StepArgs {
     uint64_t l2_nx;
     double l2_scale, l2_dx, l2_alpha, l2_beta;          // area / nx^2, dx, speeds
     double thr[(kMaxLevels + 1) * (kMaxLevels + 1)];     // T[band_i][band_j]
+    // trapezoid functional of the inverse transform per corner-layout
+    // position (global_mass weights pulled through idwt_line): the mass of a
+    // reconstructed block is sum_rc mass_a[r] mass_a[c] C[r][c]
+    double mass_a[kMaxN];
 };
 
 // MODE_STEP_LZ: a step that also stages the thresholded coefficient arrays

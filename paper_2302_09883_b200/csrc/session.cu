@@ -31,11 +31,10 @@ namespace {
 
 KernelSet select_kernels(int scheme, uint64_t n, int levels, uint64_t npatch) {
     KernelSet k{};
-    const bool half = std::getenv("WG_HALF_LINES") != nullptr;  // opt-in 65-point half-line variants
     bool ok = false;
     const char* what = "transport";
     if (scheme == WG_SCHEME_LBM_D2Q9) {
-        ok = select_lbm_kernels(n, levels, half, k);
+        ok = select_lbm_kernels(n, levels, k);
         what = "D2Q9";
     } else if (scheme == WG_SCHEME_SWE) {
         ok = select_swe_kernels(n, levels, k);
@@ -45,7 +44,7 @@ KernelSet select_kernels(int scheme, uint64_t n, int levels, uint64_t npatch) {
         if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         // C1-sized grids (64 patches of 33 points): one patch per CTA (more SMs busy)
         const bool small = n == 33 && npatch < 2ull * sms;
-        ok = select_transport_kernels(n, levels, half, small, k);
+        ok = select_transport_kernels(n, levels, small, k);
     }
     if (!ok)
         raise(WG_INVALID_ARGUMENT, std::string("device session (") + what + "): patch side " + std::to_string(n) +
@@ -54,6 +53,41 @@ KernelSet select_kernels(int scheme, uint64_t n, int levels, uint64_t npatch) {
 }
 
 namespace {
+
+// The trapezoid functional of the inverse line transform in corner layout:
+// out[k] = sum_i w_i (idwt_line e_k)_i with the global_mass weights w
+// (patchgrid.hpp:244-266: 1/2 at both ends).  The inverse is linear and
+// separable, so the trapezoid mass of idwt_nd(C) is sum_rc out[r] out[c]
+// C[r][c].  The entries are small dyadic numbers, computed exactly; for
+// conservative level counts the details' entries are exactly 0 (the detail
+// functions integrate to zero), so only the samples carry mass.
+void inverse_trapezoid_functional(uint32_t n, int levels, double* out) {
+    const uint32_t m = n - 1;
+    for (uint32_t k = 0; k < n; ++k) {
+        std::vector<double> c(n, 0.0);
+        c[k] = 1.0;
+        std::vector<double> sig(c.begin(), c.begin() + (m >> levels) + 1);
+        for (int l = levels; l >= 1; --l) {
+            const uint32_t len = (m >> (l - 1)) + 1, half = (len - 1) / 2;
+            const double* det = c.data() + (m >> l) + 1;
+            std::vector<double> x(len);
+            for (uint32_t j = 0; j <= half; ++j) {
+                double e = sig[j];
+                if (j >= 1 && j < half) {
+                    const double w0 = (j - 1 == 0 || j - 1 == half - 1) ? 0.5 : 0.25;
+                    const double w1 = (j == 0 || j == half - 1) ? 0.5 : 0.25;
+                    e = e - (w0 * det[j - 1] + w1 * det[j]);
+                }
+                x[2 * j] = e;
+            }
+            for (uint32_t j = 0; j < half; ++j) x[2 * j + 1] = det[j] + (x[2 * j] + x[2 * j + 2]) / 2.0;
+            sig.swap(x);
+        }
+        double s = 0.0;
+        for (uint32_t i = 0; i < n; ++i) s += ((i == 0 || i == m) ? 0.5 : 1.0) * sig[i];
+        out[k] = s;
+    }
+}
 
 // ---- upload: raw store + edge lines from a grid buffer (one thread per
 // logical element: consecutive threads read consecutive addresses, which
@@ -380,6 +414,7 @@ struct Session {
     uint64_t step = 0;
     double time = 0.0;
     double thr[(kMaxLevels + 1) * (kMaxLevels + 1)] = {};
+    double mass_a[kMaxN] = {};
 
     // optional per-launch timing of the fused kernel (bench roofline)
     bool profiling = false;
@@ -517,19 +552,38 @@ struct Session {
         sg.me = ks.edges3 ? 3u : sg.m;
         {
             int per_sm = 0, sms = 0;
-            WG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ks.main, ks.threads, ks.smem));
             WG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, shard.device));
             const uint64_t groups = (sg.npatch + ks.P - 1) / ks.P;
-            uint64_t resident = (uint64_t)std::max(per_sm, 1) * sms;
-            if (const char* f = std::getenv("WG_GRID_WAVES"))  // tuning knob: CTAs = waves x resident
+            uint64_t resident = 0;
+            if (ks.cluster > 1) {  // co-resident clusters (one patch per cluster)
+                cudaLaunchConfig_t lc{};
+                lc.gridDim = dim3((unsigned)(ks.cluster * sms), 1, 1);
+                lc.blockDim = dim3((unsigned)ks.threads, 1, 1);
+                lc.dynamicSmemBytes = ks.smem;
+                cudaLaunchAttribute at{};
+                at.id = cudaLaunchAttributeClusterDimension;
+                at.val.clusterDim.x = (unsigned)ks.cluster;
+                at.val.clusterDim.y = 1;
+                at.val.clusterDim.z = 1;
+                lc.attrs = &at;
+                lc.numAttrs = 1;
+                int clusters = 0;
+                WG_CUDA(cudaOccupancyMaxActiveClusters(&clusters, reinterpret_cast<const void*>(ks.main), &lc));
+                resident = (uint64_t)std::max(clusters, 1);
+            } else {
+                WG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ks.main, ks.threads, ks.smem));
+                resident = (uint64_t)std::max(per_sm, 1) * sms;
+            }
+            if (const char* f = std::getenv("WG_GRID_WAVES"))  // test knob: fewer CTAs, many patches each
                 resident = (uint64_t)std::max(1.0, std::atof(f) * (double)resident);
-            grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(groups, resident));
+            grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(groups, resident)) * (unsigned)ks.cluster;
             if (ks.scratch_doubles) scratch = dalloc<double>((uint64_t)grid * ks.scratch_doubles);
         }
         // thresholds (threshold.hpp:31-47) — the "c == 0 or levels == 0"
         // early return of apply_threshold (threshold.hpp:53) is T = 0.
         if (cfg.c == 0.0 || levels == 0) std::fill(std::begin(thr), std::end(thr), 0.0);
         else threshold_table_2d(levels, cfg.threshold_mode, cfg.c, cfg.threshold_alpha, thr);
+        inverse_trapezoid_functional(N, levels, mass_a);
 
         const uint64_t raw_block = round16((uint64_t)N * N * 8);
         const uint64_t blocks = (uint64_t)sg.npatch * sg.m;
@@ -786,6 +840,7 @@ struct Session {
             a.gravity = cfg.gravity;
         }
         std::memcpy(a.thr, thr, sizeof(thr));
+        std::memcpy(a.mass_a, mass_a, sizeof(mass_a));
         return a;
     }
 

@@ -314,12 +314,3 @@ def test_lbm_directory_ends_on_page_boundary(product):
         product.check(product.wg_session_sync(s))
     finally:
         product.wg_session_destroy(s)
-
-
-@pytest.mark.parametrize("levels,c", [(4, 1e-3), (5, 1e-5), (6, 1e-4), (4, 0.0)])
-def test_lbm_group_lines_parity(product, oracle, monkeypatch, levels, c):
-    """The 8-lane line-group D2Q9 kernel (WG_LBM_LINES=group,
-    lbm_group_kernels.cuh; a tuning variant) is bit-exact too."""
-    monkeypatch.setenv("WG_LBM_LINES", "group")
-    cfg = lbm_cfg(129, (2, 2), levels, c, 4)
-    compare_runs(api.run(cfg, lib=product), api.run(cfg, lib=oracle))

@@ -15,9 +15,9 @@ import bench  # noqa: E402
 from paper_2302_09883_b200 import abi, api  # noqa: E402
 from paper_2302_09883_b200.distributed import ShardInfo, ShardedSession  # noqa: E402
 
-LBM_NAMES = {0: "decode rows (round 0)", 12: "decode rows (rounds 1,2)", 1: "decode cols+stream", 2: "collide",
-             3: "pass1 col fwd", 4: "pass1 row thr+scan+S", 5: "pass2 alloc", 6: "pass2 CSR+row inv",
-             7: "pass2 col recon+edges", 9: "patch sums", 11: "finalize"}
+LBM_NAMES = {21: "D0+D1 wait, masks, decode rows", 22: "D2 decode cols + stream", 23: "cluster sync (streamed)",
+             24: "C collide", 25: "cluster sync (collided)", 26: "F1 col fwd + cluster sync", 27: "F2 row fwd + thr",
+             28: "S scan + M1", 29: "alloc + M2", 30: "W CSR + cone rows", 31: "edge lines + patch sums"}
 NAMES = {0: "decode rows+ghosts", 1: "decode cols", 2: "FV + mass", 3: "sync before fwd", 4: "fwd col DWT",
          5: "row DWT+thr+scan", 6: "alloc", 7: "CSR write + row inv", 8: "col recon+edges", 9: "raw store",
          10: "group sums", 11: "finalize"}
