@@ -1,17 +1,19 @@
 #!/usr/bin/env python
 """Benchmark of the compressed stencil loop (BASELINE.json metric).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload lbm_c2]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload lbm_c4]
     python bench.py --impl reference ...      # the reference CPU path
 
 A "step" is one pass of the hot path over the whole grid: ghost lines ->
-decode -> scheme update -> DWT -> threshold -> CSR -> reconstruction, for
-every patch (pipeline.hpp:194-289).  The default workload is BASELINE.json
-configs[1]: D2Q9 LBM on 1024^2 cells in 64^2-cell patches (65^2 points),
-level 4, capped threshold 1e-3 (the middle of the 1e-2..1e-5 sweep; the sweep
-itself is a parity/accuracy test case), synthetic shear-layer initial state.
-With N > 1 ranks (torchrun) the patch rows of the same grid are sharded
-(strong scaling) and the halo lines move over NCCL every step.
+decode -> scheme update -> DWT -> threshold -> CSR -> edge lines, for every
+patch (pipeline.hpp:194-289).  The default workload is BASELINE.json
+configs[3] (C4), the largest single-GPU configuration: D2Q9 LBM on 16384^2
+cells in 64^2-cell patches (65^2 points), level 4, capped threshold 1e-3,
+synthetic shear-layer initial state generated on the host (bit-identical to
+the reference-style IC), under an 8 GiB store budget smaller than the 19.9 GB
+raw state.  With N > 1 ranks (torchrun) the patch rows are sharded (strong
+scaling) and the halo lines move over NCCL (or NVLink peer stores) every
+step.
 
 Prints ONE JSON line (rank 0).  Timing: CUDA events around every step on the
 session stream, L2 flushed (a 256 MiB write) between timed steps outside the
@@ -54,10 +56,15 @@ WORKLOADS = {
     # BASELINE.json configs[0] (C1): the reference's own CPU-runnable case
     "transport_c1": dict(scheme="transport", components=1, nx=257, splits=(8, 8), levels=4, c=1e-3, mode="capped"),
     # BASELINE.json configs[3] (C4): 16384^2 D2Q9 on one GPU; the raw f-field
-    # (19.9 GB) exceeds the 8 GiB store budget, so the initial state is
-    # generated and compressed on the device
+    # (19.9 GB) exceeds the 8 GiB store budget: the host initial state (glibc,
+    # bit-identical to the reference IC) streams through the device into step 1
+    # (wg_session_step_host) and never enters the store.  N > 1: the shards'
+    # initial state is generated and compressed on the device instead.
     "lbm_c4": dict(scheme="lbm", components=9, nx=16385, splits=(256, 256), levels=4, c=1e-3, mode="capped",
-                   budget=8 << 30, device_init=True, scaling="strong"),
+                   budget=8 << 30, streamed=True, scaling="strong"),
+    # C4 with the device-generated initial state (the N > 1 path on one GPU)
+    "lbm_c4_devinit": dict(scheme="lbm", components=9, nx=16385, splits=(256, 256), levels=4, c=1e-3,
+                           mode="capped", budget=8 << 30, device_init=True, scaling="strong"),
     # BASELINE.json configs[4] (C5): 65536^2 D2Q9 (319 GB raw), sharded by patch
     # rows over the ranks; fits ONE B200 compressed
     "lbm_c5": dict(scheme="lbm", components=9, nx=65537, splits=(1024, 1024), levels=4, c=1e-3, mode="capped",
@@ -195,10 +202,13 @@ def cpu_lib():
 
 def cpu_run(w: dict, steps: int, threads: int):
     """Time the CPU implementation on `steps` steps of the workload; returns
-    (MLUPS, seconds, kind, cores, rows).  C4/C5 do not fit the host (their raw
-    state is 20 / 319 GB): their CPU rate is measured on the C2 grid
-    ("report the CPU MLUPS at C2/C3 sizes as the rate")."""
-    if w.get("device_init"):
+    (MLUPS, seconds, kind, cores, rows, sample).  C4/C5 do not fit the CPU in
+    minutes (268 M / 4.3 G cells per step): their per-cell work (65^2-point
+    patches, L = 4, capped 1e-3) is timed on the C2 grid (1024^2) — declared
+    in `sample` and by same_config = false."""
+    name = w.get("_name", "")
+    same = not (w.get("device_init") or w.get("streamed"))
+    if not same:
         w = WORKLOADS["lbm_c2"]
     lib, kind = cpu_lib()
     cfg = run_config(w, steps)
@@ -207,11 +217,25 @@ def cpu_run(w: dict, steps: int, threads: int):
         # the initial state (dam break: vmax0 = sqrt(2 g); later dts shrink,
         # so the run takes at least that many steps — the rate counts them all)
         cfg.t_end = steps * cfg.cfl * (cfg.domain_length / (w["nx"] - 1)) / (2.0 * cfg.gravity) ** 0.5
+    if w["scheme"] == "transport":
+        cfg.compute_l2 = True  # run() computes the l2 diagnostic every step (pipeline.hpp:275-276)
     cfg.threads = threads if kind == "reference" else 1
     res = api.run(cfg, lib=lib)
     secs = res.summary["total_seconds"]
     cells = (w["nx"] - 1) ** 2
-    return cells * len(res.rows) / secs / 1e6, secs, kind, cfg.threads, res.rows
+    if w["scheme"] == "lbm":
+        # the reference has no LBM: the builder's D2Q9 on the
+        # reference's own Patch / sync_ghosts / compression functions
+        what = ("the builder's D2Q9 on the reference's Patch/sync_ghosts/compression functions "
+                "(oracle/_ref/ref_shim.cpp, reference headers compiled unchanged)" if kind == "reference"
+                else "the builder's D2Q9 in the C restatement (oracle/wg_oracle.c)")
+        kind = "port"
+    else:
+        what = "run() of the reference headers (oracle/_ref)" if kind == "reference" else "run() of the C port"
+    grid = f"{w['nx'] - 1}^2"
+    sample = (f"{len(res.rows)} steps of the {grid} workload, {what}, {cfg.threads} threads, {secs:.1f} s"
+              + ("" if same else f"; C2 grid standing in for {name} (same 65^2-point patches, L=4, capped 1e-3)"))
+    return cells * len(res.rows) / secs / 1e6, secs, kind, cfg.threads, res.rows, sample, same
 
 
 # ---- the reference arm -----------------------------------------------------------
@@ -224,16 +248,15 @@ def bench_reference(args, w: dict):
     threads = os.cpu_count() or 1
     if args.warmup:
         cpu_run(w, max(1, min(args.warmup, 2)), threads)
-    mlups, secs, kind, cores, rows = cpu_run(w, args.steps, threads)
+    mlups, secs, kind, cores, rows, sample, same = cpu_run(w, args.steps, threads)
     line = {
         "impl": "reference", "metric": METRIC, "value": mlups, "unit": "MLUPS", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * secs / len(rows),
         "higher_is_better": True, "scaling": w.get("scaling", "weak"), "vs_baseline": None, "dtype": "f64",
-        "data": data_label(w), "config": config_json(args, w),
+        "data": data_label(w), "config": config_json(args, w), "same_config": same,
         "compression_ratio": statistics.fmean(r["ratio"] for r in rows),
         "cpu_baseline": {"value": mlups, "unit": "MLUPS", "cores": cores, "kind": kind, "cpu": cpu_model(),
-                         "sample": f"{len(rows)} steps of the full {w['nx'] - 1}^2 workload, run() of the "
-                                   f"{'reference headers (oracle/_ref)' if kind == 'reference' else 'C port'}"},
+                         "sample": sample},
         "e2e": {"value": mlups, "unit": "MLUPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -255,6 +278,30 @@ def config_json(args, w):
 
 
 # ---- the B200 arm ----------------------------------------------------------------
+
+
+def host_initial_state(lib, cfg, rb: int, re_: int, weak: bool, splits1: int, square_cfg):
+    """This rank's initial grid buffer in page-locked memory, filled by the
+    product's host IC (glibc libm: bit-identical to the reference IC,
+    host threads over patch rows)."""
+    import torch
+
+    if weak:  # every rank's rows are one periodic copy of the square grid
+        full = api.initial_state(square_cfg, lib=lib)
+        pinned = torch.empty(full.data.size, dtype=torch.float64, pin_memory=True)
+        pinned.numpy()[:] = full.data.reshape(-1)
+        return pinned
+    n = abi.u64()
+    c = cfg.to_c()
+    lib.check(lib.wg_run_grid_doubles(C.byref(c), C.byref(n)))
+    per_row = n.value // cfg.splits[0]
+    pinned = torch.empty(n.value, dtype=torch.float64, pin_memory=True)
+    lib.check(lib.wg_run_initial_state(C.byref(c), abi.dptr(pinned.numpy())))
+    if (rb, re_) != (0, cfg.splits[0]):
+        own = torch.empty((re_ - rb) * per_row, dtype=torch.float64, pin_memory=True)
+        own.copy_(pinned[rb * per_row: re_ * per_row])
+        return own
+    return pinned
 
 
 def bench_b200(args, w: dict):
@@ -292,46 +339,35 @@ def bench_b200(args, w: dict):
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
 
-    device_init = w.get("device_init", False)
-    if device_init:
-        host = None  # raw state larger than the budget: generated + compressed on the device
-    else:
-        # initial state on the host (glibc libm, bit-identical to the reference IC);
-        # with weak scaling every rank's rows are one copy of the square grid
-        square = run_config(w, 1)
-        full = api.initial_state(square, lib=lib)
-        if weak:
-            own = full.data
-        else:
-            own = np.ascontiguousarray(full.data[rb * w["splits"][1]: re_ * w["splits"][1]])
-        pinned = torch.empty(own.size, dtype=torch.float64, pin_memory=True)
-        host = pinned.numpy()
-        host[:] = own.reshape(-1)
-        del full
+    # initial state: host (page-locked, bit-identical to the reference IC),
+    # streamed into step 1 when the raw state exceeds the store budget (C4);
+    # generated and compressed on the device for the sharded huge grids
+    streamed = w.get("streamed", False) and world == 1
+    device_init = w.get("device_init", False) or (w.get("streamed", False) and world > 1)
+    host = None
+    if not device_init:
+        host = host_initial_state(lib, cfg, rb, re_, weak, w["splits"][1], run_config(w, 1)).numpy()
 
     sess = ShardedSession(lib, cfg, shard, stream.cuda_stream, dist if world > 1 else None)
     maybe_peer_halos(sess, cfg, dist, world)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{local}")
     try:
-        if device_init:
-            sess.init_device()
-        else:
-            sess.upload(host)
-        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
         with ClockSampler(local) as clocks:
-            # warm-up: at least W steps, continued until the clock sampler is
-            # producing samples under load (bounded), so that the clocks
-            # reported are those of the loaded GPU around the timed region
-            t_w = time.perf_counter()
-            done = 0
-            adaptive = world == 1 and not os.environ.get("WG_FIXED_WARMUP")
-            while done < args.warmup or (adaptive and clocks.count() < 3 and time.perf_counter() - t_w < 3.0):
-                sess.step(dt)
-                done += 1
-                if done % 8 == 0:
-                    sess.sync()
+            if device_init:
+                sess.init_device()
+            elif not streamed:
+                sess.upload(host)
+            evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                   for _ in range(args.steps)]
+            # exactly W untimed warm-up steps (the first one streams the host
+            # initial state in the C4 path)
+            for k in range(args.warmup):
+                if streamed and k == 0:
+                    sess.step_host(host, dt)
+                else:
+                    sess.step(dt)
             sess.sync()
-            warm_steps = done
+            warm_steps = args.warmup
             lib.check(lib.wg_session_profile(sess.handle, 1))
             if world > 1:
                 dist.barrier()
@@ -365,7 +401,7 @@ def bench_b200(args, w: dict):
 
         # ---- end to end through the public API with host buffers -------------
         e2e = e2e_run(lib, cfg, shard, stream, host, args, dt, dist if world > 1 else None,
-                      world if weak else 1)
+                      world if weak else 1, streamed)
     finally:
         sess.close()
 
@@ -376,6 +412,9 @@ def bench_b200(args, w: dict):
     launch_ms = main_ms.value / max(launches.value, 1)
     achieved = cells_local * B_ALG[w["scheme"]] / (launch_ms * 1e-3) / 1e9
     timed_rows = rows[warm_steps:]
+    n = (w["nx"] - 1) // w["splits"][0] + 1
+    kname = {"lbm": f"k_lbm_pair<{n},{w['levels']},STEP>", "swe": f"k_swe_step<{n},{w['levels']},STEP>"}.get(
+        w["scheme"], f"k_patch_step<{n},{w['levels']},STEP>")
     line = {
         "metric": METRIC, "value": value, "unit": "MLUPS", "n_gpus": world, "steps": args.steps,
         "warmup": warm_steps, "ms_per_step": tot_ms / args.steps, "higher_is_better": True,
@@ -387,28 +426,31 @@ def bench_b200(args, w: dict):
         "mass_drift": abs(timed_rows[-1]["global_mass"] - rows[0]["global_mass"]) / abs(rows[0]["global_mass"]),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
                      "frac": achieved / pk["hbm_gbs"], "traffic": traffic_from_profiles(args.workload),
-                     "kernel": f"k_{ {'lbm': 'lbm', 'swe': 'swe'}.get(w['scheme'], 'patch') }_step<MAIN>",
+                     "kernel": kname,
                      "algorithmic_bytes_per_launch": cells_local * B_ALG[w["scheme"]],
                      "avg_launch_ms": launch_ms, "peak_source": pk["source"],
                      "step_share": main_max / tot_ms if tot_ms else None},
         "e2e": e2e,
         "compute_ceiling": compute_ceiling(lib, w, value / world),  # per GPU
-        # one fused kernel launch per step (k_*_step<STEP>); Codec::lz adds the
-        # LZ-size pass (k_lz_sizes, which also writes the step's row)
-        # (+ the device-side wait and signal of the peer halo mode)
+        # one fused kernel launch per step; Codec::lz adds the LZ-size pass
+        # (k_lz_sizes, which also writes the step's row); the peer halo mode
+        # adds its device-side wait and signal
         "gpu_launches": args.steps * ((2 if w.get("codec") == "lz" else 1) + (2 if sess.peer else 0)),
         "clocks": clocks.summary(),
         "device_bytes": info.device_bytes,
         "device_mem_used_bytes": mem_used,
         "raw_state_bytes": 8 * w["components"] * (w["nx"] - 1) ** 2 if "components" in w else None,
+        "initial_state": ("device-generated (CUDA libm, not bit-pinned)" if device_init else
+                          "host glibc IC (bit-identical to the reference), streamed into step 1"
+                          if streamed else "host glibc IC (bit-identical to the reference), uploaded"),
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         # bounded sample: calibrate on a few steps, then about 12 s of CPU work
-        _, s0, _, _, _ = cpu_run(w, 3, os.cpu_count() or 1)
+        s0 = cpu_run(w, 3, os.cpu_count() or 1)[1]
         cpu_steps = args.cpu_steps or int(max(3, min(2000, 12.0 / max(s0 / 3, 1e-6))))
-        mlups, secs, kind, cores, crow = cpu_run(w, cpu_steps, os.cpu_count() or 1)
+        mlups, secs, kind, cores, crow, sample, same = cpu_run(w, cpu_steps, os.cpu_count() or 1)
         line["cpu_baseline"] = {"value": mlups, "unit": "MLUPS", "cores": cores, "kind": kind, "cpu": cpu_model(),
-                                "sample": f"{len(crow)} steps of the full {w['nx'] - 1}^2 workload ({secs:.1f} s)"}
+                                "sample": sample, "same_config": same}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -429,10 +471,11 @@ def compute_ceiling(lib, w, value_mlups):
     return out
 
 
-def e2e_run(lib, cfg, shard, stream, host, args, dt, dist, copies=1):
-    """Same metric through the public API: the host state is uploaded from
-    pinned memory inside the timed region and every step's metrics row is
-    read back to the host."""
+def e2e_run(lib, cfg, shard, stream, host, args, dt, dist, copies=1, streamed=False):
+    """Same metric through the public API with host buffers: inside the timed
+    region the host initial state goes in from page-locked memory (streamed
+    into step 1 in the C4 path), every step's metrics row comes back, and the
+    final decoded state is read back into the host grid buffer."""
     import torch
 
     from paper_2302_09883_b200.distributed import ShardedSession, collective_device
@@ -440,6 +483,7 @@ def e2e_run(lib, cfg, shard, stream, host, args, dt, dist, copies=1):
     sess = ShardedSession(lib, cfg, shard, stream.cuda_stream, dist)
     maybe_peer_halos(sess, cfg, dist, shard.world)
     row_buf = torch.empty(args.steps * C.sizeof(abi.MetricsRowC), dtype=torch.uint8, pin_memory=True)
+    out = None if host is None else host  # the state read back overwrites the (consumed) input buffer
     try:
         if dist:
             dist.barrier()
@@ -447,12 +491,18 @@ def e2e_run(lib, cfg, shard, stream, host, args, dt, dist, copies=1):
         t0 = time.perf_counter()
         if host is None:
             sess.init_device()
-        else:
+        elif not streamed:
             sess.upload(host)
         rowsz = C.sizeof(abi.MetricsRowC)
         for k in range(args.steps):
-            sess.step(dt)  # + the step's metrics row read back (async D2H into page-locked memory)
+            if streamed and k == 0:
+                sess.step_host(host, dt)
+            else:
+                sess.step(dt)
+            # + the step's metrics row read back (async D2H into page-locked memory)
             lib.check(lib.wg_session_last_row_async(sess.handle, C.c_void_p(row_buf.data_ptr() + k * rowsz)))
+        if out is not None:
+            sess.download(out)
         torch.cuda.synchronize()
         secs = time.perf_counter() - t0
         if dist:
@@ -464,15 +514,18 @@ def e2e_run(lib, cfg, shard, stream, host, args, dt, dist, copies=1):
     finally:
         sess.close()
     cells = (cfg.nx - 1) ** 2 * copies
+    row_b = C.sizeof(abi.MetricsRowC)
     if host is None:
         return {"value": cells * args.steps / secs / 1e6, "unit": "MLUPS", "h2d_bytes_per_step": 0,
-                "d2h_bytes_per_step": C.sizeof(abi.MetricsRowC),
+                "d2h_bytes_per_step": row_b, "seconds": secs,
                 "note": "initial state generated and compressed on the device inside the timed region; "
                         "every step's metrics row read back (async D2H into page-locked memory)"}
     return {"value": cells * args.steps / secs / 1e6, "unit": "MLUPS",
-            "h2d_bytes_per_step": host.nbytes / args.steps, "d2h_bytes_per_step": C.sizeof(abi.MetricsRowC),
-            "note": "initial state uploaded once inside the timed region (bytes amortised per step); "
-                    "every step's metrics row read back (async D2H into page-locked memory)"}
+            "h2d_bytes_per_step": host.nbytes / args.steps,
+            "d2h_bytes_per_step": (host.nbytes + args.steps * row_b) / args.steps, "seconds": secs,
+            "note": ("host initial state (page-locked) " + ("streamed into step 1" if streamed else "uploaded")
+                     + f" and the final decoded state read back, {args.steps} steps, inside the timed region "
+                       "(bytes amortised per step); every step's metrics row read back asynchronously")}
 
 
 def peer_halos_wanted(cfg, dist, world: int) -> bool:
@@ -502,13 +555,14 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
-    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="lbm_c2")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="lbm_c4")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-steps", type=int, default=0, help="CPU baseline steps (0: ~12 s of work)")
     args = ap.parse_args()
     if args.impl == "b200":
         args.warmup = max(args.warmup, 3)  # timing rule: at least 3 untimed warm-up steps
-    w = WORKLOADS[args.workload]
+    w = dict(WORKLOADS[args.workload])
+    w["_name"] = args.workload
     if args.impl == "reference":
         bench_reference(args, w)
     else:

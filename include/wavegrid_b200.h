@@ -254,6 +254,15 @@ wg_status wg_session_upload(wg_session* s, const double* host_grid);
 /* Same from a device grid buffer (async on the session stream). */
 wg_status wg_dev_session_upload(wg_session* s, const double* dev_grid);
 
+/* Step 1 of a run straight from a host grid buffer holding the initial
+ * state (this shard's patches, grid-buffer layout; page-locked memory is
+ * streamed by the DMA engine): the raw state never enters the store, so a
+ * store budget smaller than the raw state (C4) still starts from the
+ * reference's raw initial grid (pipeline.hpp:138-155, 194-289) — the same
+ * result as wg_session_upload + wg_session_step.  Resets step and time,
+ * then performs step 1 with `dt`.  One-shard D2Q9 sessions. */
+wg_status wg_session_step_host(wg_session* s, const double* host_grid, double dt);
+
 /* Generate the initial state of cfg ON THE DEVICE and store it through the
  * compression cycle (for grids whose raw state does not fit the store
  * budget, C4/C5).  Unlike wg_session_upload the first step then starts from

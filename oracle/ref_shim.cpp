@@ -121,8 +121,11 @@ inline void lbm_cu(double ux, double uy, double cu[9]) {
     cu[8] = uy - ux;
 }
 
+// D2Q9 BGK in its FMA form: std::fma is correctly rounded.
+inline double lbm_usq(double ux, double uy) { return std::fma(ux, ux, uy * uy); }
+
 inline double lbm_feq(int q, double rho, double cu, double usq) {
-    const double t = ((1.0 + 3.0 * cu) + (4.5 * cu) * cu) - 1.5 * usq;
+    const double t = std::fma(cu, std::fma(4.5, cu, 3.0), std::fma(-1.5, usq, 1.0));
     return (kW[q] * rho) * t;
 }
 
@@ -130,11 +133,12 @@ inline void lbm_collide(const double f[9], double omega, double out[9]) {
     const double rho = ((((((((f[0] + f[1]) + f[2]) + f[3]) + f[4]) + f[5]) + f[6]) + f[7]) + f[8]);
     const double jx = ((f[1] - f[2]) + (f[5] - f[6])) + (f[7] - f[8]);
     const double jy = ((f[3] - f[4]) + (f[5] - f[6])) + (f[8] - f[7]);
-    const double ux = jx / rho, uy = jy / rho;
-    const double usq = ux * ux + uy * uy;
+    const double inv = 1.0 / rho;
+    const double ux = jx * inv, uy = jy * inv;
+    const double usq = lbm_usq(ux, uy);
     double cu[9];
     lbm_cu(ux, uy, cu);
-    for (int q = 0; q < 9; ++q) out[q] = f[q] - (f[q] - lbm_feq(q, rho, cu[q], usq)) * omega;
+    for (int q = 0; q < 9; ++q) out[q] = std::fma(omega, lbm_feq(q, rho, cu[q], usq) - f[q], f[q]);
 }
 
 // One pull-stream + collide on every logical cell of a 2-D, 9-component
@@ -167,7 +171,7 @@ void lbm_initial(PatchGrid& grid, const wg_run_config& c) {
                 c.lbm_delta * c.lbm_u0 * std::sin(2.0 * std::numbers::pi * (Y + 0.25));
             double cu[9];
             lbm_cu(ux, uy, cu);
-            return lbm_feq(q, 1.0, cu[q], ux * ux + uy * uy);
+            return lbm_feq(q, 1.0, cu[q], lbm_usq(ux, uy));
         });
     }
 }

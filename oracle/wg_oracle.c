@@ -650,8 +650,12 @@ static void lbm_cu(double ux, double uy, double* cu) {
     cu[8] = uy - ux;
 }
 
+/* D2Q9 BGK in its FMA form (csrc/physics.cuh): C99 fma() is
+ * correctly rounded, so this restatement and the device agree bit for bit. */
+static inline double lbm_usq(double ux, double uy) { return fma(ux, ux, uy * uy); }
+
 static inline double lbm_feq(int q, double rho, double cu, double usq) {
-    const double t = ((1.0 + 3.0 * cu) + (4.5 * cu) * cu) - 1.5 * usq;
+    const double t = fma(cu, fma(4.5, cu, 3.0), fma(-1.5, usq, 1.0));
     return (kW[q] * rho) * t;
 }
 
@@ -659,11 +663,12 @@ static void lbm_collide(const double* f, double omega, double* out) {
     const double rho = ((((((((f[0] + f[1]) + f[2]) + f[3]) + f[4]) + f[5]) + f[6]) + f[7]) + f[8]);
     const double jx = ((f[1] - f[2]) + (f[5] - f[6])) + (f[7] - f[8]);
     const double jy = ((f[3] - f[4]) + (f[5] - f[6])) + (f[8] - f[7]);
-    const double ux = jx / rho, uy = jy / rho;
-    const double usq = ux * ux + uy * uy;
+    const double inv = 1.0 / rho;
+    const double ux = jx * inv, uy = jy * inv;
+    const double usq = lbm_usq(ux, uy);
     double cu[9];
     lbm_cu(ux, uy, cu);
-    for (int q = 0; q < 9; ++q) out[q] = f[q] - (f[q] - lbm_feq(q, rho, cu[q], usq)) * omega;
+    for (int q = 0; q < 9; ++q) out[q] = fma(omega, lbm_feq(q, rho, cu[q], usq) - f[q], f[q]);
 }
 
 static void lbm_step_patch(const grid_t* g, const double* cur, double* next, uint64_t p,
@@ -823,7 +828,7 @@ wg_status wg_run_initial_state(const wg_run_config* c, double* buf) {
                     double cu[9];
                     lbm_cu(ux, uy, cu);
                     for (int q = 0; q < 9; ++q)
-                        comp_ptr(&g, buf, p, q)[off] = lbm_feq(q, 1.0, cu[q], ux * ux + uy * uy);
+                        comp_ptr(&g, buf, p, q)[off] = lbm_feq(q, 1.0, cu[q], lbm_usq(ux, uy));
                 }
             }
     }

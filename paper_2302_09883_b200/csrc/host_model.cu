@@ -5,7 +5,10 @@
 // the same glibc libm (exp, sin, tanh, pow) as the reference so that the
 // initial state and the thresholds are bit-identical (SURVEY §8 hard parts:
 // "Generate ICs with exp/sin on the host").
+#include <atomic>
 #include <cmath>
+#include <thread>
+#include <vector>
 #include <cstring>
 #include <numbers>
 #include <string>
@@ -141,14 +144,27 @@ double exact_transport_at(const wg_run_config& c, double t, uint64_t i, uint64_t
 void initial_state(const wg_run_config& c, uint64_t row_begin, uint64_t row_end, double* buf) {
     const RunGeometry g = run_geometry(c);
     const uint64_t n0 = g.n[0], n1 = g.n[1], ty = n1 + 2;
-    const uint64_t npl = (row_end - row_begin) * g.splits[1];
-    std::memset(buf, 0, sizeof(double) * npl * g.m * g.tcount);
     const double dx = sim_dx(c);
     const double inv = 1.0 / static_cast<double>(c.nx - 1);
-    for (uint64_t a = row_begin; a < row_end; ++a)
+    // D2Q9 shear layer: u_y depends on the row coordinate only, u_x on the
+    // column only — each libm value is evaluated once per index (the same
+    // expression, so the same bits as evaluating it per point)
+    std::vector<double> uy_of, ux_of;
+    if (c.scheme == WG_SCHEME_LBM_D2Q9) {
+        uy_of.resize(c.nx);
+        ux_of.resize(c.nx);
+        for (uint64_t k = 0; k < c.nx; ++k) {
+            const double X = static_cast<double>(k) * inv, Y = X;
+            uy_of[k] = X <= 0.5 ? c.lbm_u0 * std::tanh(c.lbm_kappa * (X - 0.25))
+                                : c.lbm_u0 * std::tanh(c.lbm_kappa * (0.75 - X));
+            ux_of[k] = c.lbm_delta * c.lbm_u0 * std::sin(2.0 * std::numbers::pi * (Y + 0.25));
+        }
+    }
+    auto fill_row = [&](uint64_t a) {
         for (uint64_t b = 0; b < g.splits[1]; ++b) {
             const uint64_t p = (a - row_begin) * g.splits[1] + b;
             double* base = buf + p * g.m * g.tcount;
+            std::memset(base, 0, sizeof(double) * g.m * g.tcount);
             for (uint64_t i = 1; i <= n0; ++i)
                 for (uint64_t j = 1; j <= n1; ++j) {
                     // tiled grids repeat the square problem along dim 0 (the
@@ -164,18 +180,28 @@ void initial_state(const wg_run_config& c, uint64_t row_begin, uint64_t row_end,
                         const bool inside = std::abs(x - 0.5) <= 0.25 && std::abs(y - 0.5) <= 0.25;
                         base[off] = inside ? 2.0 : 1.0;
                     } else {
-                        const double X = static_cast<double>(gi) * inv;
-                        const double Y = static_cast<double>(gj) * inv;
-                        const double uy = X <= 0.5 ? c.lbm_u0 * std::tanh(c.lbm_kappa * (X - 0.25))
-                                                   : c.lbm_u0 * std::tanh(c.lbm_kappa * (0.75 - X));
-                        const double ux = c.lbm_delta * c.lbm_u0 *
-                                          std::sin(2.0 * std::numbers::pi * (Y + 0.25));
-                        const double usq = ux * ux + uy * uy;
+                        const double uy = uy_of[gi], ux = ux_of[gj];
+                        const double usq = lbm_usq(ux, uy);
                         for (int q = 0; q < 9; ++q)
                             base[q * g.tcount + off] = lbm_feq(q, 1.0, lbm_cu(q, ux, uy), usq);
                     }
                 }
         }
+    };
+    // patch rows in parallel (host threads; large grids: C4 is 21 GB)
+    const uint64_t rows = row_end - row_begin;
+    const unsigned nt = (unsigned)std::min<uint64_t>(rows, std::max(1u, std::thread::hardware_concurrency()));
+    if (nt <= 1 || rows * g.splits[1] * g.m * g.tcount < (1ull << 22)) {
+        for (uint64_t a = row_begin; a < row_end; ++a) fill_row(a);
+        return;
+    }
+    std::atomic<uint64_t> next{row_begin};
+    std::vector<std::thread> pool;
+    for (unsigned k = 0; k < nt; ++k)
+        pool.emplace_back([&] {
+            for (uint64_t a; (a = next.fetch_add(1)) < row_end;) fill_row(a);
+        });
+    for (auto& th : pool) th.join();
 }
 
 }  // namespace wg

@@ -8,8 +8,18 @@
 namespace wg {
 
 inline void kt_set_smem(const KernelSet& k) {
+    int dev = 0, optin = 0;
+    WG_CUDA(cudaGetDevice(&dev));
+    WG_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
     for (auto f : {k.main, k.decode, k.init, k.main_lz})
-        if (f) WG_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k.smem));
+        if (f) {
+            cudaFuncAttributes fa{};
+            WG_CUDA(cudaFuncGetAttributes(&fa, f));
+            if (fa.sharedSizeBytes + k.smem > (size_t)optin)
+                raise(WG_LOGIC, "kernel shared memory (static " + std::to_string(fa.sharedSizeBytes) + " + dynamic " +
+                                    std::to_string(k.smem) + ") exceeds the per-block limit");
+            WG_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k.smem));
+        }
 }
 
 // Walk L = 0.. while 2^L <= N-1 (and L <= Lmax); Make<N, L>::make() builds the set.

@@ -48,6 +48,10 @@ namespace wg {
 
 namespace cg = cooperative_groups;
 
+#ifndef WG_LBM_CELLS
+#define WG_LBM_CELLS 3
+#endif
+
 // ---- PTX helpers: mbarrier, bulk async copy, cluster barriers ---------------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -79,12 +83,30 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
         "l"(src), "r"(bytes), "r"(smem_u32(bar))
         : "memory");
 }
+// 8-byte asynchronous global -> shared copy (LDGSTS): no register, no stall
+// at issue; completed by cp_async_wait_all before the barrier that publishes it
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 // generic-proxy accesses of shared memory before later async-proxy writes
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void cluster_arrive() { asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory"); }
 __device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory"); }
+__device__ __forceinline__ void cluster_arrive_relaxed() {
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+}
 __device__ __forceinline__ void cluster_sync_all() {
     cluster_arrive();
+    cluster_wait();
+}
+// Cluster barrier after a CTA barrier: only warp 0 arrives with release
+// semantics (cumulative over the CTA's writes it observed through the CTA
+// barrier), the other warps arrive relaxed — one warp pays the fence.
+__device__ __forceinline__ void cluster_sync_cta() {
+    __syncthreads();
+    if ((threadIdx.x >> 5) == 0) cluster_arrive();
+    else cluster_arrive_relaxed();
     cluster_wait();
 }
 __device__ __forceinline__ unsigned cluster_rank() {
@@ -129,6 +151,15 @@ __host__ __device__ constexpr Bits128 inverse_cone(int ii) {
     return out;
 }
 
+// Register (interleaved) indices holding samples after L levels.
+template <int N, int L>
+__host__ __device__ constexpr Bits128 sample_bits() {
+    Bits128 b{};
+    for (int r = 0; r < N; ++r)
+        if (r % (1 << L) == 0) b.set(r);
+    return b;
+}
+
 // Output position II of the inverse line transform of a register line
 // (only the dependency cone of II survives dead-code elimination).
 template <int N, int L, int II>
@@ -144,18 +175,13 @@ __device__ __forceinline__ double idwt_at(const double (&x)[N]) {
 // ghost value at the row that enters) stored with element stride S.
 template <int N, int S>
 __device__ __forceinline__ void store_streamed(double* dst, const double (&v)[N], int cx, double ghost) {
-    if (cx == 0) {
+    double* const d = dst + cx * S;  // out[i + cx] = v[i]
 #pragma unroll
-        for (int i = 0; i < N; ++i) dst[i * S] = v[i];
-    } else if (cx == 1) {
-        dst[0] = ghost;
-#pragma unroll
-        for (int i = 1; i < N; ++i) dst[i * S] = v[i - 1];
-    } else {
-#pragma unroll
-        for (int i = 0; i < N - 1; ++i) dst[i * S] = v[i + 1];
-        dst[(N - 1) * S] = ghost;
-    }
+    for (int i = 1; i < N - 1; ++i) d[i * S] = v[i];
+    if (cx >= 0) d[0] = v[0];
+    if (cx <= 0) d[(N - 1) * S] = v[N - 1];
+    if (cx == 1) dst[0] = ghost;
+    if (cx == -1) dst[(N - 1) * S] = ghost;
 }
 
 template <int N>
@@ -167,7 +193,7 @@ struct PairLayout {
     static constexpr int BUFD = (NN + 1) & ~1;    // doubles per population buffer (16-byte multiple)
     static constexpr int NBUF = 5;                // slot 0: population 0 replica, slots 1..4: own populations
     static constexpr size_t kSmemMax = 232448;    // 227 KB per CTA (sm_100)
-    static constexpr size_t kStatic = 2048;       // static shared memory of the kernel (bound)
+    static constexpr size_t kStatic = 8192;       // static shared memory of the kernel (bound, checked at load)
     // + the scan array, the column-edge partials of the 4 own populations and
     // the per-thread mass accumulators
     static constexpr size_t fixed_bytes() {
@@ -192,11 +218,33 @@ struct SlotIn {
     const double* gv;        // the same block in global memory (re-derivation after the skip rule)
     const uint32_t* gcol;
     const uint32_t* gro;
-    const double* raw;       // IN_RAW: dense N x N block in global memory
-    uint32_t nnz, kind;
+    const double* raw;       // IN_RAW: dense N x N block in global memory (row pitch raw_ld)
+    uint32_t nnz, kind, raw_ld;
 };
 
-__host__ __device__ constexpr int pair_pop(int rank, int s) { return s == 0 ? 0 : (rank == 0 ? s : s + 4); }
+// Population of slot s on rank r: rank 0 owns {1, 3, 5, 6}, rank 1 owns
+// {2, 4, 7, 8} (two axis and two diagonal populations each: equal ghost and
+// edge-line work), slot 0 is population 0 on both.
+__host__ __device__ constexpr int pair_pop(int rank, int s) {
+    return (int)(((rank == 0 ? 0x65310u : 0x87420u) >> (4 * s)) & 15u);
+}
+__host__ __device__ constexpr int pop_owner(int q) { return q == 0 ? -1 : (int)((0x194u >> q) & 1u); }  // rank
+__host__ __device__ constexpr int pop_slot(int q) { return (int)((0x434322110ull >> (4 * q)) & 15u); }
+static_assert(pair_pop(0, 1) == 1 && pair_pop(0, 2) == 3 && pair_pop(0, 3) == 5 && pair_pop(0, 4) == 6 &&
+              pair_pop(1, 1) == 2 && pair_pop(1, 2) == 4 && pair_pop(1, 3) == 7 && pair_pop(1, 4) == 8);
+static_assert(pop_owner(1) == 0 && pop_owner(3) == 0 && pop_owner(5) == 0 && pop_owner(6) == 0 &&
+              pop_owner(2) == 1 && pop_owner(4) == 1 && pop_owner(7) == 1 && pop_owner(8) == 1);
+static_assert(pop_slot(1) == 1 && pop_slot(3) == 2 && pop_slot(5) == 3 && pop_slot(6) == 4 && pop_slot(2) == 1 &&
+              pop_slot(4) == 2 && pop_slot(7) == 3 && pop_slot(8) == 4);
+
+// Two inverse variants (instruction-cache budget): every detail level empty
+// (only the samples stored, the common well-compressed block: Z = L), or the
+// general inverse (Z = 0; exact for any content).
+template <int L, typename F>
+__device__ __forceinline__ void with_z2(int z, F&& f) {
+    if (z == L) f(std::integral_constant<int, L>{});
+    else f(std::integral_constant<int, 0>{});
+}
 
 // ---- the kernel -------------------------------------------------------------
 template <int N, int L, int MODE>
@@ -234,6 +282,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<N>::NT, 1
     __shared__ uint32_t cur_p;                  // the patch in flight (state lives in shared
     __shared__ int cur_it, cur_redo, cur_raw;   // memory: short register live ranges)
     __shared__ double red_m[NT / 32], red_f[NT / 32];
+    __shared__ double gh_row[4][N];             // ghost value streamed in along dim 0, per output column
+    __shared__ double gh_col[4][N];             // ghost column streamed in along dim 1
+    __shared__ uint8_t ilv[N];                  // register (interleaved) index of a corner position
 
     const int t = threadIdx.x;
     const ShardGeom& g = a.g;
@@ -269,32 +320,45 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<N>::NT, 1
     // ---- input prefetch of patch p into descriptor set `par` (thread 0) ----
     auto prefetch = [&](uint32_t p, int par) {
         const int rank = (int)cluster_rank();
+        DirEntry e[5];
+#pragma unroll
+        for (int sl = 0; sl < 5; ++sl)  // independent loads in flight together
+            e[sl] = (MODE != MODE_INIT && !a.raw_in) ? a.dir_in[(size_t)p * 9 + pair_pop(rank, sl)]
+                                                      : DirEntry{0, 0u, DIR_DEAD};
         unsigned used = 0;
+        unsigned char* src[5];
+        unsigned nb[5];
         for (int sl = 0; sl < 5; ++sl) {
             const int qq = pair_pop(rank, sl);
             SlotIn d{};
-            DirEntry e{0, 0u, DIR_DEAD};
-            if (MODE != MODE_INIT) e = a.dir_in[(size_t)p * 9 + qq];
-            if (e.flags & DIR_DEAD) {
-                d.kind = IN_DEAD;
-            } else if (e.flags & DIR_RAW) {
+            nb[sl] = 0;
+            if (MODE != MODE_INIT && a.raw_in) {  // streamed input: the grid buffer's logical block
+                constexpr size_t TP = N + 2;
                 d.kind = IN_RAW;
-                d.raw = reinterpret_cast<const double*>(a.store_in + e.off);
+                d.raw = a.raw_in + ((size_t)(p - a.p_begin) * 9 + qq) * TP * TP + TP + 1;
+                d.raw_ld = (uint32_t)TP;
+            } else if (e[sl].flags & DIR_DEAD) {
+                d.kind = IN_DEAD;
+            } else if (e[sl].flags & DIR_RAW) {
+                d.kind = IN_RAW;
+                d.raw = reinterpret_cast<const double*>(a.store_in + e[sl].off);
+                d.raw_ld = (uint32_t)N;
             } else {
                 d.kind = IN_CSR;
-                d.nnz = e.nnz;
-                const unsigned char* gb = a.store_in + e.off;
+                d.nnz = e[sl].nnz;
+                const unsigned char* gb = a.store_in + e[sl].off;
                 d.gv = reinterpret_cast<const double*>(gb);
-                d.gcol = reinterpret_cast<const uint32_t*>(gb + 8ull * e.nnz);
-                d.gro = d.gcol + e.nnz;
-                const unsigned bytes = (unsigned)round16(12ull * e.nnz + 4ull * (N + 1));
+                d.gcol = reinterpret_cast<const uint32_t*>(gb + 8ull * e[sl].nnz);
+                d.gro = d.gcol + e[sl].nnz;
+                const unsigned bytes = (unsigned)round16(12ull * e[sl].nnz + 4ull * (N + 1));
                 if (used + bytes <= STAGE) {
                     unsigned char* sb = stage + used;
-                    bulk_g2s(sb, gb, bytes, &mbar);
-                    used += bytes;
+                    src[sl] = const_cast<unsigned char*>(gb);
+                    nb[sl] = bytes;
                     d.v = reinterpret_cast<const double*>(sb);
-                    d.col = reinterpret_cast<const uint32_t*>(sb + 8ull * e.nnz);
-                    d.ro = d.col + e.nnz;
+                    d.col = reinterpret_cast<const uint32_t*>(sb + 8ull * e[sl].nnz);
+                    d.ro = d.col + e[sl].nnz;
+                    used += bytes;
                 } else {  // does not fit the staging area: decoded from global memory
                     d.v = d.gv;
                     d.col = d.gcol;
@@ -303,57 +367,82 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<N>::NT, 1
             }
             slot_in[par][sl] = d;
         }
-        mbar_arrive_expect(&mbar, used);
+        mbar_arrive_expect(&mbar, used);  // the transaction count first, then the copies
+        for (int sl = 0; sl < 5; ++sl)
+            if (nb[sl]) bulk_g2s(const_cast<double*>(slot_in[par][sl].v), src[sl], nb[sl], &mbar);
     };
 
+    // The ghost values of the own populations of patch p (sync_ghosts,
+    // patchgrid.hpp:131-201), gathered by all threads from the neighbours'
+    // edge lines (the previous step's output): per output column j of D2 the
+    // value streamed in along dim 0, L(-1, j - cy) (cx = +1) or L(N, j - cy)
+    // (cx = -1), corners from the diagonal neighbours; and the column
+    // streamed in along dim 1.  Issued at the end of the previous patch, so
+    // its L2 latency overlaps that patch's tail.
+    auto gather_ghosts = [&](uint32_t p) {
+        if constexpr (MODE == MODE_STEP || MODE == MODE_STEP_LZ) {
+            const int rank = (int)cluster_rank();
+            const PatchPos pp = patch_pos(p, g);
+            for (int k = t; k < 8 * N; k += NT) {
+                const int which = k / (4 * N), rem = k - which * 4 * N, sl = 1 + rem / N, j = rem - (sl - 1) * N;
+                const int q = pair_pop(rank, sl), cx = lbm_cx(q), cy = lbm_cy(q);
+                if (which == 0) {
+                    if (cx == 0) continue;
+                    const int jc = j - cy;
+                    const uint32_t bcol = jc < 0 ? pp.bl : (jc >= N ? pp.br : pp.b);
+                    const int pos = jc < 0 ? N - 2 : (jc >= N ? 1 : jc);
+                    cp_async8(&gh_row[sl - 1][j], cx == 1 ? a.ein.rowhi + edge_ix(pp.su, bcol, lbm_slot_rowhi(q), g, N) + pos
+                                                          : a.ein.rowlo + edge_ix(pp.sd, bcol, lbm_slot_rowlo(q), g, N) + pos);
+                } else {
+                    if (cy == 0) continue;
+                    cp_async8(&gh_col[sl - 1][j], cy == 1 ? a.ein.colhi + edge_ix(pp.ar, pp.bl, lbm_slot_colhi(q), g, N) + j
+                                                          : a.ein.collo + edge_ix(pp.ar, pp.br, lbm_slot_collo(q), g, N) + j);
+                }
+            }
+        }
+    };
+
+    for (int k = t; k < N; k += NT) ilv[k] = (uint8_t)interleaved_of<N, L>(k);
     if (t == 0) {
         mbar_init(&mbar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         cs.cur = cs.end = 0;
-        part = StepPartial{0, 0, 0, 0.0, 0.0, 0.0};
+        part = a.chunk_first ? StepPartial{0, 0, 0, 0.0, 0.0, 0.0} : a.partials[blockIdx.x];
     }
     __syncthreads();
     cluster_sync_all();  // the peer CTA runs before any DSMEM access
-    if (t == 0 && pair < g.npatch) prefetch(pair, 0);
+    const uint32_t p_end = a.p_end;
+    if (t == 0 && a.p_begin + pair < p_end) prefetch(a.p_begin + pair, 0);
+    if (a.p_begin + pair < p_end) gather_ghosts(a.p_begin + pair);
+    cp_async_wait_all();
+    __syncthreads();
+    WG_PHASE_MARK(-1);
 
     unsigned phase = 0;
     if (t == 0) {
-        cur_p = pair;
+        cur_p = a.p_begin + pair;
         cur_it = 0;
+        ppos = patch_pos(cur_p, g);
+        cur_redo = 0;
+        cur_raw = 0;
+    }
+    if (t < 5) {
+        rmask[t] = Bits128{0ull, 0ull};
+        slot_top[t] = -1;
     }
     __syncthreads();
     for (;;) {
-        if (cur_p >= g.npatch) break;
-        // D0: inputs arrived; row masks of the stored blocks
+        if (cur_p >= p_end) break;
+        // D0: inputs arrived; row masks of the stored blocks and the ghost
+        // values, gathered by all threads (no barrier: D1's covers them; the
+        // per-patch state was reset at the end of the previous patch)
+        WG_PHASE_MARK(12);
         mbar_wait(&mbar, phase);
         phase ^= 1u;
-        if (t < 5) {
-            rmask[t] = Bits128{0ull, 0ull};
-            slot_top[t] = -1;
-        }
-        if (t == 0) {
-            ppos = patch_pos(cur_p, g);
-            cur_redo = 0;
-            cur_raw = 0;
-        }
+        WG_PHASE_MARK(13);
         acc_m[t] = 0.0;
         acc_f[t] = 0.0;
-        __syncthreads();
-        WG_PHASE_MARK(-1);
         const int par = cur_it & 1;
-        if (MODE != MODE_INIT) {
-            for (int k = t; k < 5 * N; k += NT) {
-                const int sl = k / N, r = k - sl * N;
-                const SlotIn& d = slot_in[par][sl];
-                const bool ne = d.kind == IN_CSR ? d.ro[r + 1] > d.ro[r] : d.kind == IN_RAW;
-                if (ne) {
-                    if (r < 64) atomicOr(&rmask[sl].lo, 1ull << r);
-                    else atomicOr(&rmask[sl].hi, 1ull << (r - 64));
-                }
-            }
-        }
-        __syncthreads();
-
         // produce the post-collide state (D1, D2, C); pass 1 re-derives the
         // state of a skip-rule patch after the transform overwrote it
         for (;;) {
@@ -372,7 +461,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<N>::NT, 1
                     const double uy = X <= 0.5 ? a.ic_u0 * tanh(a.ic_kappa * (X - 0.25))
                                                : a.ic_u0 * tanh(a.ic_kappa * (0.75 - X));
                     const double ux = a.ic_delta * a.ic_u0 * sin(2.0 * 3.141592653589793 * (Y + 0.25));
-                    const double usq = ux * ux + uy * uy;
+                    const double usq = lbm_usq(ux, uy);
 #pragma unroll
                     for (int sl = 0; sl < 5; ++sl) {
                         const int qq = pair_pop(rank, sl);
@@ -381,9 +470,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<N>::NT, 1
                     }
                 }
                 __syncthreads();
-                if (t == 0 && !cur_redo && cur_p + npairs < g.npatch) prefetch(cur_p + npairs, par ^ 1);
+                if (t == 0 && !cur_redo && cur_p + npairs < p_end) prefetch(cur_p + npairs, par ^ 1);
                 cluster_sync_all();
             } else {
+                WG_PHASE_MARK(14);
+                if (cur_redo) {  // skip-rule re-derivation: this patch's ghosts again
+                    cp_async_wait_all();
+                    __syncthreads();
+                    gather_ghosts(cur_p);
+                    cp_async_wait_all();
+                }
                 // D1: decode rows (own slots: row li; population 0: every row,
 
                 // strided).  The pull-streaming shift along dim 1 commutes with
@@ -400,16 +496,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<N>::NT, 1
                         const uint32_t* ro = redo ? d.gro : d.ro;
                         const uint32_t k0 = ro[r], k1 = ro[r + 1];
                         if (k0 == k1) return;
+                        // the column pass reads only the rows that decode to something
+                        if (r < 64) atomicOr(&rmask[&d - &slot_in[par][0]].lo, 1ull << r);
+                        else atomicOr(&rmask[&d - &slot_in[par][0]].hi, 1ull << (r - 64));
                         WG_CHECK(k1 <= d.nnz && k0 < k1, 1);
                         double* rowp = Bs + (size_t)r * N;
-                        const int z = z_of_top(N, L, (int)cc[k1 - 1]);
-                        const int top = z_top(N, z);
+                        // two variants: only sample columns stored (Z = L) or general
+                        const int z = z_of_top(N, L, (int)cc[k1 - 1]) == L ? L : 0;
+                        const int top = z_top(N, z);  // the positions the variant reads
                         for (int jj = 0; jj <= top; ++jj) rowp[jj] = 0.0;
                         for (uint32_t k = k0; k < k1; ++k) {
                             WG_CHECK(cc[k] < (uint32_t)N, 2);
                             rowp[cc[k]] = vv[k];
                         }
-                        with_z<L>(z, [&](auto ZC) {
+                        with_z2<L>(z, [&](auto ZC) {
                             constexpr int Z = decltype(ZC)::value;
                             double x[N];
 #pragma unroll
@@ -430,7 +530,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<N>::NT, 1
                 WG_PHASE_MARK(21);
                 // next patch's inputs: the staging area is free once D1 has run
                 // (the skip rule's re-derivation reads the global copies)
-                if (t == 0 && !cur_redo && cur_p + npairs < g.npatch) {
+                if (t == 0 && !cur_redo && cur_p + npairs < p_end) {
                     fence_proxy_async();
                     prefetch(cur_p + npairs, par ^ 1);
                 }
@@ -445,19 +545,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<N>::NT, 1
                     double* const Bs = bufs + (size_t)jb.s * BUFD;
                     const int jc = (MODE == MODE_DECODE) ? j : j - cy;
                     const SlotIn& d = slot_in[par][jb.s];
-                    const PatchPos pp = ppos;
-                    double ghost = 0.0;
-                    if (MODE != MODE_DECODE && cx != 0) {
-                        // ghost value of the streamed-in row: L(-1, jc) (cx = +1) or L(N, jc) (cx = -1)
-                        const uint32_t bcol = jc < 0 ? pp.bl : (jc >= N ? pp.br : pp.b);
-                        const int pos = jc < 0 ? N - 2 : (jc >= N ? 1 : jc);
-                        ghost = cx == 1 ? a.ein.rowhi[edge_ix(pp.su, bcol, lbm_slot_rowhi(q), g, N) + pos]
-                                        : a.ein.rowlo[edge_ix(pp.sd, bcol, lbm_slot_rowlo(q), g, N) + pos];
-                    }
+                    const double ghost = (MODE != MODE_DECODE && cx != 0) ? gh_row[jb.s - 1][j] : 0.0;
                     auto emit = [&](const double (&v)[N]) {
                         if (MODE == MODE_DECODE) {
                             constexpr int TP = N + 2;
-                            double* out = a.decode_out + ((size_t)cur_p * 9 + q) * (size_t)TP * TP + TP + 1 + j;
+                            double* out = a.decode_out + ((size_t)(cur_p - a.p_begin) * 9 + q) * (size_t)TP * TP + TP + 1 + j;
 #pragma unroll
                             for (int i = 0; i < N; ++i) out[i * TP] = v[i];
                         } else {
@@ -466,14 +558,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<N>::NT, 1
                     };
                     double v[N];
                     if (jc < 0 || jc >= N) {  // a ghost column: the neighbour's edge line
-                        const double* gl = jc < 0 ? a.ein.colhi + edge_ix(pp.ar, pp.bl, lbm_slot_colhi(q), g, N)
-                                                  : a.ein.collo + edge_ix(pp.ar, pp.br, lbm_slot_collo(q), g, N);
+                        const double* gl = gh_col[jb.s - 1];
 #pragma unroll
                         for (int i = 0; i < N; ++i) v[i] = gl[i];
                         emit(v);
                     } else if (d.kind == IN_RAW) {
 #pragma unroll
-                        for (int i = 0; i < N; ++i) v[i] = d.raw[(size_t)i * N + jc];
+                        for (int i = 0; i < N; ++i) v[i] = d.raw[(size_t)i * d.raw_ld + jc];
                         emit(v);
                     } else if (d.kind == IN_DEAD) {
 #pragma unroll
@@ -484,7 +575,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<N>::NT, 1
                         int top = -1;
                         if (m.hi) top = 64 + 63 - __clzll((long long)m.hi);
                         else if (m.lo) top = 63 - __clzll((long long)m.lo);
-                        with_z<L>(z_of_top(N, L, top), [&](auto ZC) {
+                        with_z2<L>(z_of_top(N, L, top), [&](auto ZC) {
                             constexpr int Z = decltype(ZC)::value;
 #pragma unroll
                             for (int rr = 0; rr < N; ++rr) {
@@ -497,57 +588,61 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<N>::NT, 1
                     }
                 }
                 if (MODE == MODE_DECODE) break;
-                __syncthreads();
                 WG_PHASE_MARK(22);
-                cluster_sync_all();  // both halves streamed
+                cluster_sync_cta();  // both halves streamed
                 WG_PHASE_MARK(23);
-                // C: BGK collide of this CTA's column half (lbm_collide, physics.cuh)
+                // D2 has read the ghosts: gather the next patch's (asynchronously,
+                // completed at the end of this patch)
+                if (cur_p + npairs < p_end) gather_ghosts(cur_p + npairs);
+                // C: BGK collide of this CTA's column half (lbm_collide, physics.cuh);
+                // the mass of the scheme output (strict check) as w * rho per
+                // cell (BGK conserves it; a tolerance-checked diagnostic)
                 {
                     const unsigned rank = cluster_rank(), peer = rank ^ 1u;
                     cg::cluster_group cluster = cg::this_cluster();
-                    const int lo = half_lo(), H = half_n();
                     double* P[9];  // population pointers (the peer's populations through DSMEM)
 #pragma unroll
                     for (int k = 0; k < 9; ++k) {
-                        const bool mine = k == 0 || (rank == 0 ? (k >= 1 && k <= 4) : (k >= 5));
-                        const int sl = k == 0 ? 0 : (k <= 4 ? k : k - 4);
+                        const bool mine = k == 0 || pop_owner(k) == (int)rank;
+                        const int sl = pop_slot(k);
                         P[k] = mine ? bufs + (size_t)sl * BUFD : cluster.map_shared_rank(bufs + (size_t)sl * BUFD, peer);
                     }
-                    constexpr int K = 2;
-                    const int cells = N * H;
                     const bool redo = cur_redo != 0;
-                    double mfv = 0.0;
-                    for (int c0 = t; c0 < cells; c0 += K * NT) {
-                        double f[K][9];
-                        int o[K];
-                        double w[K];
+                    auto collide_half = [&](auto HC, auto LOC) {
+                        constexpr int H = decltype(HC)::value, lo = decltype(LOC)::value, cells = N * H;
+                        constexpr int K = WG_LBM_CELLS;  // cells per iteration (independent chains)
+                        double mfv = 0.0;
+                        for (int c0 = t; c0 < cells; c0 += K * NT) {
+                            double f[K][9];
+                            int o[K];
+                            double w[K];
 #pragma unroll
-                        for (int u = 0; u < K; ++u) {
-                            const int c = c0 + u * NT;
-                            const int cc = c < cells ? c : c0;
-                            const int i = cc / H, jj = lo + (cc - i * H);
-                            o[u] = i * N + jj;
-                            w[u] = ((i == 0 || i == N - 1) ? 0.5 : 1.0) * ((jj == 0 || jj == N - 1) ? 0.5 : 1.0);
+                            for (int u = 0; u < K; ++u) {
+                                const int c = c0 + u * NT;
+                                const int cc = c < cells ? c : c0;
+                                const int i = cc / H, jj = lo + (cc - i * H);
+                                o[u] = i * N + jj;
+                                w[u] = ((i == 0 || i == N - 1) ? 0.5 : 1.0) * ((jj == 0 || jj == N - 1) ? 0.5 : 1.0);
 #pragma unroll
-                            for (int k = 0; k < 9; ++k) f[u][k] = P[k][o[u]];
-                        }
+                                for (int k = 0; k < 9; ++k) f[u][k] = P[k][o[u]];
+                            }
 #pragma unroll
-                        for (int u = 0; u < K; ++u) lbm_collide(f[u], a.omega);
+                            for (int u = 0; u < K; ++u) {
+                                const double rho = lbm_collide(f[u], a.omega);
+                                if (c0 + u * NT < cells) {
 #pragma unroll
-                        for (int u = 0; u < K; ++u) {
-                            if (c0 + u * NT < cells) {
-#pragma unroll
-                                for (int k = 0; k < 9; ++k) {
-                                    P[k][o[u]] = f[u][k];
-                                    if (!redo) mfv += w[u] * f[u][k];
+                                    for (int k = 0; k < 9; ++k) P[k][o[u]] = f[u][k];
+                                    mfv += w[u] * rho;
                                 }
                             }
                         }
-                    }
-                    acc_f[t] += mfv;
+                        if (!redo) acc_f[t] += mfv;
+                    };
+                    if (rank == 0) collide_half(std::integral_constant<int, H0>{}, std::integral_constant<int, 0>{});
+                    else collide_half(std::integral_constant<int, N - H0>{}, std::integral_constant<int, H0>{});
                 }
                 WG_PHASE_MARK(24);
-                cluster_sync_all();  // the peer's populations are written back
+                cluster_sync_cta();  // the peer's populations are written back
                 WG_PHASE_MARK(25);
             }
             if (cur_redo || !a.compress) {  // the collided state, to be stored raw
@@ -576,11 +671,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<N>::NT, 1
                     }
                 }
             }
-            cluster_sync_all();  // population 0's replicas hold both column halves
+            cluster_sync_cta();  // population 0's replicas hold both column halves
             WG_PHASE_MARK(26);
             // F2: forward transform along dim 1 (rows) + threshold (threshold.hpp:51-86);
             // the thresholded row is parked in its own buffer row across the barriers
             unsigned long long cnt = 0;  // zeroed << 32 | nnz of this row
+            bool samp_only = true;       // every kept coefficient of the row is a sample (column)
             {
                 const Job jb = job_of();
                 if (jb.on) {
@@ -602,20 +698,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<N>::NT, 1
                             lz[corner_pos<N, L>(rr)] = (y != 0.0 && fabs(y) < trow[band_of_r<N, L>(rr)]) ? 0.0 : y;
                         }
                     }
-                    // kept / zeroed flags as bit masks (one predicated OR each), counted by popc
-                    unsigned long long km[2] = {0ull, 0ull}, zm[2] = {0ull, 0ull};
+                    // kept / nonzero flags as bit masks (one predicated OR each), counted by popc
+                    unsigned long long km[2] = {0ull, 0ull}, nm[2] = {0ull, 0ull};
 #pragma unroll
                     for (int rr = 0; rr < N; ++rr) {
                         const double y = x[rr];
                         const bool nzx = y != 0.0;
-                        const bool kill = fabs(y) < trow[band_of_r<N, L>(rr)];
-                        const bool keep = nzx && !kill;
+                        const bool keep = nzx && !(fabs(y) < trow[band_of_r<N, L>(rr)]);
                         if (keep) km[rr >> 6] |= 1ull << (rr & 63);
-                        if (nzx && kill) zm[rr >> 6] |= 1ull << (rr & 63);
-                        x[rr] = keep ? y : 0.0;
+                        if (nzx) nm[rr >> 6] |= 1ull << (rr & 63);
                     }
                     const unsigned nz = (unsigned)(__popcll(km[0]) + __popcll(km[1]));
-                    const unsigned zr = (unsigned)(__popcll(zm[0]) + __popcll(zm[1]));
+                    const unsigned zr = (unsigned)(__popcll(nm[0]) + __popcll(nm[1])) - nz;
+                    {
+                        constexpr Bits128 SAMP = sample_bits<N, L>();
+                        samp_only = ((km[0] & ~SAMP.lo) | (km[1] & ~SAMP.hi)) == 0ull;
+                    }
+                    if (nz) {  // the thresholded row (killed -> +0.0, -0.0 -> +0.0 like the CSR round trip)
+#pragma unroll
+                        for (int rr = 0; rr < N; ++rr) x[rr] = ((km[rr >> 6] >> (rr & 63)) & 1ull) ? x[rr] : 0.0;
+                    }
                     if (nz) atomicMax(&slot_top[jb.s], r);
                     // mass of the reconstruction: sum_rc a_r a_c C[r][c] (trapezoid
                     // functional of idwt_nd, host-computed exact dyadic values; for
@@ -634,8 +736,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<N>::NT, 1
                         if (nz) val = jb.cy == -1 ? idwt_at<N, L, 1>(x) : idwt_at<N, L, N - 2>(x);
                         side[(size_t)(jb.s - 1) * N + r] = val;
                     }
+                    // park the row for W (a row without kept coefficients is
+                    // needed only as zeros of a cone row of the row edge line)
+                    const bool cone_row = jb.s > 0 && jb.cx != 0 && (jb.cx == -1 ? CONE_LO : CONE_HI).has(r);
+                    if (nz) {
 #pragma unroll
-                    for (int rr = 0; rr < N; ++rr) rowp[rr] = x[rr];  // interleaved order
+                        for (int rr = 0; rr < N; ++rr) rowp[rr] = x[rr];  // interleaved order
+                    } else if (cone_row) {
+#pragma unroll
+                        for (int rr = 0; rr < N; ++rr) rowp[rr] = 0.0;
+                    }
                     cnt = ((unsigned long long)zr << 32) | nz;
                 }
             }
@@ -650,7 +760,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<N>::NT, 1
                 cg::cluster_group cluster = cg::this_cluster();
                 cluster.map_shared_rank(mail_tot, peer_of())[t] = slot_tot[t];
             }
-            cluster_sync_all();  // M1: the pair's counts exchanged
+            cluster_sync_cta();  // M1: the pair's counts exchanged
             WG_PHASE_MARK(28);
             const bool cycle = a.thr_any != 0;
             if (t == 0) {
@@ -668,16 +778,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<N>::NT, 1
                 part.zeroed += zr_m;
                 skip_patch = (zero == 0) || !cycle;
                 if (!skip_patch) {
-                    for (int sl = (rank == 0 ? 0 : 1); sl < 5; ++sl) {
+                    // one allocation for the blocks this CTA owns (population 0's by rank 0)
+                    const int s0 = rank == 0 ? 0 : 1;
+                    uint64_t total = 0;
+                    for (int sl = s0; sl < 5; ++sl) {
+                        slot_nnz[sl] = (uint32_t)(slot_tot[sl] & 0xffffffffull) +
+                                       (sl == 0 ? (uint32_t)(mail_tot[0] & 0xffffffffull) : 0u);
+                        total += round16(12ull * slot_nnz[sl] + 4ull * (N + 1));
+                    }
+                    uint64_t off = chunk_alloc(a, cs, total);
+                    const bool ok = off != ~0ull;
+                    for (int sl = s0; sl < 5; ++sl) {
                         const int qq = pair_pop((int)rank, sl);
-                        const uint32_t bnnz = (uint32_t)(slot_tot[sl] & 0xffffffffull) +
-                                              (sl == 0 ? (uint32_t)(mail_tot[0] & 0xffffffffull) : 0u);
-                        const uint64_t off = chunk_alloc(a, cs, round16(12ull * bnnz + 4ull * (N + 1)));
-                        slot_ok[sl] = off != ~0ull;
+                        slot_ok[sl] = ok;
                         slot_off[sl] = off;
-                        slot_nnz[sl] = bnnz;
                         slot_k0[sl] = 0;
-                        a.dir_out[(size_t)cur_p * 9 + qq] = slot_ok[sl] ? DirEntry{off, bnnz, 0u} : DirEntry{0, 0u, DIR_DEAD};
+                        a.dir_out[(size_t)cur_p * 9 + qq] = ok ? DirEntry{off, slot_nnz[sl], 0u} : DirEntry{0, 0u, DIR_DEAD};
+                        if (ok) off += round16(12ull * slot_nnz[sl] + 4ull * (N + 1));
                     }
                     cg::cluster_group cluster = cg::this_cluster();
                     if (rank == 0) {
@@ -689,7 +806,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<N>::NT, 1
                     }
                 }
             }
-            cluster_sync_all();  // M2: population 0's block offset delivered
+            cluster_sync_cta();  // M2: population 0's block offset delivered
             WG_PHASE_MARK(29);
             if (t == 0 && cluster_rank() == 1 && !skip_patch) {
                 slot_off[0] = mail_off0;
@@ -697,30 +814,66 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<N>::NT, 1
             }
             __syncthreads();
             if (!skip_patch) {
-                // W: CSR rows (csr_encode, codec.hpp:37-60) from the parked rows;
-                // the cone rows of the row edge line are inverse transformed in
-                // place (a thread only touches its own parked row)
+                // W: CSR blocks (csr_encode, codec.hpp:37-60) from the parked
+                // rows: each thread its row offset; the entries of a warp's
+                // non-empty rows written by the whole warp, one row at a time
+                // (ballot of the non-zeros, popc prefix: row-major, ascending
+                // columns); then the cone rows of the row edge line are
+                // inverse transformed in place (a thread only touches its own
+                // parked row)
                 const Job jb = job_of();
+                const unsigned nz = (unsigned)(cnt & 0xffffffffull);
+                uint32_t k = 0;
                 if (jb.on) {
-                    double* const rowp = bufs + (size_t)jb.s * BUFD + (size_t)jb.li * N;
-                    const int r = jb.li, s = jb.s;
-                    double x[N];
-#pragma unroll
-                    for (int rr = 0; rr < N; ++rr) x[rr] = rowp[rr];
-                    const unsigned nz = (unsigned)(cnt & 0xffffffffull);
-                    if (slot_ok[s]) {
-                        const int first = s == 0 ? 4 * N : (s - 1) * N;
-                        const unsigned long long before = first == 0 ? 0ull : inc[first - 1];
-                        const uint32_t k = (uint32_t)((inc[t] - before) & 0xffffffffull) - nz + slot_k0[s];
+                    const int s = jb.s;
+                    const int first = s == 0 ? 4 * N : (s - 1) * N;
+                    const unsigned long long before = first == 0 ? 0ull : inc[first - 1];
+                    k = (uint32_t)((inc[t] - before) & 0xffffffffull) - nz + slot_k0[s];
+                    if (slot_ok[s]) {  // row offsets: u32 from 0 (csr_encode)
+                        uint32_t* ro = reinterpret_cast<uint32_t*>(a.store_out + slot_off[s] + 12ull * slot_nnz[s]);
+                        if (jb.li == 0) ro[0] = 0;
+                        ro[jb.li + 1] = k + nz;
                         WG_CHECK(slot_off[s] + 12ull * slot_nnz[s] + 4ull * (N + 1) <= a.cap_out &&
                                      k + nz <= slot_nnz[s], 10);
-                        write_csr_row<N, L>(a.store_out + slot_off[s], slot_nnz[s], r, k, nz, x);
                     }
-                    if (s > 0 && jb.cx != 0 && nz && (jb.cx == -1 ? CONE_LO : CONE_HI).has(r)) {
-                        idwt_line_reg<N, L>(x);
+                }
+                {
+                    const int lane = t & 31;
+                    unsigned todo = __ballot_sync(0xffffffffu, jb.on && nz != 0 && slot_ok[jb.s]);
+                    while (todo) {
+                        const int src = __ffs(todo) - 1;
+                        todo &= todo - 1;
+                        const int s_ = __shfl_sync(0xffffffffu, jb.s, src), r_ = __shfl_sync(0xffffffffu, jb.li, src);
+                        uint32_t k_ = __shfl_sync(0xffffffffu, k, src);
+                        const double* row = bufs + (size_t)s_ * BUFD + (size_t)r_ * N;  // interleaved order
+                        unsigned char* const blk = a.store_out + slot_off[s_];
+                        double* vo = reinterpret_cast<double*>(blk);
+                        uint32_t* co = reinterpret_cast<uint32_t*>(blk + 8ull * slot_nnz[s_]);
+#pragma unroll
+                        for (int base = 0; base < N; base += 32) {
+                            const int pc = base + lane;  // corner-layout column
+                            const double xv = pc < N ? row[ilv[pc < N ? pc : 0]] : 0.0;
+                            const unsigned m = __ballot_sync(0xffffffffu, xv != 0.0);
+                            if (xv != 0.0) {
+                                const uint32_t o = k_ + (uint32_t)__popc(m & ((1u << lane) - 1u));
+                                vo[o] = xv;
+                                co[o] = (uint32_t)pc;
+                            }
+                            k_ += (uint32_t)__popc(m);
+                        }
+                    }
+                    __syncwarp();
+                }
+                if (jb.on && nz && jb.s > 0 && jb.cx != 0 && (jb.cx == -1 ? CONE_LO : CONE_HI).has(jb.li)) {
+                    double* const rowp = bufs + (size_t)jb.s * BUFD + (size_t)jb.li * N;
+                    with_z2<L>(samp_only ? L : 0, [&](auto ZC) {
+                        double x[N];
+#pragma unroll
+                        for (int rr = 0; rr < N; ++rr) x[rr] = rowp[rr];
+                        idwt_line_reg<N, L, decltype(ZC)::value>(x);
 #pragma unroll
                         for (int jj = 0; jj < N; ++jj) rowp[jj] = x[jj];  // natural order: Y[r][.]
-                    }
+                    });
                 }
                 __syncthreads();
                 WG_PHASE_MARK(30);
@@ -754,7 +907,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<N>::NT, 1
                         double* dst = cy == -1 ? a.eout.collo + edge_ix((uint32_t)pp.ar, pp.b, lbm_slot_collo(q), g, N)
                                                : a.eout.colhi + edge_ix((uint32_t)pp.ar, pp.b, lbm_slot_colhi(q), g, N);
                         const double* src = side + (size_t)(jb.s - 1) * N;
-                        with_z<L>(z_of_top(N, L, slot_top[jb.s]), [&](auto ZC) {
+                        with_z2<L>(z_of_top(N, L, slot_top[jb.s]), [&](auto ZC) {
                             constexpr int Z = decltype(ZC)::value;
                             double y[N];
 #pragma unroll
@@ -816,6 +969,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<N>::NT, 1
                 if (jb.cy == 1) a.eout.colhi[edge_ix((uint32_t)pp.ar, pp.b, lbm_slot_colhi(q), g, N) + li] = Bs[(size_t)li * N + N - 2];
             }
         }
+        cp_async_wait_all();  // the next patch's ghosts (issued after D2)
         // per-patch sums (fixed association: warps in order)
         if (MODE != MODE_DECODE) {
             __syncthreads();
@@ -845,6 +999,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<N>::NT, 1
         if (t == 0) {
             cur_p += npairs;
             ++cur_it;
+            ppos = patch_pos(cur_p, g);
+            cur_redo = 0;
+            cur_raw = 0;
+        }
+        if (t < 5) {
+            rmask[t] = Bits128{0ull, 0ull};
+            slot_top[t] = -1;
         }
         __syncthreads();
     }

@@ -109,6 +109,15 @@ struct StepArgs {
     // position (global_mass weights pulled through idwt_line): the mass of a
     // reconstructed block is sum_rc mass_a[r] mass_a[c] C[r][c]
     double mass_a[kMaxN];
+    // D2Q9 chunked launches (the streamed first step from a host initial
+    // state, chunked decode): this launch handles patches [p_begin, p_end);
+    // raw_in (non-null) holds their input in the grid-buffer layout
+    // ([patch][m][(n+2)^2], patches from p_begin) instead of the store;
+    // decode_out is indexed from p_begin.  The step's partial sums accumulate
+    // over the launches: chunk_first starts them, chunk_last reduces them.
+    const double* raw_in;
+    uint32_t p_begin, p_end;
+    int chunk_first, chunk_last;
 };
 
 // MODE_STEP_LZ: a step that also stages the thresholded coefficient arrays
@@ -663,6 +672,10 @@ __device__ __forceinline__ void finalize_step(const StepArgs& a, const StepParti
     __syncthreads();
     if (!am_last || threadIdx.x >= 32) return;
     __threadfence();
+    if (!a.chunk_last) {  // a chunk of a step: partials stay for the next launch
+        if (threadIdx.x == 0) *a.done = 0;
+        return;
+    }
     const int lane = threadIdx.x;
     unsigned long long cb = 0, nz = 0, zr = 0;
     double m = 0.0, mf = 0.0, l2 = 0.0;

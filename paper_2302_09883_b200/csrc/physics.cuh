@@ -250,12 +250,17 @@ __device__ __forceinline__ void swe_cell_fluxes(const double (&w)[3], const doub
 
 // ---- D2Q9 BGK (builder-defined, oracle/ref_shim.cpp) -------
 // q: 0 rest, 1 +x, 2 -x, 3 +y, 4 -y, 5 (+1,+1), 6 (-1,-1), 7 (+1,-1), 8 (-1,+1)
-__host__ __device__ constexpr int lbm_cx(int q) {
-    return q == 1 || q == 5 || q == 7 ? 1 : (q == 2 || q == 6 || q == 8 ? -1 : 0);
-}
-__host__ __device__ constexpr int lbm_cy(int q) {
-    return q == 3 || q == 5 || q == 8 ? 1 : (q == 4 || q == 6 || q == 7 ? -1 : 0);
-}
+// (c + 1) packed in 2 bits per q: a branch-free lookup for a runtime q
+constexpr unsigned kLbmCxP = (1u << 0) | (2u << 2) | (0u << 4) | (1u << 6) | (1u << 8) | (2u << 10) | (0u << 12) |
+                             (2u << 14) | (0u << 16);
+constexpr unsigned kLbmCyP = (1u << 0) | (1u << 2) | (1u << 4) | (2u << 6) | (0u << 8) | (2u << 10) | (0u << 12) |
+                             (0u << 14) | (2u << 16);
+__host__ __device__ constexpr int lbm_cx(int q) { return (int)((kLbmCxP >> (2 * q)) & 3u) - 1; }
+__host__ __device__ constexpr int lbm_cy(int q) { return (int)((kLbmCyP >> (2 * q)) & 3u) - 1; }
+static_assert(lbm_cx(1) == 1 && lbm_cx(2) == -1 && lbm_cx(5) == 1 && lbm_cx(6) == -1 && lbm_cx(7) == 1 &&
+              lbm_cx(8) == -1 && lbm_cx(0) == 0 && lbm_cx(3) == 0 && lbm_cx(4) == 0);
+static_assert(lbm_cy(3) == 1 && lbm_cy(4) == -1 && lbm_cy(5) == 1 && lbm_cy(6) == -1 && lbm_cy(7) == -1 &&
+              lbm_cy(8) == 1 && lbm_cy(0) == 0 && lbm_cy(1) == 0 && lbm_cy(2) == 0);
 __host__ __device__ constexpr double lbm_w(int q) {
     return q == 0 ? 4.0 / 9.0 : (q < 5 ? 1.0 / 9.0 : 1.0 / 36.0);
 }
@@ -274,20 +279,30 @@ __host__ __device__ __forceinline__ double lbm_cu(int q, double ux, double uy) {
     }
 }
 
+// Equilibrium, FMA form (the scheme's definition):
+//   feq_q = (w_q rho) * fma(cu, fma(4.5, cu, 3.0), fma(-1.5, usq, 1.0))
+//         = w_q rho (1 + 3 cu + 4.5 cu^2 - 1.5 u^2),  usq = fma(ux, ux, uy * uy)
+// Every fma is an explicit correctly rounded fused multiply-add (the C
+// oracles call C99 fma()), so host and device agree bit for bit.
+__host__ __device__ __forceinline__ double lbm_usq(double ux, double uy) { return fma(ux, ux, uy * uy); }
 __host__ __device__ __forceinline__ double lbm_feq(int q, double rho, double cu, double usq) {
-    const double t = ((1.0 + 3.0 * cu) + (4.5 * cu) * cu) - 1.5 * usq;
+    const double t = fma(cu, fma(4.5, cu, 3.0), fma(-1.5, usq, 1.0));
     return (lbm_w(q) * rho) * t;
 }
 
-// BGK collide of the 9 pulled populations f (in place).
-__host__ __device__ __forceinline__ void lbm_collide(double (&f)[9], double omega) {
+// BGK collide of the 9 pulled populations f (in place); returns the density.
+//   rho = sum_q f_q (sequential), j = (x, y) momentum sums, u = j * (1 / rho)
+//   f_q <- fma(omega, feq_q - f_q, f_q)          (= f - (f - feq) omega)
+__host__ __device__ __forceinline__ double lbm_collide(double (&f)[9], double omega) {
     const double rho = ((((((((f[0] + f[1]) + f[2]) + f[3]) + f[4]) + f[5]) + f[6]) + f[7]) + f[8]);
     const double jx = ((f[1] - f[2]) + (f[5] - f[6])) + (f[7] - f[8]);
     const double jy = ((f[3] - f[4]) + (f[5] - f[6])) + (f[8] - f[7]);
-    const double ux = jx / rho, uy = jy / rho;
-    const double usq = ux * ux + uy * uy;
+    const double inv = 1.0 / rho;
+    const double ux = jx * inv, uy = jy * inv;
+    const double usq = lbm_usq(ux, uy);
 #pragma unroll
-    for (int q = 0; q < 9; ++q) f[q] = f[q] - (f[q] - lbm_feq(q, rho, lbm_cu(q, ux, uy), usq)) * omega;
+    for (int q = 0; q < 9; ++q) f[q] = fma(omega, lbm_feq(q, rho, lbm_cu(q, ux, uy), usq) - f[q], f[q]);
+    return rho;
 }
 
 }  // namespace wg

@@ -405,6 +405,10 @@ struct Session {
     uint32_t lz_ctas = 0;
     // pinned-host upload pipeline (created on first use)
     double* stage = nullptr;
+    // row-chunk staging of the streamed first step / chunked download (D2Q9)
+    double* rstage[3] = {nullptr, nullptr, nullptr};
+    uint32_t rstage_rows = 0;
+    cudaEvent_t rstage_ev[6] = {};
     cudaStream_t copy_stream = nullptr;
     cudaEvent_t stage_ev[4] = {};
     uint64_t launched = 0;  // SWE step launches (steps past t_end are no-ops)
@@ -477,6 +481,15 @@ struct Session {
         }
         cudaFree(stage);
         stage = nullptr;
+        for (auto& b : rstage) {
+            cudaFree(b);
+            b = nullptr;
+        }
+        for (auto& ev : rstage_ev)
+            if (ev) {
+                cudaEventDestroy(ev);
+                ev = nullptr;
+            }
         cudaFree(lz_dense);
         cudaFree(lz_done);
         lz_done = nullptr;
@@ -841,6 +854,11 @@ struct Session {
         }
         std::memcpy(a.thr, thr, sizeof(thr));
         std::memcpy(a.mass_a, mass_a, sizeof(mass_a));
+        a.raw_in = nullptr;
+        a.p_begin = 0;
+        a.p_end = sg.npatch;
+        a.chunk_first = 1;
+        a.chunk_last = 1;
         return a;
     }
 
@@ -949,8 +967,110 @@ struct Session {
         }
     }
 
+    // Row-chunk staging (D2Q9): three device buffers of rstage_rows patch
+    // rows of the grid-buffer layout each (~512 MB), allocated on first use.
+    uint64_t row_doubles() const { return (uint64_t)sg.P1 * sg.m * geo.tcount; }
+    void ensure_row_stage() {
+        if (rstage[0]) return;
+        const uint64_t per_row = row_doubles() * 8;
+        rstage_rows = (uint32_t)std::clamp<uint64_t>((512ull << 20) / std::max<uint64_t>(per_row, 1), 1, sg.R);
+        if (const char* e = std::getenv("WG_STREAM_ROWS"))  // test knob: rows per chunk
+            rstage_rows = (uint32_t)std::clamp<long>(std::atol(e), 1, (long)sg.R);
+        for (auto& b : rstage) b = dalloc<double>((uint64_t)rstage_rows * row_doubles());
+        for (auto& ev : rstage_ev) WG_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    }
+
+    // The first step of a run straight from a host initial state (grid-buffer
+    // layout, page-locked or pageable): the raw state is never stored.  Patch
+    // rows stream through the device in chunks (DMA on the copy stream); the
+    // edge lines of a chunk are built when it arrives, and the step kernel
+    // runs on the previous chunk with its raw input read from the staging
+    // buffer (StepArgs::raw_in), so the store holds only the compressed
+    // result — the reference's step 1 on its raw initial grid (pipeline.hpp:
+    // 138-155, 194-289) under a store budget smaller than the raw state (C4).
+    void step_from_host(const double* hgrid, double dt) {
+        if (ks.cluster < 2 || sg.world != 1 || is_swe())
+            raise(WG_INVALID_ARGUMENT, "streamed first step: one-shard D2Q9 sessions only");
+        ensure_row_stage();
+        // the state of an upload (wg_session_upload), without the raw store
+        cur = 0;
+        step = 0;
+        row0 = 0;
+        time = 0.0;
+        WG_CUDA(cudaMemsetAsync(bump, 0, 2 * sizeof(unsigned long long), stream));
+        if (lz_done) k_set_u64<<<1, 1, 0, stream>>>(lz_done, 0ull);
+        const uint32_t R = sg.R, RC = rstage_rows, C = (R + RC - 1) / RC;
+        cudaEvent_t* copied = rstage_ev;
+        cudaEvent_t* consumed = rstage_ev + 3;
+        for (int k = 0; k < 3; ++k) WG_CUDA(cudaEventRecord(consumed[k], stream));
+        auto dma_edges = [&](int b, uint32_t r0, uint32_t nr) {
+            WG_CUDA(cudaStreamWaitEvent(copy_stream, consumed[b], 0));
+            WG_CUDA(cudaMemcpyAsync(rstage[b], hgrid + (uint64_t)r0 * row_doubles(), (uint64_t)nr * row_doubles() * 8,
+                                    cudaMemcpyHostToDevice, copy_stream));
+            WG_CUDA(cudaEventRecord(copied[b], copy_stream));
+            WG_CUDA(cudaStreamWaitEvent(stream, copied[b], 0));
+            const uint64_t threads = (uint64_t)nr * sg.P1 * sg.m * N * N;
+            k_edges_from_grid<<<(unsigned)((threads + 255) / 256), 256, 0, stream>>>(rstage[b], N, sg, r0 * sg.P1,
+                                                                                      nr * sg.P1, edges[cur]);
+            WG_LAUNCH_CHECK("streamed edges");
+        };
+        if (C > 1) {  // the last patch row first: the periodic ghost source of row 0
+            dma_edges(2, R - 1, 1);
+            WG_CUDA(cudaEventRecord(consumed[2], stream));
+        }
+        dma_edges(0, 0, std::min(RC, R));
+        grow_rows(1);
+        StepArgs a = step_args(0, 1);
+        a.omega = 1.0 / cfg.lbm_tau;
+        a.step = 1;
+        a.time = dt;
+        a.row_out = rows;
+        a.mass_fv_out = mass_fv;
+        for (uint32_t c = 0; c < C; ++c) {
+            const uint32_t r0 = c * RC, nr = std::min(RC, R - r0);
+            if (c + 1 < C) dma_edges((int)((c + 1) % 3), r0 + RC, std::min(RC, R - r0 - RC));
+            a.raw_in = rstage[c % 3];
+            a.p_begin = r0 * sg.P1;
+            a.p_end = (r0 + nr) * sg.P1;
+            a.chunk_first = c == 0;
+            a.chunk_last = c + 1 == C;
+            (lz_dense ? ks.main_lz : ks.main)<<<grid, ks.threads, ks.smem, stream>>>(a);
+            WG_LAUNCH_CHECK("streamed step");
+            WG_CUDA(cudaEventRecord(consumed[c % 3], stream));
+        }
+        if (lz_dense) {
+            k_lz_sizes<<<lz_ctas, 32 * kLzWarps, 0, stream>>>(lz_dense, (uint64_t)sg.npatch * sg.m, N * N,
+                                                               LzFinal{lz_done, a.row_out, nullptr, nullptr});
+            WG_LAUNCH_CHECK("lz sizes");
+        }
+        cur = 1;
+        step = 1;
+        time = dt;
+    }
+
     void download(double* hgrid) {
         if (is_swe()) sync();  // the current pool follows the device step counter
+        if (ks.cluster > 1) {  // D2Q9: decoded in row chunks through the staging buffers
+            ensure_row_stage();
+            const uint32_t R = sg.R, RC = rstage_rows;
+            for (uint32_t r0 = 0, c = 0; r0 < R; r0 += RC, ++c) {
+                const uint32_t nr = std::min(RC, R - r0);
+                const int b = (int)(c % 2);
+                WG_CUDA(cudaEventSynchronize(rstage_ev[3 + b]));  // its previous copy-out is done
+                WG_CUDA(cudaMemsetAsync(rstage[b], 0, (uint64_t)nr * row_doubles() * 8, stream));
+                StepArgs a = step_args(cur, 1 - cur);
+                a.decode_out = rstage[b];
+                a.p_begin = r0 * sg.P1;
+                a.p_end = (r0 + nr) * sg.P1;
+                ks.decode<<<grid, ks.threads, ks.smem, stream>>>(a);
+                WG_LAUNCH_CHECK("decode");
+                WG_CUDA(cudaMemcpyAsync(hgrid + (uint64_t)r0 * row_doubles(), rstage[b],
+                                        (uint64_t)nr * row_doubles() * 8, cudaMemcpyDeviceToHost, stream));
+                WG_CUDA(cudaEventRecord(rstage_ev[3 + b], stream));
+            }
+            sync();
+            return;
+        }
         const uint64_t n = (uint64_t)sg.npatch * sg.m * geo.tcount;
         DevBuf<double> d(n);
         WG_CUDA(cudaMemsetAsync(d.p, 0, n * sizeof(double), stream));
@@ -1313,6 +1433,13 @@ wg_status wg_dev_session_upload(wg_session* s, const double* dev_grid) {
     return guard([&] { reinterpret_cast<Session*>(s)->upload_dev(dev_grid); });
 }
 
+wg_status wg_session_step_host(wg_session* s, const double* host_grid, double dt) {
+    return guard([&] {
+        if (!s || !host_grid) raise(WG_INVALID_ARGUMENT, "wg_session_step_host: null argument");
+        reinterpret_cast<Session*>(s)->step_from_host(host_grid, dt);
+    });
+}
+
 wg_status wg_session_init_device(wg_session* s) {
     return guard([&] { reinterpret_cast<Session*>(s)->init_device(); });
 }
@@ -1491,8 +1618,15 @@ wg_status wg_run(const wg_run_config* cfg, wg_metrics_row* rows, uint64_t max_ro
         cudaEvent_t e0, e1;
         WG_CUDA(cudaEventCreate(&e0));
         WG_CUDA(cudaEventCreate(&e1));
-        s.upload_host(grid.data());
+        // a raw initial state larger than the store budget streams into step 1
+        const bool streamed = cfg->scheme == WG_SCHEME_LBM_D2Q9 && !dts.empty() &&
+                              (uint64_t)s.sg.npatch * s.sg.m * round16((uint64_t)s.N * s.N * 8) > s.cap;
+        if (!streamed) s.upload_host(grid.data());
         WG_CUDA(cudaEventRecord(e0, s.stream));
+        if (streamed) {
+            s.step_from_host(grid.data(), dts[0]);
+            dts.erase(dts.begin());
+        }
         if (s.is_swe()) {
             // the step count is known only on the device: launch batches
             // sized from the current dt, then read the clock back

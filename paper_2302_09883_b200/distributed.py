@@ -94,14 +94,18 @@ def reduce_rows(rows: list[dict], dist, device) -> list[dict]:
     keys = ["dense_bytes", "compressed_bytes", "nnz", "zeroed"]
     device = collective_device(dist, device)
     ints = torch.tensor([[r[k] for k in keys] for r in rows], dtype=torch.int64, device=device)
-    mass = torch.tensor([r["global_mass"] for r in rows], dtype=torch.float64, device=device)
+    # global_mass and the transport l2 are sums over patches: each shard's
+    # share adds exactly (l2_scale is applied per shard, solver.hpp:302-304)
+    dbl = torch.tensor([[r["global_mass"], r.get("l2", 0.0)] for r in rows], dtype=torch.float64, device=device)
     dist.all_reduce(ints)
-    dist.all_reduce(mass)
+    dist.all_reduce(dbl)
     out = []
-    for r, iv, m in zip(rows, ints.tolist(), mass.tolist()):
+    for r, iv, (m, l2) in zip(rows, ints.tolist(), dbl.tolist()):
         o = dict(r)
         o.update(dict(zip(keys, iv)))
         o["global_mass"] = m
+        if "l2" in r:
+            o["l2"] = l2
         o["ratio"] = o["dense_bytes"] / o["compressed_bytes"] if o["compressed_bytes"] > 0 else 1.0
         out.append(o)
     return out
@@ -189,6 +193,18 @@ class ShardedSession:
     def upload(self, host_grid: np.ndarray):
         self.lib.check(self.lib.wg_session_upload(self.handle, abi.dptr(host_grid)))
         self._initial_exchange()
+
+    def step_host(self, host_grid: np.ndarray, dt: float = 1.0):
+        """Step 1 straight from a host initial state (wg_session_step_host:
+        the raw state streams through the device and never enters the store;
+        one-shard D2Q9, C4)."""
+        if self.shard.world != 1:
+            raise ValueError("step_host: one-shard sessions only")
+        self.lib.check(self.lib.wg_session_step_host(self.handle, abi.dptr(host_grid), dt))
+
+    def download(self, host_grid: np.ndarray):
+        """The decoded state of this shard into a host grid buffer."""
+        self.lib.check(self.lib.wg_session_download(self.handle, abi.dptr(host_grid)))
 
     def init_device(self):
         """Initial state generated and compressed on the device (C4/C5)."""

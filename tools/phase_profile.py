@@ -15,7 +15,8 @@ import bench  # noqa: E402
 from paper_2302_09883_b200 import abi, api  # noqa: E402
 from paper_2302_09883_b200.distributed import ShardInfo, ShardedSession  # noqa: E402
 
-LBM_NAMES = {21: "D0+D1 wait, masks, decode rows", 22: "D2 decode cols + stream", 23: "cluster sync (streamed)",
+LBM_NAMES = {12: "end of patch (sums, reset)", 13: "D0 mbarrier wait", 14: "D0 masks + ghost gather",
+             21: "D1 decode rows", 22: "D2 decode cols + stream", 23: "cluster sync (streamed)",
              24: "C collide", 25: "cluster sync (collided)", 26: "F1 col fwd + cluster sync", 27: "F2 row fwd + thr",
              28: "S scan + M1", 29: "alloc + M2", 30: "W CSR + cone rows", 31: "edge lines + patch sums"}
 NAMES = {0: "decode rows+ghosts", 1: "decode cols", 2: "FV + mass", 3: "sync before fwd", 4: "fwd col DWT",
