@@ -188,7 +188,11 @@ template <int N>
 struct PairLayout {
     static constexpr int H0 = (N + 1) / 2;        // rank 0's half of population 0 (columns / rows)
     static constexpr int JOBS = 4 * N + H0;       // line jobs of rank 0 (rank 1: one fewer)
-    static constexpr int NT = ((JOBS + 31) / 32) * 32;
+    // the line jobs' warps + one control warp (prefetch, allocation, mailbox,
+    // the serial column-edge inverses) — free in registers: 9-12 warps all
+    // get 168 registers per thread (3 warps per SM sub-partition)
+    static constexpr int NT = ((JOBS + 31) / 32) * 32 + 32;
+    static constexpr int CTL = NT - 32;  // first thread of the control warp
     static constexpr int NN = N * N;
     static constexpr int BUFD = (NN + 1) & ~1;    // doubles per population buffer (16-byte multiple)
     static constexpr int NBUF = 5;                // slot 0: population 0 replica, slots 1..4: own populations
@@ -251,7 +255,7 @@ template <int N, int L, int MODE>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<N>::NT, 1)
     k_lbm_pair(const __grid_constant__ StepArgs a) {
     using Lay = PairLayout<N>;
-    constexpr int NT = Lay::NT, NN = N * N, BUFD = Lay::BUFD, H0 = Lay::H0;
+    constexpr int NT = Lay::NT, NN = N * N, BUFD = Lay::BUFD, H0 = Lay::H0, CTL = Lay::CTL;
     constexpr size_t STAGE = Lay::stage_bytes();
     constexpr Bits128 CONE_LO = inverse_cone<N, L>(1), CONE_HI = inverse_cone<N, L>(N - 2);
 
@@ -403,7 +407,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<N>::NT, 1
     };
 
     for (int k = t; k < N; k += NT) ilv[k] = (uint8_t)interleaved_of<N, L>(k);
-    if (t == 0) {
+    if (t == CTL) {
         mbar_init(&mbar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         cs.cur = cs.end = 0;
@@ -412,23 +416,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<N>::NT, 1
     __syncthreads();
     cluster_sync_all();  // the peer CTA runs before any DSMEM access
     const uint32_t p_end = a.p_end;
-    if (t == 0 && a.p_begin + pair < p_end) prefetch(a.p_begin + pair, 0);
+    if (t == CTL && a.p_begin + pair < p_end) prefetch(a.p_begin + pair, 0);
     if (a.p_begin + pair < p_end) gather_ghosts(a.p_begin + pair);
     cp_async_wait_all();
     __syncthreads();
     WG_PHASE_MARK(-1);
 
     unsigned phase = 0;
-    if (t == 0) {
+    if (t == CTL) {
         cur_p = a.p_begin + pair;
         cur_it = 0;
         ppos = patch_pos(cur_p, g);
         cur_redo = 0;
         cur_raw = 0;
     }
-    if (t < 5) {
-        rmask[t] = Bits128{0ull, 0ull};
-        slot_top[t] = -1;
+    if (t >= CTL && t < CTL + 5) {
+        rmask[t - CTL] = Bits128{0ull, 0ull};
+        slot_top[t - CTL] = -1;
     }
     __syncthreads();
     for (;;) {
@@ -470,7 +474,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<N>::NT, 1
                     }
                 }
                 __syncthreads();
-                if (t == 0 && !cur_redo && cur_p + npairs < p_end) prefetch(cur_p + npairs, par ^ 1);
+                if (t == CTL && !cur_redo && cur_p + npairs < p_end) prefetch(cur_p + npairs, par ^ 1);
                 cluster_sync_all();
             } else {
                 WG_PHASE_MARK(14);
@@ -519,18 +523,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<N>::NT, 1
                             store_streamed<N, 1>(rowp, x, (MODE == MODE_DECODE) ? 0 : cy, 0.0);
                         });
                     };
-                    if (jb.on) {
+                    if (jb.on) {  // one call site (instruction cache): own slots one row, population 0 strided
                         double* Bs = bufs + (size_t)jb.s * BUFD;
-                        if (jb.s > 0) decode_row(Bs, slot_in[par][jb.s], jb.li, jb.cy);
-                        else
-                            for (int r = t - 4 * N; r < N; r += half_n()) decode_row(Bs, slot_in[par][0], r, 0);
+                        const int step = jb.s > 0 ? N : half_n();
+                        for (int r = jb.s > 0 ? jb.li : t - 4 * N; r < N; r += step)
+                            decode_row(Bs, slot_in[par][jb.s], r, jb.cy);
                     }
                 }
                 __syncthreads();
                 WG_PHASE_MARK(21);
                 // next patch's inputs: the staging area is free once D1 has run
                 // (the skip rule's re-derivation reads the global copies)
-                if (t == 0 && !cur_redo && cur_p + npairs < p_end) {
+                if (t == CTL && !cur_redo && cur_p + npairs < p_end) {
                     fence_proxy_async();
                     prefetch(cur_p + npairs, par ^ 1);
                 }
@@ -608,8 +612,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<N>::NT, 1
                         P[k] = mine ? bufs + (size_t)sl * BUFD : cluster.map_shared_rank(bufs + (size_t)sl * BUFD, peer);
                     }
                     const bool redo = cur_redo != 0;
-                    auto collide_half = [&](auto HC, auto LOC) {
-                        constexpr int H = decltype(HC)::value, lo = decltype(LOC)::value, cells = N * H;
+                    {
+                        // one code path for both ranks: H0 columns from lo (rank 1's
+                        // half is one column narrower: that column's cells are skipped)
+                        constexpr int H = H0, cells = N * H;
+                        const int lo = half_lo();
                         constexpr int K = WG_LBM_CELLS;  // cells per iteration (independent chains)
                         double mfv = 0.0;
                         for (int c0 = t; c0 < cells; c0 += K * NT) {
@@ -620,7 +627,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<N>::NT, 1
                             for (int u = 0; u < K; ++u) {
                                 const int c = c0 + u * NT;
                                 const int cc = c < cells ? c : c0;
-                                const int i = cc / H, jj = lo + (cc - i * H);
+                                const int i = cc / H, jj = min(lo + (cc - i * H), N - 1);
                                 o[u] = i * N + jj;
                                 w[u] = ((i == 0 || i == N - 1) ? 0.5 : 1.0) * ((jj == 0 || jj == N - 1) ? 0.5 : 1.0);
 #pragma unroll
@@ -629,7 +636,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<N>::NT, 1
 #pragma unroll
                             for (int u = 0; u < K; ++u) {
                                 const double rho = lbm_collide(f[u], a.omega);
-                                if (c0 + u * NT < cells) {
+                                const int c = c0 + u * NT;
+                                if (c < cells && lo + (c % H) < N) {
 #pragma unroll
                                     for (int k = 0; k < 9; ++k) P[k][o[u]] = f[u][k];
                                     mfv += w[u] * rho;
@@ -637,16 +645,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<N>::NT, 1
                             }
                         }
                         if (!redo) acc_f[t] += mfv;
-                    };
-                    if (rank == 0) collide_half(std::integral_constant<int, H0>{}, std::integral_constant<int, 0>{});
-                    else collide_half(std::integral_constant<int, N - H0>{}, std::integral_constant<int, H0>{});
+                    }
                 }
                 WG_PHASE_MARK(24);
                 cluster_sync_cta();  // the peer's populations are written back
                 WG_PHASE_MARK(25);
             }
             if (cur_redo || !a.compress) {  // the collided state, to be stored raw
-                if (t == 0) cur_raw = 1;
+                if (t == CTL) cur_raw = 1;
                 break;
             }
 
@@ -752,18 +758,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<N>::NT, 1
             WG_PHASE_MARK(27);
             // S: CTA scan of the counts in job order, per-slot totals, mailbox
             cta_inclusive_scan<NT>(cnt, inc);
-            if (t < 5) {
-                const int first = t == 0 ? 4 * N : (t - 1) * N;
-                const int n = t == 0 ? half_n() : N;
+            if (t >= CTL && t < CTL + 5) {
+                const int u = t - CTL;
+                const int first = u == 0 ? 4 * N : (u - 1) * N;
+                const int n = u == 0 ? half_n() : N;
                 const unsigned long long before = first == 0 ? 0ull : inc[first - 1];
-                slot_tot[t] = inc[first + n - 1] - before;
+                slot_tot[u] = inc[first + n - 1] - before;
                 cg::cluster_group cluster = cg::this_cluster();
-                cluster.map_shared_rank(mail_tot, peer_of())[t] = slot_tot[t];
+                cluster.map_shared_rank(mail_tot, peer_of())[u] = slot_tot[u];
             }
             cluster_sync_cta();  // M1: the pair's counts exchanged
             WG_PHASE_MARK(28);
             const bool cycle = a.thr_any != 0;
-            if (t == 0) {
+            if (t == CTL) {
                 const unsigned rank = cluster_rank();
                 unsigned long long zero = 0, nnz_m = 0, zr_m = 0;
                 for (int sl = 0; sl < 5; ++sl) {
@@ -808,7 +815,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<N>::NT, 1
             }
             cluster_sync_cta();  // M2: population 0's block offset delivered
             WG_PHASE_MARK(29);
-            if (t == 0 && cluster_rank() == 1 && !skip_patch) {
+            if (t == CTL && cluster_rank() == 1 && !skip_patch) {
                 slot_off[0] = mail_off0;
                 slot_ok[0] = mail_ok0;
             }
@@ -901,13 +908,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<N>::NT, 1
                                       idwt_at<N, L, N - 2>(y));
                         }
                     }
-                    if (cy != 0 && j == 0) {  // column line: the column inverse of the partials
+                }
+                if (t > CTL && t < CTL + 5) {  // column lines: the column inverse of the partials (control lanes)
+                    const int sl = t - CTL, q = pair_pop((int)cluster_rank(), sl), cy = lbm_cy(q);
+                    const PatchPos pp = ppos;
+                    if (cy != 0) {
                         // rows without kept coefficients hold +0.0 partials: the
                         // zero-detail inverse variant of the top row applies
                         double* dst = cy == -1 ? a.eout.collo + edge_ix((uint32_t)pp.ar, pp.b, lbm_slot_collo(q), g, N)
                                                : a.eout.colhi + edge_ix((uint32_t)pp.ar, pp.b, lbm_slot_colhi(q), g, N);
-                        const double* src = side + (size_t)(jb.s - 1) * N;
-                        with_z2<L>(z_of_top(N, L, slot_top[jb.s]), [&](auto ZC) {
+                        const double* src = side + (size_t)(sl - 1) * N;
+                        with_z2<L>(z_of_top(N, L, slot_top[sl]), [&](auto ZC) {
                             constexpr int Z = decltype(ZC)::value;
                             double y[N];
 #pragma unroll
@@ -921,14 +932,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<N>::NT, 1
                 }
                 break;
             }
-            if (t == 0) cur_redo = 1;  // skip rule: the buffers hold the transform, re-derive the state
+            if (t == CTL) cur_redo = 1;  // skip rule: the buffers hold the transform, re-derive the state
             __syncthreads();
         }
         __syncthreads();  // cur_raw visible to every thread
         if (MODE != MODE_DECODE && cur_raw) {
             // skip rule / no compression: the collided state itself, stored raw
             const unsigned rank = cluster_rank();
-            if (t == 0) {
+            if (t == CTL) {
                 for (int sl = (rank == 0 ? 0 : 1); sl < 5; ++sl) {
                     const int qq = pair_pop((int)rank, sl);
                     const uint64_t off = chunk_alloc(a, cs, round16((uint64_t)NN * 8));
@@ -943,7 +954,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<N>::NT, 1
                 }
             }
             cluster_sync_all();
-            if (t == 0 && rank == 1) {
+            if (t == CTL && rank == 1) {
                 slot_off[0] = mail_off0;
                 slot_ok[0] = mail_ok0;
             }
@@ -984,7 +995,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<N>::NT, 1
                 red_f[t >> 5] = mf;
             }
             __syncthreads();
-            if (t == 0) {
+            if (t == CTL) {
                 double sm = 0.0, sf = 0.0;
                 for (int w = 0; w < NT / 32; ++w) {
                     sm += red_m[w];
@@ -996,16 +1007,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<N>::NT, 1
         }
         __syncthreads();  // buffers and descriptors free for the next patch
         WG_PHASE_MARK(31);
-        if (t == 0) {
+        if (t == CTL) {
             cur_p += npairs;
             ++cur_it;
             ppos = patch_pos(cur_p, g);
             cur_redo = 0;
             cur_raw = 0;
         }
-        if (t < 5) {
-            rmask[t] = Bits128{0ull, 0ull};
-            slot_top[t] = -1;
+        if (t >= CTL && t < CTL + 5) {
+            rmask[t - CTL] = Bits128{0ull, 0ull};
+            slot_top[t - CTL] = -1;
         }
         __syncthreads();
     }
