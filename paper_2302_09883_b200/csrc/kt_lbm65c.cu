@@ -1,4 +1,4 @@
-// kt_lbm65c.cu — D2Q9 step kernels for 65-point patches, level 5 (L = 6 = k is not conservative; not instantiated) (lbm_pair.cuh: one
+// kt_lbm65c.cu — D2Q9 step kernels for 65-point patches, levels 5-6 (L = 6 = k: valid, not conservative) (lbm_pair.cuh: one
 // patch per 2-CTA cluster; step, Codec::lz step, decode and device initial
 // state).  One translation unit per patch side / level range so the
 // instantiations build in parallel.
@@ -6,6 +6,6 @@
 
 namespace wg {
 
-bool select_lbm65c(int levels, KernelSet& k) { return pick_level<PairL, 65, 5, 5>(levels, k); }
+bool select_lbm65c(int levels, KernelSet& k) { return pick_level<PairL, 65, 6, 5>(levels, k); }
 
 }  // namespace wg

@@ -151,6 +151,19 @@ __host__ __device__ constexpr Bits128 inverse_cone(int ii) {
     return out;
 }
 
+// Threshold counts of one coefficient (apply_threshold, threshold.hpp:51-86:
+// kept iff y != 0 && !(|y| < T), NaN kept): kept += 1, nonzero += 1, as two
+// predicated adds (setp with predicate combination; |y| is an operand modifier).
+__device__ __forceinline__ void thr_count(double y, double T, unsigned& kept, unsigned& nonzero) {
+    asm("{\n\t.reg .pred p0, p1;\n\t.reg .f64 a;\n\t"
+        "setp.ne.f64 p0, %2, 0d0000000000000000;\n\t"
+        "abs.f64 a, %2;\n\t"
+        "setp.geu.and.f64 p1, a, %3, p0;\n\t"
+        "@p1 add.u32 %0, %0, 1;\n\t"
+        "@p0 add.u32 %1, %1, 1;\n\t}"
+        : "+r"(kept), "+r"(nonzero)
+        : "d"(y), "d"(T));
+}
 // Register (interleaved) indices holding samples after L levels.
 template <int N, int L>
 __host__ __device__ constexpr Bits128 sample_bits() {
@@ -704,53 +717,53 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<N>::NT, 1
                             lz[corner_pos<N, L>(rr)] = (y != 0.0 && fabs(y) < trow[band_of_r<N, L>(rr)]) ? 0.0 : y;
                         }
                     }
-                    // kept / nonzero flags as bit masks (one predicated OR each), counted by popc
-                    unsigned long long km[2] = {0ull, 0ull}, nm[2] = {0ull, 0ull};
+                    // counts: kept (y != 0 && !(|y| < T)) and nonzero, four
+                    // independent counter pairs (two predicated adds per value)
+                    // (ck[3]: the sample positions — every other position is a detail)
+                    unsigned ck[4] = {0u, 0u, 0u, 0u}, cn[4] = {0u, 0u, 0u, 0u};
 #pragma unroll
-                    for (int rr = 0; rr < N; ++rr) {
-                        const double y = x[rr];
-                        const bool nzx = y != 0.0;
-                        const bool keep = nzx && !(fabs(y) < trow[band_of_r<N, L>(rr)]);
-                        if (keep) km[rr >> 6] |= 1ull << (rr & 63);
-                        if (nzx) nm[rr >> 6] |= 1ull << (rr & 63);
-                    }
-                    const unsigned nz = (unsigned)(__popcll(km[0]) + __popcll(km[1]));
-                    const unsigned zr = (unsigned)(__popcll(nm[0]) + __popcll(nm[1])) - nz;
-                    {
-                        constexpr Bits128 SAMP = sample_bits<N, L>();
-                        samp_only = ((km[0] & ~SAMP.lo) | (km[1] & ~SAMP.hi)) == 0ull;
-                    }
-                    if (nz) {  // the thresholded row (killed -> +0.0, -0.0 -> +0.0 like the CSR round trip)
+                    for (int rr = 0; rr < N; ++rr)
+                        thr_count(x[rr], trow[band_of_r<N, L>(rr)], ck[band_of_r<N, L>(rr) == 0 ? 3 : (rr & 1) + 1],
+                                  cn[rr & 3]);
+                    const unsigned nz = (ck[1] + ck[2]) + ck[3];
+                    const unsigned zr = (cn[0] + cn[1]) + (cn[2] + cn[3]) - nz;
+                    samp_only = (ck[1] + ck[2]) == 0u;  // no kept detail coefficient
+                    // park the thresholded row for W (killed -> +0.0, -0.0 -> +0.0
+                    // like the CSR round trip); a row without kept coefficients is
+                    // needed only as zeros of a cone row of the row edge line
+                    const bool cone_row = jb.s > 0 && jb.cx != 0 && (jb.cx == -1 ? CONE_LO : CONE_HI).has(r);
+                    if (nz) {
 #pragma unroll
-                        for (int rr = 0; rr < N; ++rr) x[rr] = ((km[rr >> 6] >> (rr & 63)) & 1ull) ? x[rr] : 0.0;
-                    }
-                    if (nz) atomicMax(&slot_top[jb.s], r);
-                    // mass of the reconstruction: sum_rc a_r a_c C[r][c] (trapezoid
-                    // functional of idwt_nd, host-computed exact dyadic values; for
-                    // conservative levels only the samples carry mass)
-                    const double ar = a.mass_a[r];
-                    if (ar != 0.0 && nz) {
-                        double acc = 0.0;
+                        for (int rr = 0; rr < N; ++rr) {
+                            const double y = x[rr];
+                            rowp[rr] = (y != 0.0 && !(fabs(y) < trow[band_of_r<N, L>(rr)])) ? y : 0.0;
+                        }
+                        atomicMax(&slot_top[jb.s], r);
+                        // mass of the reconstruction: sum_rc a_r a_c C[r][c] (trapezoid
+                        // functional of idwt_nd, host-computed exact dyadic values; for
+                        // conservative levels only the samples carry mass)
+                        const double ar = a.mass_a[r];
+                        if (ar != 0.0) {
+                            double acc = 0.0;
 #pragma unroll
-                        for (int rr = 0; rr < N; ++rr) acc += x[rr] * a.mass_a[corner_pos<N, L>(rr)];
-                        acc_m[t] = ar * acc;
+                            for (int rr = 0; rr < N; ++rr) acc += rowp[rr] * a.mass_a[corner_pos<N, L>(rr)];
+                            acc_m[t] = ar * acc;
+                        }
+                    } else if (cone_row) {
+#pragma unroll
+                        for (int rr = 0; rr < N; ++rr) rowp[rr] = 0.0;
                     }
                     // column edge line of the reconstruction (own populations):
                     // Y[r][jj] = row inverse at jj = 1 (cy = -1) or N-2 (cy = +1)
                     if (jb.s > 0 && jb.cy != 0) {
                         double val = 0.0;
-                        if (nz) val = jb.cy == -1 ? idwt_at<N, L, 1>(x) : idwt_at<N, L, N - 2>(x);
+                        if (nz) {
+                            double y[N];
+#pragma unroll
+                            for (int rr = 0; rr < N; ++rr) y[rr] = rowp[rr];  // only the cone is loaded
+                            val = jb.cy == -1 ? idwt_at<N, L, 1>(y) : idwt_at<N, L, N - 2>(y);
+                        }
                         side[(size_t)(jb.s - 1) * N + r] = val;
-                    }
-                    // park the row for W (a row without kept coefficients is
-                    // needed only as zeros of a cone row of the row edge line)
-                    const bool cone_row = jb.s > 0 && jb.cx != 0 && (jb.cx == -1 ? CONE_LO : CONE_HI).has(r);
-                    if (nz) {
-#pragma unroll
-                        for (int rr = 0; rr < N; ++rr) rowp[rr] = x[rr];  // interleaved order
-                    } else if (cone_row) {
-#pragma unroll
-                        for (int rr = 0; rr < N; ++rr) rowp[rr] = 0.0;
                     }
                     cnt = ((unsigned long long)zr << 32) | nz;
                 }
