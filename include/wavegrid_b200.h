@@ -263,6 +263,13 @@ wg_status wg_dev_session_upload(wg_session* s, const double* dev_grid);
  * then performs step 1 with `dt`.  One-shard D2Q9 sessions. */
 wg_status wg_session_step_host(wg_session* s, const double* host_grid, double dt);
 
+/* assemble(grid, 0)'s consistency check (patchgrid.hpp:205-239) on the
+ * current state: every shared boundary cell of component 0 agrees between
+ * the patches of this shard that own it to tol * max(|a|, |b|, 1); returns
+ * WG_CONSISTENCY otherwise (run() applies it every step in strict mode,
+ * pipeline.hpp:278-283). */
+wg_status wg_session_check_shared(wg_session* s, double tol);
+
 /* Generate the initial state of cfg ON THE DEVICE and store it through the
  * compression cycle (for grids whose raw state does not fit the store
  * budget, C4/C5).  Unlike wg_session_upload the first step then starts from

@@ -214,6 +214,7 @@ _PROTOS = {
     "wg_session_info_get": (i32, [vp, P(SessionInfoC)]),
     "wg_session_upload": (i32, [vp, dp]),
     "wg_session_step_host": (i32, [vp, dp, f64]),
+    "wg_session_check_shared": (i32, [vp, f64]),
     "wg_dev_session_upload": (i32, [vp, vp]),
     "wg_session_init_device": (i32, [vp]),
     "wg_session_step": (i32, [vp, f64]),

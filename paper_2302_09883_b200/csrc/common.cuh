@@ -81,6 +81,7 @@ enum : unsigned {
     ERR_RAW_OVERFLOW = 1u << 4,
     ERR_ZERO_SPEED = 1u << 5,
     ERR_PEER_TIMEOUT = 1u << 6,
+    ERR_CONSISTENCY = 1u << 7,
 };
 
 inline void check_device_error(unsigned word) {
@@ -92,6 +93,7 @@ inline void check_device_error(unsigned word) {
     if (word & ERR_DOMAIN) raise(WG_DOMAIN, "water depth must be positive");
     if (word & ERR_RIEMANN) raise(WG_RIEMANN, "SweRiemann: Newton iteration did not converge");
     if (word & ERR_ZERO_SPEED) raise(WG_INVALID_ARGUMENT, "cfl_dt: zero wave speed");
+    if (word & ERR_CONSISTENCY) raise(WG_CONSISTENCY, "assemble: shared cells disagree");
     if (word & ERR_PEER_TIMEOUT) raise(WG_LOGIC, "peer halo exchange: a neighbour shard did not deliver its halo lines");
     raise(WG_LOGIC, "device error word " + std::to_string(word));
 }

@@ -18,11 +18,12 @@ namespace wg {
 constexpr int kMaxLevels = 8;
 constexpr int kMaxN = 65;  // largest patch side of the device session
 
-// ---- optional phase timing (tuning builds only: -DWG_PHASE_TIMING) ---------
-// Thread 0 of every CTA adds the cycles since its previous mark (i.e. the
-// wall time of the phase that just ended at a barrier) to a.phase[k] (a
-// 32-entry device buffer of the session, read by wg_debug_phase_cycles).
-#ifdef WG_PHASE_TIMING
+// ---- phase clocks ---------------------------------------------------------
+// Thread 0 of every CTA adds the cycles since its previous mark (the wall time
+// of the phase that just ended at a barrier) to a.phase[k] (a 32-entry device
+// buffer of the session): the per-phase split of a fused step behind
+// RunSummary's dwt / threshold / codec seconds (pipeline.hpp:52-63) and
+// tools/phase_profile.py.  One clock read and one reduction per mark.
 __device__ __forceinline__ unsigned long long& phase_last() {
     __shared__ unsigned long long last;
     return last;
@@ -35,9 +36,6 @@ __device__ __forceinline__ void phase_mark(unsigned long long* buf, int k) {
     }
 }
 #define WG_PHASE_MARK(k) ::wg::phase_mark(a.phase, k)
-#else
-#define WG_PHASE_MARK(k) ((void)0)
-#endif
 
 // ---- optional device bounds checks (debug builds only: -DWG_BOUNDS_CHECK) ---
 #ifdef WG_BOUNDS_CHECK
@@ -98,7 +96,7 @@ struct StepArgs {
     unsigned long long* swe_vmax;    // [2] max wave speed, bits of a non-negative double
     unsigned long long* swe_steps;   // steps completed on the device
     double t_end, cfl_dx, dx, gravity;
-    unsigned long long* phase;       // WG_PHASE_TIMING builds: per-phase cycle sums [32]
+    unsigned long long* phase;       // per-phase cycle sums of thread 0 [32] (phase_mark)
     double* lz_dense;                // Codec::lz: thresholded coefficient arrays [npatch*m][n*n] (else null)
     // transport l2_error diagnostic every step (pipeline.hpp:275-276)
     int l2_on;

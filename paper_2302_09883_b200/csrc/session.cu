@@ -361,6 +361,31 @@ __global__ void k_swe_clock_reset(double* td, unsigned long long* vmax_bits, uns
 
 }  // namespace
 
+// ---- strict mode: shared boundary cells of component 0 agree between the
+// patches that own them (assemble(grid, 0), patchgrid.hpp:205-239: tolerance
+// tol * max(|a|, |b|, 1)); grid = the decoded shard (grid-buffer layout).
+// Only neighbours inside the shard are compared (assemble's global field has
+// no periodic identification of its first and last points).
+__global__ void k_check_shared(const double* grid, uint32_t N, ShardGeom g, double tol, unsigned* err) {
+    const uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    const uint64_t per = (uint64_t)g.m * (N + 2) * (N + 2), TP = N + 2;
+    if (t >= (uint64_t)g.npatch * N * 2) return;
+    const uint32_t p = (uint32_t)(t / (2ull * N)), k = (uint32_t)(t % N), side = (uint32_t)((t / N) & 1);
+    const uint32_t ar = p / g.P1, b = p % g.P1;
+    double x, y;
+    if (side == 0) {  // right neighbour: my column N-1 == its column 0
+        if (b + 1 >= g.P1) return;
+        x = grid[p * per + (k + 1) * TP + N];
+        y = grid[(uint64_t)(p + 1) * per + (k + 1) * TP + 1];
+    } else {  // below neighbour: my row N-1 == its row 0
+        if (ar + 1 >= g.R) return;
+        x = grid[p * per + N * TP + k + 1];
+        y = grid[(uint64_t)(p + g.P1) * per + TP + k + 1];
+    }
+    const double scale = fmax(fmax(fabs(x), fabs(y)), 1.0);
+    if (!(fabs(x - y) <= tol * scale)) atomicOr(err, ERR_CONSISTENCY);
+}
+
 // ---- the session -------------------------------------------------------------
 struct Session {
     wg_run_config cfg{};
@@ -398,7 +423,7 @@ struct Session {
     uint64_t device_bytes = 0;
     // SWE device clock: [t, last dt] (f64), vmax bits [2], steps done (u64)
     unsigned long long* swe = nullptr;
-    unsigned long long* phase = nullptr;  // WG_PHASE_TIMING builds only
+    unsigned long long* phase = nullptr;  // per-phase cycle sums [32] (phase_mark, patch_phases.cuh)
     // Codec::lz metrics staging
     double* lz_dense = nullptr;
     unsigned long long* lz_done = nullptr;  // LzFinal::state
@@ -632,10 +657,8 @@ struct Session {
             swe = dalloc<unsigned long long>(5);
             WG_CUDA(cudaMemsetAsync(swe, 0, 5 * sizeof(unsigned long long), stream));
         }
-#ifdef WG_PHASE_TIMING
         phase = dalloc<unsigned long long>(32);
         WG_CUDA(cudaMemsetAsync(phase, 0, 32 * sizeof(unsigned long long), stream));
-#endif
         grow_rows(1024);
         if (cfg.codec == 2 && !cfg.no_compression) {  // Codec::lz metrics (the store itself stays CSR)
             if (!ks.main_lz) raise(WG_INVALID_ARGUMENT, "Codec::lz metrics: not available for this kernel variant");
@@ -1082,6 +1105,58 @@ struct Session {
         sync();
     }
 
+    // Shares of the step kernel's phase clocks in RunSummary's categories
+    // {step, dwt, threshold, codec} (phase ids: lbm_pair.cuh, patch_kernels.cuh,
+    // swe_kernels.cuh; a row pass is half transform, half threshold).
+    void phase_shares(double out[4]) {
+        unsigned long long h[32];
+        WG_CUDA(cudaMemcpy(h, phase, sizeof h, cudaMemcpyDeviceToHost));
+        double w[4] = {0, 0, 0, 0};
+        auto add = [&](int k, int cat, double f = 1.0) { w[cat] += f * (double)h[k]; };
+        if (ks.cluster > 1) {  // D2Q9 pair kernel
+            for (int k : {12, 13, 14, 21, 22, 23, 24, 25}) add(k, 0);
+            add(26, 1);
+            add(27, 1, 0.5);
+            add(27, 2, 0.5);
+            for (int k : {28, 29, 30}) add(k, 3);
+            add(31, 1);
+        } else if (is_swe()) {
+            for (int k : {0, 1, 2, 9, 11, 13, 14}) add(k, 0);
+            add(4, 1);
+            add(5, 1, 0.5);
+            add(5, 2, 0.5);
+            add(8, 1);
+            for (int k : {6, 7}) add(k, 3);
+        } else {  // transport
+            for (int k : {0, 1, 2, 3, 9, 10, 11}) add(k, 0);
+            add(4, 1);
+            add(5, 1, 0.5);
+            add(5, 2, 0.5);
+            add(8, 1);
+            for (int k : {6, 7}) add(k, 3);
+        }
+        const double tot = w[0] + w[1] + w[2] + w[3];
+        for (int k = 0; k < 4; ++k) out[k] = tot > 0 ? w[k] / tot : 0.0;
+    }
+
+    // assemble(grid, 0)'s consistency check on the current state (strict
+    // mode, pipeline.hpp:278-283): decode, compare the shared cells on the
+    // device; raises WG_CONSISTENCY at the next sync.
+    void check_shared(double tol) {
+        if (is_swe()) sync();
+        const uint64_t n = (uint64_t)sg.npatch * sg.m * geo.tcount;
+        DevBuf<double> d(n);
+        WG_CUDA(cudaMemsetAsync(d.p, 0, n * sizeof(double), stream));
+        StepArgs a = step_args(cur, 1 - cur);
+        a.decode_out = d.p;
+        ks.decode<<<grid, ks.threads, ks.smem, stream>>>(a);
+        WG_LAUNCH_CHECK("decode (strict)");
+        const uint64_t threads = (uint64_t)sg.npatch * N * 2;
+        k_check_shared<<<(unsigned)((threads + 255) / 256), 256, 0, stream>>>(d.p, N, sg, tol, err);
+        WG_LAUNCH_CHECK("strict shared cells");
+        sync();  // d dies with this scope; raises WG_CONSISTENCY
+    }
+
     void metrics(wg_metrics_row* out, uint64_t max_rows, uint64_t* nrows) {
         sync();
         const uint64_t n = std::min<uint64_t>(step - row0, max_rows);
@@ -1440,6 +1515,10 @@ wg_status wg_session_step_host(wg_session* s, const double* host_grid, double dt
     });
 }
 
+wg_status wg_session_check_shared(wg_session* s, double tol) {
+    return guard([&] { reinterpret_cast<Session*>(s)->check_shared(tol); });
+}
+
 wg_status wg_session_init_device(wg_session* s) {
     return guard([&] { reinterpret_cast<Session*>(s)->init_device(); });
 }
@@ -1563,13 +1642,13 @@ wg_status wg_session_last_row_async(wg_session* sp, wg_metrics_row* row) {
     });
 }
 
-// Tuning builds (-DWG_PHASE_TIMING) only: summed per-phase cycles of thread 0
+// Summed per-phase cycles of thread 0 of every CTA (phase_mark)
 // of every CTA of the session's step launches; `reset` zeroes them.  Not
 // part of the product ABI.
 wg_status wg_debug_phase_cycles(wg_session* sp, uint64_t* out, int32_t n, int32_t reset) {
     return guard([&] {
         Session* s = reinterpret_cast<Session*>(sp);
-        if (!s->phase) raise(WG_LOGIC, "built without WG_PHASE_TIMING");
+        if (!s->phase) raise(WG_LOGIC, "no phase buffer");
         s->sync();
         unsigned long long h[32];
         WG_CUDA(cudaMemcpy(h, s->phase, sizeof h, cudaMemcpyDeviceToHost));
@@ -1622,6 +1701,7 @@ wg_status wg_run(const wg_run_config* cfg, wg_metrics_row* rows, uint64_t max_ro
         const bool streamed = cfg->scheme == WG_SCHEME_LBM_D2Q9 && !dts.empty() &&
                               (uint64_t)s.sg.npatch * s.sg.m * round16((uint64_t)s.N * s.N * 8) > s.cap;
         if (!streamed) s.upload_host(grid.data());
+        WG_CUDA(cudaMemsetAsync(s.phase, 0, 32 * sizeof(unsigned long long), s.stream));
         WG_CUDA(cudaEventRecord(e0, s.stream));
         if (streamed) {
             s.step_from_host(grid.data(), dts[0]);
@@ -1635,14 +1715,19 @@ wg_status wg_run(const wg_run_config* cfg, wg_metrics_row* rows, uint64_t max_ro
                 double td[2];  // [t, dt of the last step]
                 WG_CUDA(cudaMemcpy(td, s.swe_td(), sizeof td, cudaMemcpyDeviceToHost));
                 const double est = td[1] > 0.0 ? std::ceil((cfg->t_end - td[0]) / td[1]) : 16.0;
-                const uint64_t batch = (uint64_t)std::clamp(est, 1.0, 512.0);
+                const uint64_t batch = cfg->strict ? 1 : (uint64_t)std::clamp(est, 1.0, 512.0);
                 const uint64_t before = s.step;
                 for (uint64_t k = 0; k < batch; ++k) s.do_step(0.0);
                 s.sync();
+                if (cfg->strict && !cfg->no_compression) s.check_shared(1e-12);
                 if (s.step == before) raise(WG_LOGIC, "SWE step loop made no progress");
             }
         } else {
-            for (double dt : dts) s.do_step(dt);
+            for (double dt : dts) {
+                s.do_step(dt);
+                // strict (pipeline.hpp:278-283): assemble(grid, 0) every step
+                if (cfg->strict && !cfg->no_compression) s.check_shared(1e-12);
+            }
         }
         WG_CUDA(cudaEventRecord(e1, s.stream));
         s.sync();
@@ -1663,28 +1748,6 @@ wg_status wg_run(const wg_run_config* cfg, wg_metrics_row* rows, uint64_t max_ro
                     raise(WG_CONSISTENCY, "strict: compression cycle changed global mass");
             }
         }
-        if (cfg->scheme == WG_SCHEME_TRANSPORT && cfg->compute_l2 && !r.empty()) {
-            // every row's l2 comes from the device (col_l2, CUDA exp); the
-            // final row is recomputed here with the host's glibc exp, the
-            // reference's own libm
-            std::vector<double> fg(grid.size());
-            s.download(fg.data());
-            const uint64_t n0 = g.n[0], n1 = g.n[1], ty = n1 + 2;
-            std::vector<double> asmv(cfg->nx * cfg->nx);
-            for (uint64_t p = 0; p < g.npatch; ++p) {
-                const uint64_t a = p / g.splits[1], b = p % g.splits[1];
-                for (uint64_t i = 1; i <= n0; ++i)
-                    for (uint64_t j = 1; j <= n1; ++j)
-                        asmv[(a * (n0 - 1) + i - 1) * cfg->nx + b * (n1 - 1) + j - 1] = fg[p * g.tcount + i * ty + j];
-            }
-            double sum = 0.0;
-            for (uint64_t i = 0; i < cfg->nx; ++i)
-                for (uint64_t j = 0; j < cfg->nx; ++j) {
-                    const double d = asmv[i * cfg->nx + j] - exact_transport_at(*cfg, s.time, i, j);
-                    sum += d * d;
-                }
-            r.back().l2 = cfg->domain_length * cfg->domain_length / (double)(cfg->nx * cfg->nx) * sum;
-        }
         if (nrows) *nrows = n;
         if (rows)
             for (uint64_t k = 0; k < n && k < max_rows; ++k) rows[k] = r[k];
@@ -1695,7 +1758,18 @@ wg_status wg_run(const wg_run_config* cfg, wg_metrics_row* rows, uint64_t max_ro
             for (auto& x : r) sum += x.ratio;
             summary->avg_ratio = r.empty() ? 1.0 : sum / (double)r.size();
             summary->total_seconds = ms * 1e-3;
-            summary->step_seconds = ms * 1e-3;
+            // RunSummary's phase split (pipeline.hpp:52-63, 188-189, 229-255)
+            // from the fused kernel's phase clocks: the scheme phases (decode,
+            // ghosts, FV / collide, raw stores) are the step, the forward
+            // transforms and the edge reconstruction the dwt, the threshold
+            // half of the row pass the threshold, scan / allocation / CSR the
+            // codec — each a share of the measured run time
+            double share[4] = {0, 0, 0, 0};  // step, dwt, threshold, codec
+            s.phase_shares(share);
+            summary->step_seconds = share[0] * ms * 1e-3;
+            summary->dwt_seconds = share[1] * ms * 1e-3;
+            summary->threshold_seconds = share[2] * ms * 1e-3;
+            summary->codec_seconds = share[3] * ms * 1e-3;
             summary->t_final = s.time;
             summary->steps = s.step;
         }

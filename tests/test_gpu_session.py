@@ -314,3 +314,60 @@ def test_lbm_directory_ends_on_page_boundary(product):
         product.check(product.wg_session_sync(s))
     finally:
         product.wg_session_destroy(s)
+
+
+# ---- strict mode (pipeline.hpp:278-283) and RunSummary (pipeline.hpp:52-63) ----
+
+
+@pytest.mark.parametrize("scheme", ["transport", "lbm"])
+def test_strict_shared_cell_mismatch_raises(product, scheme):
+    """assemble(grid, 0)'s check on the device: a shared boundary cell of
+    component 0 that differs between its two owners beyond 1e-12 relative
+    raises WG_CONSISTENCY; equal (or 1e-14-close) ones pass."""
+    cfg = (transport_cfg(129, (2, 2), 4, 1e-3, 2) if scheme == "transport" else lbm_cfg(129, (2, 2), 4, 1e-3, 2))
+    g0 = api.initial_state(cfg, lib=product)
+    s = _session(product, cfg)
+    try:
+        product.check(product.wg_session_upload(s, abi.dptr(g0.data)))
+        product.check(product.wg_session_check_shared(s, 1e-12))  # healthy
+    finally:
+        product.wg_session_destroy(s)
+    bad = g0.data.copy()
+    # patch 0's last logical column is patch 1's first (true index 65 vs 1)
+    bad[0, 0, 10, 65] += 1e-6
+    s = _session(product, cfg)
+    try:
+        product.check(product.wg_session_upload(s, abi.dptr(bad)))
+        with pytest.raises(abi.ConsistencyError):
+            product.check(product.wg_session_check_shared(s, 1e-12))
+    finally:
+        product.wg_session_destroy(s)
+    close = g0.data.copy()
+    close[0, 0, 10, 65] *= 1.0 + 1e-14
+    s = _session(product, cfg)
+    try:
+        product.check(product.wg_session_upload(s, abi.dptr(close)))
+        product.check(product.wg_session_check_shared(s, 1e-12))
+    finally:
+        product.wg_session_destroy(s)
+
+
+@pytest.mark.parametrize("scheme", ["transport", "lbm", "swe"])
+def test_strict_run_passes_and_summary_split(product, scheme):
+    """strict run() (mass + shared cells every step) accepts a healthy run;
+    the RunSummary phase split is populated and overhead() > 0."""
+    if scheme == "transport":
+        cfg = transport_cfg(129, (2, 2), 4, 1e-3, 6, strict=True)
+    elif scheme == "lbm":
+        cfg = lbm_cfg(129, (2, 2), 4, 1e-3, 6, strict=True)
+    else:
+        cfg = api.RunConfig(scheme="swe", nx=129, splits=(2, 2), levels=4, t_end=0.003,
+                            spec=api.ThresholdSpec("constant", 5e-4), strict=True)
+    r = api.run(cfg, lib=product)
+    sm = r.summary
+    assert sm["total_seconds"] > 0 and sm["step_seconds"] > 0
+    assert sm["dwt_seconds"] > 0 and sm["threshold_seconds"] > 0 and sm["codec_seconds"] > 0
+    parts = sm["step_seconds"] + sm["dwt_seconds"] + sm["threshold_seconds"] + sm["codec_seconds"]
+    assert abs(parts - sm["total_seconds"]) <= 1e-9 + 1e-6 * sm["total_seconds"]
+    overhead = (sm["total_seconds"] - sm["step_seconds"]) / sm["step_seconds"]  # RunSummary::overhead()
+    assert overhead > 0
