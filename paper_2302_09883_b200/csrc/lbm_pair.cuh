@@ -225,7 +225,7 @@ struct PairLayout {
     static constexpr size_t smem_bytes() { return fixed_bytes() + stage_bytes(); }
 };
 
-enum : uint32_t { IN_CSR = 0, IN_RAW = 1, IN_DEAD = 2 };
+enum : uint32_t { IN_CSR = 0, IN_RAW = 1, IN_DEAD = 2, IN_CONST = 3 };
 
 // Where a slot's input block of the current patch lives.
 struct SlotIn {
@@ -356,6 +356,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<N>::NT, 1
                 d.raw_ld = (uint32_t)TP;
             } else if (e[sl].flags & DIR_DEAD) {
                 d.kind = IN_DEAD;
+            } else if (e[sl].flags & DIR_CONST) {  // constant raw block (value in the entry)
+                d.kind = IN_CONST;
+                d.nnz = (uint32_t)(e[sl].off & 0xffffffffull);
+                d.raw_ld = (uint32_t)(e[sl].off >> 32);
             } else if (e[sl].flags & DIR_RAW) {
                 d.kind = IN_RAW;
                 d.raw = reinterpret_cast<const double*>(a.store_in + e[sl].off);
@@ -583,9 +587,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<N>::NT, 1
 #pragma unroll
                         for (int i = 0; i < N; ++i) v[i] = d.raw[(size_t)i * d.raw_ld + jc];
                         emit(v);
-                    } else if (d.kind == IN_DEAD) {
+                    } else if (d.kind == IN_DEAD || d.kind == IN_CONST) {
+                        const double c = d.kind == IN_DEAD ? 0.0
+                                                           : __longlong_as_double((long long)(((unsigned long long)d.raw_ld << 32) | d.nnz));
 #pragma unroll
-                        for (int i = 0; i < N; ++i) v[i] = 0.0;
+                        for (int i = 0; i < N; ++i) v[i] = c;
                         emit(v);
                     } else {
                         const Bits128 m = rmask[jb.s];

@@ -177,6 +177,12 @@ __device__ __forceinline__ bool decode_row(double* T, int li, const DirEntry e,
         for (int j = 0; j < N; ++j) rowp[j] = 0.0;
         return true;
     }
+    if (e.flags & DIR_CONST) {  // constant raw block: the value itself is in the entry
+        const double c = __longlong_as_double((long long)e.off);
+#pragma unroll
+        for (int j = 0; j < N; ++j) rowp[j] = c;
+        return true;
+    }
     if (raw) {
         // a raw block fills the whole tile interior; thread li copies COLUMN
         // li so that consecutive threads read consecutive addresses
@@ -598,7 +604,7 @@ template <int N>
 __device__ __forceinline__ void prefetch_block(const StepArgs& a, const DirEntry e, int tid, int nthreads) {
     const unsigned long long bytes = (e.flags & DIR_RAW) ? (unsigned long long)N * N * 8
                                                           : 12ull * e.nnz + 4ull * (N + 1);
-    if (!(e.flags & DIR_DEAD)) prefetch_range(a.store_in + e.off, bytes, tid, nthreads);
+    if (!(e.flags & (DIR_DEAD | DIR_CONST))) prefetch_range(a.store_in + e.off, bytes, tid, nthreads);
 }
 
 // L2 prefetch of the neighbours' edge lines (all stored components) that

@@ -1239,9 +1239,16 @@ struct Session {
             put32(sg.m);
             put32(raw ? 0u : (uint32_t)levels);
             for (uint32_t q = 0; q < sg.m; ++q) {
-                if (e[q].off + (raw ? rawb : 12ull * e[q].nnz + 4ull * (N + 1)) > used)
+                const bool cst = (e[q].flags & DIR_CONST) != 0;
+                if (!cst && e[q].off + (raw ? rawb : 12ull * e[q].nnz + 4ull * (N + 1)) > used)
                     raise(WG_CORRUPT_STREAM, "checkpoint: directory entry outside the pool");
-                const unsigned char* b = pool.data() + e[q].off;
+                std::vector<double> cbuf;  // a constant block, materialised (the file holds raw records)
+                if (cst) {
+                    double c;
+                    std::memcpy(&c, &e[q].off, 8);
+                    cbuf.assign(nn, c);
+                }
+                const unsigned char* b = cst ? reinterpret_cast<const unsigned char*>(cbuf.data()) : pool.data() + e[q].off;
                 if (raw) {
                     if (!(e[q].flags & DIR_RAW)) raise(WG_LOGIC, "checkpoint: mixed raw/CSR patch");
                     const uint64_t chunk = 64 * 1024, nch = (rawb + chunk - 1) / chunk;
@@ -1458,6 +1465,12 @@ struct Session {
         if (raw) *raw = is_raw ? 1 : 0;
         if (nnz) *nnz = is_raw ? (uint64_t)N * N : e.nnz;
         const unsigned char* base = store[cur] + e.off;
+        if (e.flags & DIR_CONST) {  // constant block: the value is in the entry
+            double c;
+            std::memcpy(&c, &e.off, 8);
+            if (v) std::fill(v, v + (size_t)N * N, c);
+            return;
+        }
         if (is_raw) {
             if (v) WG_CUDA(cudaMemcpy(v, base, (size_t)N * N * 8, cudaMemcpyDeviceToHost));
             return;

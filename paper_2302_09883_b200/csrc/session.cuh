@@ -22,12 +22,14 @@
 namespace wg {
 
 constexpr uint32_t DIR_RAW = 1u;
-constexpr uint32_t DIR_DEAD = 2u;  // block lost to a store overflow: decodes as zeros, error raised
+constexpr uint32_t DIR_DEAD = 2u;   // block lost to a store overflow: decodes as zeros, error raised
+constexpr uint32_t DIR_CONST = 4u;  // a raw block whose n*n values are bitwise equal: off holds the
+                                    // value's bits, nothing in the pool (SWE's flat regions)
 
 struct DirEntry {
     uint64_t off;    // byte offset in the pool
     uint32_t nnz;    // CSR entries (0 for raw)
-    uint32_t flags;  // DIR_RAW
+    uint32_t flags;  // DIR_RAW / DIR_DEAD / DIR_CONST (with DIR_RAW)
 };
 
 struct EdgeSet {

@@ -41,18 +41,11 @@ struct SweLayout {
     static constexpr size_t scratch_doubles() { return (size_t)3 * N * N; }
 };
 
-// skip-rule patches (nothing zeroed, pipeline.hpp:243-249) keep a component
-// as CSR when its reconstruction equals the FV output bit for bit (and the
-// CSR block is at most 1/8 of the raw one, so a failed attempt stays inside
-// the pool's 1/8 slack): the flat regions of the dam
-// break then stay compressed instead of raw.  The stored state, metrics and
-// edges are identical either way (the next decode yields the same bits).
-// Measured at C3 (tools/ab_swe_exact.sh): DRAM 0.83 vs 1.90 GB per step, but
-// 5.21 vs 5.39 GLUPS (the flat CSR components now need inverse transforms in
-// a compute-bound kernel), so off by default; all GPU tests pass either way.
-#ifndef WG_SWE_EXACT_CSR
-#define WG_SWE_EXACT_CSR 0
-#endif
+// Skip-rule patches (nothing zeroed, pipeline.hpp:243-249) store the FV
+// output raw; a component whose n*n values are bitwise equal (the flat
+// regions of the dam break: h = 1 or 2, hu = hv = 0) is stored as a
+// constant directory entry (DIR_CONST: the value in the entry, nothing in the
+// pool) — the next decode is a fill with the same bits.
 
 #ifndef WG_SWE_MIN_BLOCKS
 #define WG_SWE_MIN_BLOCKS 2  // 2 CTAs per SM (spills in the lifting phases, +44% C3)
@@ -68,7 +61,7 @@ __global__ void __launch_bounds__(SweLayout<N>::NT, WG_SWE_MIN_BLOCKS) k_swe_ste
     __shared__ uint64_t slot_off[3];
     __shared__ int slot_ok[3];
     __shared__ uint32_t comp_nnz[3];
-    __shared__ int slot_exact[3];
+    __shared__ int slot_const[3];
     __shared__ unsigned long long patch_bytes, patch_nnz, patch_zero;
     __shared__ ChunkState cs;
     __shared__ double wmax[NT / 32];
@@ -103,7 +96,7 @@ __global__ void __launch_bounds__(SweLayout<N>::NT, WG_SWE_MIN_BLOCKS) k_swe_ste
     if (!clk.live) return;        // t >= t_end: the launch is a no-op
     const double r = clk.dt / a.dx;  // solver.hpp:212
 
-    StepPartial part{0, 0, 0, 0.0, 0.0};
+    StepPartial part{0, 0, 0, 0.0, 0.0, 0.0};
     double macc = 0.0, mfacc = 0.0, vmax = 0.0;
     if (t == 0) cs.cur = cs.end = 0;
     WG_PHASE_MARK(-1);
@@ -193,10 +186,7 @@ __global__ void __launch_bounds__(SweLayout<N>::NT, WG_SWE_MIN_BLOCKS) k_swe_ste
                 }
                 // skip rule decided before anything is written (pipeline.hpp:243)
                 for (int sl = 0; sl < 3; ++sl) {
-                    slot_exact[sl] = 1;
-                    const bool exact_try = WG_SWE_EXACT_CSR && patch_zero == 0 &&
-                                           12ull * comp_nnz[sl] + 4ull * (N + 1) <= (uint64_t)NN;
-                    if (!cycle || (patch_zero == 0 && !exact_try)) {
+                    if (!cycle || patch_zero == 0) {
                         slot_ok[sl] = 0;
                         continue;
                     }
@@ -224,16 +214,8 @@ __global__ void __launch_bounds__(SweLayout<N>::NT, WG_SWE_MIN_BLOCKS) k_swe_ste
             WG_PHASE_MARK(7);
             if (ok) {
                 decode_col<N, L>(T, li, false, v);
-                if (!store_raw) {
-                    write_edges<N>(a.eout, pp, s, g, li, v);
-                    if (s == 0) m += col_mass<N>(li, v);
-                } else {  // skip rule: is the CSR form exact for this column?
-                    bool same = true;
-#pragma unroll
-                    for (int i = 0; i < N; ++i)
-                        same &= __double_as_longlong(v[i]) == __double_as_longlong(S[(size_t)s * NN + i * N + li]);
-                    if (!same) slot_exact[s] = 0;
-                }
+                write_edges<N>(a.eout, pp, s, g, li, v);
+                if (s == 0) m += col_mass<N>(li, v);
             }
             __syncthreads();
             WG_PHASE_MARK(8);
@@ -254,10 +236,24 @@ __global__ void __launch_bounds__(SweLayout<N>::NT, WG_SWE_MIN_BLOCKS) k_swe_ste
             }
         }
         if (store_raw) {  // raw store of the FV output (skip rule / no_compression)
+            // constant components (bitwise) become DIR_CONST entries
+            if (t < 3) slot_const[t] = 1;
+            __syncthreads();
+            if (lane_ok) {
+                const unsigned long long c0 = (unsigned long long)__double_as_longlong(S[(size_t)s * NN]);
+                bool same = true;
+#pragma unroll 5
+                for (int i = 0; i < N; ++i)
+                    same &= (unsigned long long)__double_as_longlong(S[(size_t)s * NN + i * N + li]) == c0;
+                if (!same) slot_const[s] = 0;
+            }
+            __syncthreads();
             if (t == 0) {
                 for (int sl = 0; sl < 3; ++sl) {
-                    if (a.compress && slot_ok[sl] && slot_exact[sl]) {  // exact CSR kept (its directory entry stands)
+                    if (slot_const[sl]) {
                         slot_ok[sl] = 2;
+                        a.dir_out[(size_t)p * 3 + sl] =
+                            DirEntry{(uint64_t)__double_as_longlong(S[(size_t)sl * NN]), 0u, DIR_RAW | DIR_CONST};
                         continue;
                     }
                     const uint64_t off = chunk_alloc(a, cs, round16((uint64_t)NN * 8));
