@@ -49,7 +49,8 @@ typedef enum wg_status {
     WG_CUDA = 6,             /* CUDA runtime / launch failure (no fallback) */
     WG_OUT_OF_MEMORY = 7,    /* device memory or compressed-store budget    */
     WG_OUT_OF_RANGE = 8,     /* std::out_of_range, wavelet.hpp:164          */
-    WG_LOGIC = 9             /* std::logic_error                            */
+    WG_LOGIC = 9,            /* std::logic_error                            */
+    WG_ABORTED = 10          /* a wg_run_hooked hook stopped the run        */
 } wg_status;
 
 /* Copies the message of the last failure on this thread (NUL-terminated). */
@@ -172,6 +173,10 @@ typedef struct wg_run_config { /* RunConfig + SimConfig, pipeline.hpp:23-38, sol
      * along dim 0 (periodic copies, identical initial state in each; 0 or 1
      * = the reference's grid).  Weak scaling: one copy per rank.            */
     uint64_t tile_rows;
+    /* RunConfig::chunk_size (pipeline.hpp:28): LZ chunk bytes of Codec::lz
+     * (lz_encode, codec.hpp:223-235); 0 is rejected with Codec::lz like
+     * lz_encode rejects it.  Default 64 KiB.                                 */
+    uint64_t lz_chunk_size;
 } wg_run_config;
 
 typedef struct wg_metrics_row { /* MetricsRow, pipeline.hpp:40-50 */
@@ -218,6 +223,22 @@ wg_status wg_run_initial_state(const wg_run_config* cfg, double* grid);
 wg_status wg_run(const wg_run_config* cfg, wg_metrics_row* rows,
                  uint64_t max_rows, uint64_t* nrows, double* final_grid,
                  wg_run_summary* summary);
+
+/* run() with the harness hooks of pipeline.hpp:161-181, 285-288 (metrics
+ * file, observer, snapshots) left to the caller.  After every step's metrics
+ * row (where run() writes the metrics line, calls the observer and takes
+ * snapshots) hook(user, row, NULL) is called; it returns WG_HOOK_CONTINUE,
+ * WG_HOOK_WANT_GRID (called again as hook(user, row, grid) with the current
+ * state as a grid buffer, valid during the call; the product copies it into
+ * final_grid, which must then be non-NULL) or WG_HOOK_ABORT (the run stops
+ * and returns WG_ABORTED; the caller rethrows what its hook caught).  The
+ * return value of the second call is CONTINUE or ABORT.  hook == NULL is
+ * wg_run. */
+enum { WG_HOOK_CONTINUE = 0, WG_HOOK_WANT_GRID = 1, WG_HOOK_ABORT = -1 };
+typedef int (*wg_step_hook)(void* user, const wg_metrics_row* row, const double* grid);
+wg_status wg_run_hooked(const wg_run_config* cfg, wg_metrics_row* rows,
+                        uint64_t max_rows, uint64_t* nrows, double* final_grid,
+                        wg_run_summary* summary, wg_step_hook hook, void* user);
 
 /* ---- device-resident session (the B200 hot path) ------------------------ */
 /* The state lives ONLY as a compressed patch store in HBM; one step =

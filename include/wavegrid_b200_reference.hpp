@@ -20,7 +20,11 @@
 #pragma once
 
 #include <cstdint>
+#include <cstdio>
 #include <cstring>
+#include <exception>
+#include <fstream>
+#include <memory>
 #include <span>
 #include <stdexcept>
 #include <string>
@@ -194,6 +198,7 @@ inline wg_run_config to_c(const RunConfig& rc) {
     c.strict = rc.strict ? 1 : 0;
     c.threads = rc.threads;
     c.compute_l2 = 1;
+    c.lz_chunk_size = rc.chunk_size;
     return c;
 }
 
@@ -211,26 +216,110 @@ inline MetricsRow from_c(const wg_metrics_row& r) {
     return m;
 }
 
-// run() on the device.  Harness features that are not on the hot path
-// (metrics_path, snapshots, observer) are rejected rather than silently
-// ignored; Codec::lz runs too (its stream sizes are computed on the device).
+namespace detail_b200 {
+
+// The harness around run()'s loop (pipeline.hpp:161-181, 285-288): metrics
+// CSV, observer and snapshots, driven by wg_run_hooked's per-step hook.  The
+// state is copied back only for the steps where the observer or a snapshot
+// needs it.
+struct RunHooks {
+    const RunConfig& rc;
+    std::ofstream metrics;
+    std::vector<char> snap_done;
+    PatchGrid grid;
+    std::exception_ptr err;
+
+    explicit RunHooks(const RunConfig& c)
+        : rc(c), snap_done(c.snapshot_times.size(), 0),
+          grid(decompose({c.sim.nx, c.sim.nx}, c.sim.splits, c.sim.component_count())) {}
+
+    bool snapshot_due(double t) const {
+        for (std::size_t k = 0; k < rc.snapshot_times.size(); ++k)
+            if (!snap_done[k] && !(t < rc.snapshot_times[k] - 1e-9)) return true;
+        return false;
+    }
+    void maybe_snapshot(double t) {  // pipeline.hpp:168-181
+        for (std::size_t k = 0; k < rc.snapshot_times.size(); ++k) {
+            if (snap_done[k] || t < rc.snapshot_times[k] - 1e-9) continue;
+            snap_done[k] = 1;
+            std::vector<Field> comps;
+            for (std::size_t c = 0; c < grid.components; ++c) comps.push_back(assemble(grid, c));
+            char name[64];
+            std::snprintf(name, sizeof(name), "t%.3f", rc.snapshot_times[k]);
+            save_wgrd(rc.snapshot_prefix + name + ".wgrd", comps);
+            if (rc.csv_snapshots) wavegrid::detail::write_field_csv(rc.snapshot_prefix + name + ".csv", comps[0]);
+        }
+    }
+    int on_step(const wg_metrics_row& r, const double* state) {
+        const MetricsRow row = from_c(r);
+        if (!state) {
+            if (metrics.is_open()) wavegrid::detail::write_metrics_row(metrics, row);
+            return (rc.observer || snapshot_due(row.time)) ? WG_HOOK_WANT_GRID : WG_HOOK_CONTINUE;
+        }
+        std::size_t n = 0;
+        for (const auto& p : grid.patches)
+            for (const auto& f : p.comps) n += f.values.size();
+        unpack(std::span<const double>(state, n), grid);
+        if (rc.observer) rc.observer(grid, row);
+        maybe_snapshot(row.time);
+        return WG_HOOK_CONTINUE;
+    }
+    static int trampoline(void* user, const wg_metrics_row* row, const double* state) {
+        auto* h = static_cast<RunHooks*>(user);
+        try {
+            return h->on_step(*row, state);
+        } catch (...) {  // rethrown by run() once the library has unwound
+            h->err = std::current_exception();
+            return WG_HOOK_ABORT;
+        }
+    }
+};
+
+}  // namespace detail_b200
+
+// run() on the device, with the reference's harness: the metrics file, the
+// per-step observer and the snapshots (pipeline.hpp:161-181, 285-288) are
+// served through wg_run_hooked; an exception thrown by the observer
+// propagates out of run() like the reference's.
 inline RunResult run(const RunConfig& rc) {
-    if (!rc.metrics_path.empty() || !rc.snapshot_times.empty() || rc.observer)
-        throw std::invalid_argument("b200::run: metrics files, snapshots and observers are not supported");
+    rc.sim.validate();
     const wg_run_config c = to_c(rc);
     uint64_t steps = 0, doubles = 0;
     check(wg_run_step_count(&c, &steps));
     check(wg_run_grid_doubles(&c, &doubles));
+    const bool hooked = !rc.metrics_path.empty() || !rc.snapshot_times.empty() || bool(rc.observer);
+    std::unique_ptr<detail_b200::RunHooks> h;
+    if (hooked) {
+        h = std::make_unique<detail_b200::RunHooks>(rc);
+        if (!rc.metrics_path.empty()) {
+            h->metrics.open(rc.metrics_path);
+            if (!h->metrics) throw std::runtime_error("cannot open metrics file: " + rc.metrics_path);
+            wavegrid::detail::write_metrics_header(h->metrics);
+        }
+        if (h->snapshot_due(0.0)) {  // maybe_snapshot(0.0) on the initial state
+            std::vector<double> init(doubles);
+            check(wg_run_initial_state(&c, init.data()));
+            unpack(init, h->grid);
+            h->maybe_snapshot(0.0);
+        }
+    }
     std::vector<wg_metrics_row> rows(steps ? steps : (1u << 20));
     std::vector<double> grid(doubles);
     wg_run_summary s{};
     uint64_t n = 0;
-    check(wg_run(&c, rows.data(), rows.size(), &n, grid.data(), &s));
+    const wg_status st = wg_run_hooked(&c, rows.data(), rows.size(), &n, grid.data(), &s,
+                                       hooked ? &detail_b200::RunHooks::trampoline : nullptr, h.get());
+    if (h) h->metrics.close();
+    if (st == WG_ABORTED && h && h->err) std::rethrow_exception(h->err);
+    check(st);
     RunResult res;
     for (uint64_t k = 0; k < n && k < rows.size(); ++k) res.rows.push_back(from_c(rows[k]));
     res.summary.avg_ratio = s.avg_ratio;
     res.summary.total_seconds = s.total_seconds;
     res.summary.step_seconds = s.step_seconds;
+    res.summary.dwt_seconds = s.dwt_seconds;
+    res.summary.threshold_seconds = s.threshold_seconds;
+    res.summary.codec_seconds = s.codec_seconds;
     res.grid = decompose({rc.sim.nx, rc.sim.nx}, rc.sim.splits, rc.sim.component_count());
     unpack(grid, res.grid);
     res.t_final = s.t_final;

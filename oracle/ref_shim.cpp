@@ -31,11 +31,17 @@ namespace {
 
 thread_local std::string g_err;
 
+// thrown by a wg_run_hooked observer whose hook asked to stop
+struct HookAbort {};
+
 template <typename F>
 wg_status guard(F&& f) {
     try {
         f();
         return WG_OK;
+    } catch (const HookAbort&) {
+        g_err = "run stopped by its step hook";
+        return WG_ABORTED;
     } catch (const consistency_error& e) {
         g_err = e.what();
         return WG_CONSISTENCY;
@@ -190,7 +196,8 @@ RunConfig to_run_config(const wg_run_config* c) {
     rc.levels = c->levels;
     rc.spec = ThresholdSpec{to_mode(c->threshold_mode), c->c, c->threshold_alpha};
     if (c->codec != 1 && c->codec != 2) throw std::invalid_argument("unknown codec");
-    rc.codec = c->codec == 2 ? Codec::lz : Codec::csr;  // chunk_size: the RunConfig default (64 KiB)
+    rc.codec = c->codec == 2 ? Codec::lz : Codec::csr;
+    rc.chunk_size = c->lz_chunk_size;
     rc.no_compression = c->no_compression != 0;
     rc.strict = c->strict != 0;
     rc.threads = c->threads ? c->threads : 1;
@@ -213,7 +220,9 @@ void copy_row(const MetricsRow& r, wg_metrics_row* o) {
 // sync_ghosts -> lbm_step per patch -> swap -> the per-patch compression
 // cycle of pipeline.hpp:217-257 verbatim in structure (reference functions)
 // -> metrics with global mass summed over the 9 populations.
-RunResult run_lbm(const wg_run_config* c) {
+using Observer = std::function<void(const PatchGrid&, const MetricsRow&)>;
+
+RunResult run_lbm(const wg_run_config* c, const Observer& observer = {}) {
     if (c->lbm_tau <= 0.5) throw std::invalid_argument("LBM: tau must exceed 1/2");
     const std::size_t m = 9;
     PatchGrid grid = decompose({c->nx, c->nx}, {c->splits[0], c->splits[1]}, m);
@@ -251,7 +260,7 @@ RunResult run_lbm(const wg_run_config* c) {
                 for (auto& cs : coeffs) zeroed += apply_threshold(cs, spec);
                 for (std::size_t q = 0; q < m; ++q) comps[q] = std::move(coeffs[q].values);
                 const CompressedPatch enc = encode_patch(comps, plan.dims, static_cast<std::uint32_t>(c->levels),
-                                                         c->codec == 2 ? Codec::lz : Codec::csr);
+                                                         c->codec == 2 ? Codec::lz : Codec::csr, c->lz_chunk_size);
                 auto decoded = decode_patch(enc);
                 std::size_t nnz = 0;
                 for (const auto& d : decoded)
@@ -283,6 +292,7 @@ RunResult run_lbm(const wg_run_config* c) {
         double mass = 0.0;
         for (std::size_t q = 0; q < m; ++q) mass += global_mass(grid, q);
         row.global_mass = mass;
+        if (observer) observer(grid, row);  // pipeline.hpp:285-286
         res.rows.push_back(row);
     }
     res.summary.total_seconds = total_timer.lap();
@@ -294,6 +304,26 @@ RunResult run_lbm(const wg_run_config* c) {
     res.t_final = static_cast<double>(c->lbm_steps);
     res.grid = std::move(grid);
     return res;
+}
+
+// The reference's observer (pipeline.hpp:36-37, 286) forwarding to a
+// wg_step_hook: the row first, the state only when the hook asks for it.
+Observer hook_observer(wg_step_hook hook, void* user) {
+    if (!hook) return {};
+    return [hook, user](const PatchGrid& g, const MetricsRow& r) {
+        wg_metrics_row row;
+        copy_row(r, &row);
+        int k = hook(user, &row, nullptr);
+        if (k == WG_HOOK_WANT_GRID) {
+            std::size_t n = 0;
+            for (const auto& p : g.patches)
+                for (const auto& f : p.comps) n += f.values.size();
+            std::vector<double> buf(n);
+            store_grid(g, buf.data());
+            k = hook(user, &row, buf.data());
+        }
+        if (k < 0) throw HookAbort{};
+    };
 }
 
 }  // namespace
@@ -468,6 +498,7 @@ void wg_run_config_default(wg_run_config* c) {
     c->lbm_u0 = 0.05;
     c->lbm_kappa = 80.0;
     c->lbm_delta = 0.05;
+    c->lz_chunk_size = 64 * 1024;
 }
 
 wg_status wg_run_step_count(const wg_run_config* c, uint64_t* steps) {
@@ -535,14 +566,16 @@ wg_status wg_run_initial_state(const wg_run_config* c, double* out) {
     });
 }
 
-wg_status wg_run(const wg_run_config* c, wg_metrics_row* rows, uint64_t max_rows,
-                 uint64_t* nrows, double* final_grid, wg_run_summary* summary) {
+wg_status wg_run_hooked(const wg_run_config* c, wg_metrics_row* rows, uint64_t max_rows,
+                        uint64_t* nrows, double* final_grid, wg_run_summary* summary, wg_step_hook hook,
+                        void* user) {
     return guard([&] {
         RunResult r;
         if (c->scheme == WG_SCHEME_LBM_D2Q9) {
-            r = run_lbm(c);
+            r = run_lbm(c, hook_observer(hook, user));
         } else {
             RunConfig rc = to_run_config(c);
+            rc.observer = hook_observer(hook, user);
             r = run(rc);
         }
         if (nrows) *nrows = r.rows.size();
@@ -561,6 +594,11 @@ wg_status wg_run(const wg_run_config* c, wg_metrics_row* rows, uint64_t max_rows
             summary->steps = r.rows.size();
         }
     });
+}
+
+wg_status wg_run(const wg_run_config* c, wg_metrics_row* rows, uint64_t max_rows,
+                 uint64_t* nrows, double* final_grid, wg_run_summary* summary) {
+    return wg_run_hooked(c, rows, max_rows, nrows, final_grid, summary, nullptr, nullptr);
 }
 
 }  // extern "C"

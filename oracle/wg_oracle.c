@@ -719,6 +719,7 @@ void wg_run_config_default(wg_run_config* c) { /* RunConfig{}, SimConfig{} */
     c->lbm_u0 = 0.05;
     c->lbm_kappa = 80.0;
     c->lbm_delta = 0.05;
+    c->lz_chunk_size = 64 * 1024;
 }
 
 static uint32_t comps_of(int scheme) {
@@ -913,13 +914,13 @@ static uint64_t lz_chunk_payload(const unsigned char* in, uint64_t n) {
     return out;
 }
 
-/* LzStream::byte_size of lz_encode(bytes, 64 KiB chunks) (codec.hpp:99-105, 223-235). */
-static uint64_t lz_stream_size(const double* a, uint64_t count) {
+/* LzStream::byte_size of lz_encode(bytes, chunk) (codec.hpp:99-105, 223-235). */
+static uint64_t lz_stream_size(const double* a, uint64_t count, uint64_t chunk) {
     const unsigned char* b = (const unsigned char*)a;
     const uint64_t bytes = count * 8;
     uint64_t s = 0;
-    for (uint64_t off = 0; off < bytes; off += 65536)
-        s += 8 + lz_chunk_payload(b + off, bytes - off < 65536 ? bytes - off : 65536);
+    for (uint64_t off = 0; off < bytes; off += chunk)
+        s += 8 + lz_chunk_payload(b + off, bytes - off < chunk ? bytes - off : chunk);
     return s;
 }
 
@@ -950,7 +951,7 @@ static wg_status compress_patch(const wg_run_config* c, const grid_t* g, double*
     }
     for (uint32_t q = 0; q < m; ++q) { /* CSR round trip: bytes, nnz, -0.0 -> +0.0 */
         double* cs = coef + q * n0 * n1;
-        if (c->codec == 2) comp_bytes += lz_stream_size(cs, n0 * n1); /* Codec::lz: the thresholded bytes */
+        if (c->codec == 2) comp_bytes += lz_stream_size(cs, n0 * n1, c->lz_chunk_size); /* Codec::lz: the thresholded bytes */
         uint64_t k = 0;
         for (uint64_t e = 0; e < n0 * n1; ++e) {
             if (cs[e] != 0.0) ++k;
@@ -978,14 +979,19 @@ static wg_status compress_patch(const wg_run_config* c, const grid_t* g, double*
 
 /* run(RunConfig), pipeline.hpp:129-305 (single thread; the thread count of
  * the reference does not change results, test_pipeline.cpp:55-71). */
-wg_status wg_run(const wg_run_config* c, wg_metrics_row* rows, uint64_t max_rows,
-                 uint64_t* nrows, double* final_grid, wg_run_summary* summary) {
+/* run(), pipeline.hpp:129-305; the hook is called where run() writes the
+ * metrics line and calls the observer (pipeline.hpp:285-286). */
+wg_status wg_run_hooked(const wg_run_config* c, wg_metrics_row* rows, uint64_t max_rows,
+                        uint64_t* nrows, double* final_grid, wg_run_summary* summary,
+                        wg_step_hook hook, void* user) {
     grid_t g;
     wg_status st;
     if (c->scheme != WG_SCHEME_LBM_D2Q9 && (st = sim_validate(c))) return st;
     if ((st = run_grid(c, &g))) return st;
     if ((st = plan_validate(g.n, 2, c->levels))) return st;
     if (c->codec != 1 && c->codec != 2) return fail(WG_INVALID_ARGUMENT, "unknown codec");
+    if (c->codec == 2 && c->lz_chunk_size == 0)
+        return fail(WG_INVALID_ARGUMENT, "lz_encode: chunk_size must be > 0");
     if (c->scheme == WG_SCHEME_LBM_D2Q9 && c->lbm_tau <= 0.5)
         return fail(WG_INVALID_ARGUMENT, "LBM: tau must exceed 1/2");
     const uint64_t total = g.npatch * g.m * g.tcount;
@@ -1073,6 +1079,14 @@ wg_status wg_run(const wg_run_config* c, wg_metrics_row* rows, uint64_t max_rows
             }
             if ((st = assemble_g(&g, grid, 0, 1e-12, asm_buf, seen))) break;
         }
+        if (hook) {
+            int k = hook(user, &row, NULL);
+            if (k == WG_HOOK_WANT_GRID) k = hook(user, &row, grid);
+            if (k < 0) {
+                st = fail(WG_ABORTED, "run stopped by its step hook");
+                break;
+            }
+        }
         if (rows && step <= max_rows) rows[step - 1] = row;
         ratio_sum += row.ratio;
     }
@@ -1094,4 +1108,9 @@ wg_status wg_run(const wg_run_config* c, wg_metrics_row* rows, uint64_t max_rows
     free(asm_buf);
     free(seen);
     return st;
+}
+
+wg_status wg_run(const wg_run_config* c, wg_metrics_row* rows, uint64_t max_rows,
+                 uint64_t* nrows, double* final_grid, wg_run_summary* summary) {
+    return wg_run_hooked(c, rows, max_rows, nrows, final_grid, summary, NULL, NULL);
 }

@@ -54,6 +54,10 @@ class LogicError(WavegridError):
     status = 9
 
 
+class Aborted(WavegridError):  # a wg_run_hooked hook stopped the run
+    status = 10
+
+
 class InvalidArgument(WavegridError, ValueError):  # std::invalid_argument
     status = 1
 
@@ -72,6 +76,7 @@ _EXC = {
     7: OutOfMemoryError,
     8: OutOfRange,
     9: LogicError,
+    10: Aborted,
 }
 
 # ---- enums ------------------------------------------------------------------
@@ -131,6 +136,7 @@ class RunConfigC(C.Structure):
         ("lbm_delta", f64),
         ("store_budget_bytes", u64),
         ("tile_rows", u64),
+        ("lz_chunk_size", u64),
     ]
 
 
@@ -208,6 +214,7 @@ _PROTOS = {
     "wg_run_grid_doubles": (i32, [P(RunConfigC), P(u64)]),
     "wg_run_initial_state": (i32, [P(RunConfigC), dp]),
     "wg_run": (i32, [P(RunConfigC), P(MetricsRowC), u64, P(u64), dp, P(RunSummaryC)]),
+    "wg_run_hooked": (i32, [P(RunConfigC), P(MetricsRowC), u64, P(u64), dp, P(RunSummaryC), vp, vp]),
     # device session (product only)
     "wg_session_create": (i32, [P(RunConfigC), P(ShardC), vp, P(vp)]),
     "wg_session_destroy": (i32, [vp]),

@@ -382,6 +382,7 @@ class RunConfig:
     tile_rows: int = 1
     metrics_path: str = ""       # RunConfig::metrics_path: CSV of the rows (pipeline.hpp:162-166)
     codec: str = "csr"           # RunConfig::codec: "csr" or "lz" (codec.hpp:250)
+    chunk_size: int = 64 * 1024  # RunConfig::chunk_size: LZ chunk bytes (pipeline.hpp:28)
 
     def to_c(self) -> abi.RunConfigC:
         c = abi.RunConfigC()
@@ -402,6 +403,7 @@ class RunConfig:
         c.lbm_tau, c.lbm_u0, c.lbm_kappa, c.lbm_delta = self.lbm_tau, self.lbm_u0, self.lbm_kappa, self.lbm_delta
         c.store_budget_bytes = self.store_budget_bytes
         c.tile_rows = self.tile_rows
+        c.lz_chunk_size = self.chunk_size
         return c
 
     @property

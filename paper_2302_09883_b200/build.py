@@ -82,7 +82,8 @@ def build_oracles(reference: bool = True) -> None:
     subprocess.run(["make", "-s", "-C", str(REPO / "oracle"), *targets], check=True)
     if "ref" in targets and LIB.exists():
         # the C++ drop-in test programs need the reference headers (here only)
-        subprocess.run(["make", "-s", "-C", str(REPO / "tests" / "cpp"), "all"], check=True)
+        # and the reference's own suites routed through the drop-in (tests/cpp/Makefile)
+        subprocess.run(["make", "-s", "-j8", "-C", str(REPO / "tests" / "cpp"), "all", "reftests"], check=True)
 
 
 if __name__ == "__main__":

@@ -241,6 +241,7 @@ void wg_run_config_default(wg_run_config* c) {  // RunConfig{}, SimConfig{}
     c->lbm_u0 = 0.05;
     c->lbm_kappa = 80.0;
     c->lbm_delta = 0.05;
+    c->lz_chunk_size = 64 * 1024;
 }
 
 wg_status wg_band_threshold(const int32_t* scales, uint32_t rank, int32_t mode, double c,

@@ -289,7 +289,7 @@ struct LzFinal {
 // read through L2 (it was written by the step kernel just before).
 constexpr int kLzWarps = 2;  // per CTA: 32 KiB of tables, 7 CTAs (14 warps) per SM
 __global__ void __launch_bounds__(32 * kLzWarps) k_lz_sizes(const double* dense, uint64_t nblocks, uint32_t nn,
-                                                            LzFinal f) {
+                                                            uint32_t chunk, LzFinal f) {
     __shared__ __align__(16) unsigned short tables[kLzWarps][8192];
     unsigned long long k = 0;
     if (f.steps) {
@@ -303,8 +303,11 @@ __global__ void __launch_bounds__(32 * kLzWarps) k_lz_sizes(const double* dense,
     for (uint64_t b = wid; b < nblocks; b += nw) {
         const unsigned char* in = reinterpret_cast<const unsigned char*>(dense + b * nn);
         const uint32_t bytes = nn * 8;
-        for (uint32_t off = 0; off < bytes; off += 65536u) {
-            const uint32_t len = min(65536u, bytes - off);
+        // RunConfig::chunk_size (lz_encode, codec.hpp:223-235); a block is at
+        // most 65^2 x 8 = 33800 bytes, so every chunk parses with 16-bit
+        // table positions whatever the configured size
+        for (uint32_t off = 0; off < bytes; off += chunk) {
+            const uint32_t len = min(chunk, bytes - off);
             sum += 8 + lz_chunk_size_warp(in + off, len, table);
         }
     }
@@ -541,6 +544,9 @@ struct Session {
 
     bool is_swe() const { return cfg.scheme == WG_SCHEME_SWE; }
     // patches per staging chunk of a pinned-host upload (16 MB of grid buffer)
+    // LZ chunk bytes (RunConfig::chunk_size), clamped to 32 bits: a block is
+    // far smaller, so a larger chunk is the same single chunk
+    uint32_t lz_chunk() const { return (uint32_t)std::min<uint64_t>(cfg.lz_chunk_size, 0xFFFFFFFFull); }
     uint32_t stage_chunk() const {
         return (uint32_t)std::max<uint64_t>(1, (16ull << 20) / ((uint64_t)sg.m * geo.tcount * 8));
     }
@@ -551,6 +557,7 @@ struct Session {
     void create(const wg_run_config& c, const wg_shard* sh, void* strm) {
         cfg = c;
         if (cfg.codec != 1 && cfg.codec != 2) raise(WG_INVALID_ARGUMENT, "unknown codec");
+        if (cfg.codec == 2 && cfg.lz_chunk_size == 0) raise(WG_INVALID_ARGUMENT, "lz_encode: chunk_size must be > 0");
 
         if (cfg.scheme != WG_SCHEME_LBM_D2Q9) sim_validate(cfg);
         if (cfg.scheme == WG_SCHEME_LBM_D2Q9 && cfg.lbm_tau <= 0.5)
@@ -629,8 +636,11 @@ struct Session {
         // atomic, small enough that the unused tails (<= one chunk per CTA)
         // stay a small fraction of the pool
         chunk = std::clamp<uint64_t>(round16(blocks * raw_block / (8ull * grid)), 4096, 256 * 1024);
-        cap = cfg.store_budget_bytes ? cfg.store_budget_bytes / 2
-                                     : blocks * raw_block + blocks * raw_block / 8 + (uint64_t)grid * chunk;
+        // without a budget the pools hold the worst case, every block a dense
+        // CSR block (12 N^2 + 4 (N + 1) bytes: 1.5x raw) — a valid run of the
+        // reference never overflows the store, whatever the threshold
+        const uint64_t csr_max = round16(12ull * N * N + 4ull * (N + 1));
+        cap = cfg.store_budget_bytes ? cfg.store_budget_bytes / 2 : blocks * csr_max + (uint64_t)grid * chunk;
         cap = std::max<uint64_t>(cap, 16) & ~uint64_t(15);
         for (int k = 0; k < 2; ++k) {
             store[k] = dalloc<unsigned char>(cap);
@@ -918,7 +928,7 @@ struct Session {
             ev_main.emplace_back(e0, e1);
         }
         if (lz_dense) {  // Codec::lz: the step's compressed_bytes/ratio from the LZ stream sizes
-            k_lz_sizes<<<lz_ctas, 32 * kLzWarps, 0, stream>>>(lz_dense, (uint64_t)sg.npatch * sg.m, N * N,
+            k_lz_sizes<<<lz_ctas, 32 * kLzWarps, 0, stream>>>(lz_dense, (uint64_t)sg.npatch * sg.m, N * N, lz_chunk(),
                                                                LzFinal{lz_done, a.row_out, nullptr, nullptr});
             WG_LAUNCH_CHECK("lz sizes");
         }
@@ -959,7 +969,7 @@ struct Session {
         WG_LAUNCH_CHECK("fused swe step");
         if (lz_dense) {
             const uint64_t nb = (uint64_t)sg.npatch * sg.m;
-            k_lz_sizes<<<lz_ctas, 32 * kLzWarps, 0, stream>>>(lz_dense, nb, N * N,
+            k_lz_sizes<<<lz_ctas, 32 * kLzWarps, 0, stream>>>(lz_dense, nb, N * N, lz_chunk(),
                                                                LzFinal{lz_done, nullptr, rows - row0, swe + 4});
             WG_LAUNCH_CHECK("lz sizes");
         }
@@ -1062,7 +1072,7 @@ struct Session {
             WG_CUDA(cudaEventRecord(consumed[c % 3], stream));
         }
         if (lz_dense) {
-            k_lz_sizes<<<lz_ctas, 32 * kLzWarps, 0, stream>>>(lz_dense, (uint64_t)sg.npatch * sg.m, N * N,
+            k_lz_sizes<<<lz_ctas, 32 * kLzWarps, 0, stream>>>(lz_dense, (uint64_t)sg.npatch * sg.m, N * N, lz_chunk(),
                                                                LzFinal{lz_done, a.row_out, nullptr, nullptr});
             WG_LAUNCH_CHECK("lz sizes");
         }
@@ -1355,8 +1365,10 @@ struct Session {
                     if (ro[0] != 0 || ro[N] != nv) raise(WG_CORRUPT_STREAM, "csr_decode: row offsets");
                     for (uint32_t r = 0; r < N; ++r)
                         if (ro[r] > ro[r + 1]) raise(WG_CORRUPT_STREAM, "csr_decode: row offsets");
-                    for (uint64_t k = 0; k < nv; ++k)
-                        if (co[k] >= N) raise(WG_CORRUPT_STREAM, "csr_decode: column out of range");
+                    for (uint32_t r = 0; r < N; ++r)  // columns in range and strictly increasing per row
+                        for (uint32_t k = ro[r]; k < ro[r + 1]; ++k)
+                            if (co[k] >= N || (k > ro[r] && co[k] <= co[k - 1]))
+                                raise(WG_CORRUPT_STREAM, "csr_decode: bad column index");
                     e.nnz = (uint32_t)nv;
                     e.flags = 0;
                 } else {  // LzStream (lz_decode, codec.hpp:177-244) of the raw block
@@ -1695,8 +1707,8 @@ wg_status wg_session_profile_read(wg_session* sp, double* main_ms, uint64_t* lau
 }
 
 // run(RunConfig) (pipeline.hpp:129-305) on one device through a session.
-wg_status wg_run(const wg_run_config* cfg, wg_metrics_row* rows, uint64_t max_rows, uint64_t* nrows,
-                 double* final_grid, wg_run_summary* summary) {
+wg_status wg_run_hooked(const wg_run_config* cfg, wg_metrics_row* rows, uint64_t max_rows, uint64_t* nrows,
+                        double* final_grid, wg_run_summary* summary, wg_step_hook hook, void* user) {
     return guard([&] {
         if (cfg->scheme != WG_SCHEME_LBM_D2Q9) sim_validate(*cfg);
         const RunGeometry g = run_geometry(*cfg);
@@ -1720,6 +1732,28 @@ wg_status wg_run(const wg_run_config* cfg, wg_metrics_row* rows, uint64_t max_ro
             s.step_from_host(grid.data(), dts[0]);
             dts.erase(dts.begin());
         }
+        // the caller's per-step hook (metrics file, observer, snapshots:
+        // pipeline.hpp:285-288): the step's row, then the state on request
+        if (hook && !final_grid) raise(WG_INVALID_ARGUMENT, "wg_run_hooked: a hook needs the final_grid buffer");
+        auto after_step = [&] {
+            if (!hook) return;
+            wg_metrics_row row{};
+            s.sync();
+            WG_CUDA(cudaMemcpy(&row, s.rows + (s.step - 1 - s.row0), sizeof row, cudaMemcpyDeviceToHost));
+            if (cfg->strict && !cfg->no_compression) {  // the mass half, before the observer sees the row
+                double mfv = 0.0;
+                WG_CUDA(cudaMemcpy(&mfv, s.mass_fv + (s.step - 1 - s.row0), sizeof mfv, cudaMemcpyDeviceToHost));
+                if (std::abs(row.global_mass - mfv) > 1e-12 * std::max(std::abs(mfv), 1.0))
+                    raise(WG_CONSISTENCY, "strict: compression cycle changed global mass");
+            }
+            int k = hook(user, &row, nullptr);
+            if (k == WG_HOOK_WANT_GRID) {
+                s.download(final_grid);
+                k = hook(user, &row, final_grid);
+            }
+            if (k < 0) raise(WG_ABORTED, "run stopped by its step hook");
+        };
+        if (streamed) after_step();
         if (s.is_swe()) {
             // the step count is known only on the device: launch batches
             // sized from the current dt, then read the clock back
@@ -1728,18 +1762,20 @@ wg_status wg_run(const wg_run_config* cfg, wg_metrics_row* rows, uint64_t max_ro
                 double td[2];  // [t, dt of the last step]
                 WG_CUDA(cudaMemcpy(td, s.swe_td(), sizeof td, cudaMemcpyDeviceToHost));
                 const double est = td[1] > 0.0 ? std::ceil((cfg->t_end - td[0]) / td[1]) : 16.0;
-                const uint64_t batch = cfg->strict ? 1 : (uint64_t)std::clamp(est, 1.0, 512.0);
+                const uint64_t batch = (cfg->strict || hook) ? 1 : (uint64_t)std::clamp(est, 1.0, 512.0);
                 const uint64_t before = s.step;
                 for (uint64_t k = 0; k < batch; ++k) s.do_step(0.0);
                 s.sync();
                 if (cfg->strict && !cfg->no_compression) s.check_shared(1e-12);
                 if (s.step == before) raise(WG_LOGIC, "SWE step loop made no progress");
+                after_step();
             }
         } else {
             for (double dt : dts) {
                 s.do_step(dt);
                 // strict (pipeline.hpp:278-283): assemble(grid, 0) every step
                 if (cfg->strict && !cfg->no_compression) s.check_shared(1e-12);
+                after_step();
             }
         }
         WG_CUDA(cudaEventRecord(e1, s.stream));
@@ -1787,6 +1823,11 @@ wg_status wg_run(const wg_run_config* cfg, wg_metrics_row* rows, uint64_t max_ro
             summary->steps = s.step;
         }
     });
+}
+
+wg_status wg_run(const wg_run_config* cfg, wg_metrics_row* rows, uint64_t max_rows, uint64_t* nrows,
+                 double* final_grid, wg_run_summary* summary) {
+    return wg_run_hooked(cfg, rows, max_rows, nrows, final_grid, summary, nullptr, nullptr);
 }
 
 }  // extern "C"
