@@ -271,8 +271,8 @@ def config_json(args, w):
                            + (" (weak: one periodic copy of the grid per rank)" if w.get("scaling", "weak") == "weak" else
                               " (strong: the grid split over the ranks)"),
             "halo_exchange": ("none (one shard)" if args.gpus == 1 else
-                              "in-kernel NVLink peer stores (WG_PEER_HALOS=1)"
-                              if os.environ.get("WG_PEER_HALOS") == "1" and w["scheme"] != "swe"
+                              "in-kernel NVLink peer stores (CUDA IPC; WG_PEER_HALOS=0: NCCL)"
+                              if os.environ.get("WG_PEER_HALOS", "1") == "1" and w["scheme"] != "swe"
                               else "NCCL point-to-point between steps"),
             "l2": "flushed between timed steps (256 MiB write)"}
 
@@ -323,6 +323,13 @@ def bench_b200(args, w: dict):
             dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
         else:
             dist.init_process_group(backend)
+        # visible communicator: every rank's device, gathered over the process group
+        names = [None] * world
+        dist.all_gather_object(names, f"rank {rank}: cuda:{local} {torch.cuda.get_device_name(local)}")
+        if rank == 0:
+            nccl_v = ".".join(map(str, torch.cuda.nccl.version())) if backend == "nccl" else "-"
+            print(f"[bench] process group {backend} (NCCL {nccl_v}) world {world}: " + "; ".join(names),
+                  file=sys.stderr, flush=True)
     lib = abi.load_product()
     cfg = run_config(w, args.warmup + args.steps)
     dt = transport_dt(cfg) if w["scheme"] == "transport" else 1.0
@@ -529,10 +536,10 @@ def e2e_run(lib, cfg, shard, stream, host, args, dt, dist, copies=1, streamed=Fa
 
 
 def peer_halos_wanted(cfg, dist, world: int) -> bool:
-    """WG_PEER_HALOS=1 (opt-in until validated on a multi-GPU box): the step
-    kernels store the halo lines into the neighbours' halo slots over NVLink
-    (CUDA IPC), instead of an NCCL exchange between steps."""
-    return (world > 1 and os.environ.get("WG_PEER_HALOS") == "1" and cfg.scheme != "swe"
+    """Peer halo mode (default at N > 1 over NCCL; WG_PEER_HALOS=0 selects the
+    NCCL point-to-point exchange between steps): the step kernels store the
+    halo lines into the neighbours' halo slots over NVLink (CUDA IPC)."""
+    return (world > 1 and os.environ.get("WG_PEER_HALOS", "1") == "1" and cfg.scheme != "swe"
             and dist is not None and dist.get_backend() == "nccl")
 
 
@@ -555,12 +562,16 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
-    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="lbm_c4")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default=None,
+                    help="default: lbm_c4 (BASELINE configs[3]) at N=1, lbm_c5 (configs[4], the grid split "
+                         "over the ranks, peer halos) at N>1")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-steps", type=int, default=0, help="CPU baseline steps (0: ~12 s of work)")
     args = ap.parse_args()
     if args.impl == "b200":
         args.warmup = max(args.warmup, 3)  # timing rule: at least 3 untimed warm-up steps
+    if args.workload is None:
+        args.workload = "lbm_c4" if args.gpus == 1 else "lbm_c5"
     w = dict(WORKLOADS[args.workload])
     w["_name"] = args.workload
     if args.impl == "reference":

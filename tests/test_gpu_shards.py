@@ -229,3 +229,68 @@ def test_peer_halos_reject_swe(product):
             two.sessions[0].peer_attach(ex[1], ex[1])
     finally:
         two.close()
+
+
+def _block(lib, sess, patch: int, comp: int, n: int):
+    v = np.zeros(n * n)
+    col = np.zeros(n * n, dtype=np.uint32)
+    row = np.zeros(n + 1, dtype=np.uint32)
+    nnz, raw = abi.u64(), C.c_int32()
+    lib.check(lib.wg_session_patch_csr(sess.handle, patch, comp, abi.dptr(v), col.ctypes.data_as(C.POINTER(C.c_uint32)),
+                                       row.ctypes.data_as(C.POINTER(C.c_uint32)), C.byref(nnz), C.byref(raw)))
+    k = nnz.value if not raw.value else n * n
+    return raw.value, bits(v[:k]).tobytes(), col[: nnz.value].tobytes(), row.tobytes()
+
+
+def test_peer_halos_c5_geometry(product):
+    """Peer halo mode at the C5 geometry (65536^2 grid: 1024 x 1024 patches of
+    65^2 points, L = 4, capped 1e-3, device initial state): a band of 8 patch
+    rows (8192 patches) as ONE shard (periodic over the band) against the
+    same band as 4 peer-attached shards of 2 rows each — the step kernels
+    store every halo line into the neighbour shard's slots.  Per-step counts
+    equal, masses to round-off, and the stored CSR blocks of sampled patches
+    (both sides of every shard boundary) bitwise equal."""
+    import torch
+
+    cfg = _cfg("lbm", 65537, (1024, 1024), 4, 1e-3)
+    R, world, steps, n = 8, 4, 4, 65
+    stream = torch.cuda.Stream()
+    single = ShardedSession(product, cfg, ShardInfo(0, 1, 0, R, 0), stream.cuda_stream, None)
+    per = R // world
+    multi = [ShardedSession(product, cfg, ShardInfo(r, world, per * r, per * (r + 1), 0), stream.cuda_stream, None)
+             for r in range(world)]
+    try:
+        ex = [s.peer_export() for s in multi]
+        for r, s in enumerate(multi):
+            s.peer_attach(ex[(r - 1) % world], ex[(r + 1) % world])
+        product.check(product.wg_session_init_device(single.handle))
+        for s in multi:
+            product.check(product.wg_session_init_device(s.handle))
+        for s in multi:  # every shard built its own edges: now the halo rows
+            s.peer_push()
+        for _ in range(steps):
+            product.check(product.wg_session_step(single.handle, 1.0))
+            for s in multi:
+                product.check(product.wg_session_step(s.handle, 1.0))
+        single.sync()
+        for s in multi:
+            s.sync()
+        r1, rn = single.rows(), [s.rows() for s in multi]
+        assert len(r1) == steps
+        for k in range(steps):
+            for key in ("dense_bytes", "compressed_bytes", "nnz", "zeroed"):
+                assert r1[k][key] == sum(p[k][key] for p in rn), key
+            m = sum(p[k]["global_mass"] for p in rn)
+            assert abs(m - r1[k]["global_mass"]) <= 1e-12 * abs(r1[k]["global_mass"])
+        P1 = 1024
+        for row in range(R):  # first, middle and last patch of every patch row, all 9 populations
+            owner, local_row = row // per, row % per
+            for col in (0, 511, 1023):
+                for q in range(9):
+                    a = _block(product, single, row * P1 + col, q, n)
+                    b = _block(product, multi[owner], local_row * P1 + col, q, n)
+                    assert a == b, (row, col, q)
+    finally:
+        single.close()
+        for s in multi:
+            s.close()
