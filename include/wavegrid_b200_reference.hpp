@@ -23,6 +23,7 @@
 #include <cstdio>
 #include <cstring>
 #include <exception>
+#include <filesystem>
 #include <fstream>
 #include <memory>
 #include <span>
@@ -324,6 +325,46 @@ inline RunResult run(const RunConfig& rc) {
     unpack(grid, res.grid);
     res.t_final = s.t_final;
     return res;
+}
+
+// sweep(SweepConfig) (pipeline.hpp:360-401) with every run on the device:
+// the same grid of (codec, level, threshold) runs, metrics files and
+// summary.csv, the runs going through b200::run.
+inline std::vector<SweepEntry> sweep(const SweepConfig& sc) {
+    namespace fs = std::filesystem;
+    if (!sc.out_dir.empty()) fs::create_directories(sc.out_dir);
+    std::vector<SweepEntry> table;
+    for (const Codec codec : sc.codecs)
+        for (const int level : sc.levels)
+            for (const double c : sc.thresholds) {
+                RunConfig rc = sc.base;
+                rc.codec = codec;
+                rc.levels = level;
+                rc.spec.c = c;
+                char file[128];
+                std::snprintf(file, sizeof file, "run_%s_L%d_c%g.csv", codec == Codec::lz ? "lz" : "csr", level, c);
+                rc.metrics_path = sc.out_dir.empty() ? std::string(file) : (fs::path(sc.out_dir) / file).string();
+                const RunResult r = run(rc);
+                SweepEntry e;
+                e.codec = codec;
+                e.level = level;
+                e.threshold = c;
+                e.avg_ratio = r.summary.avg_ratio;
+                e.final_l2 = r.rows.empty() ? 0.0 : r.rows.back().l2;
+                e.metrics_file = rc.metrics_path;
+                table.push_back(std::move(e));
+            }
+    if (!sc.out_dir.empty()) {
+        std::ofstream os((fs::path(sc.out_dir) / "summary.csv").string());
+        os << "codec,level,threshold,avg_ratio,final_l2_error,metrics_file\n";
+        for (const SweepEntry& e : table) {
+            char line[256];
+            std::snprintf(line, sizeof line, "%s,%d,%.17g,%.17g,%.17g,", e.codec == Codec::lz ? "lz" : "csr", e.level,
+                          e.threshold, e.avg_ratio, e.final_l2);
+            os << line << e.metrics_file << '\n';
+        }
+    }
+    return table;
 }
 
 // ---- the device-resident loop ------------------------------------------------

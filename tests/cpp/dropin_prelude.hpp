@@ -15,8 +15,8 @@
 // the sm_100a product on the GPU box, the C oracle on CPU.
 //
 // Routed: dwt_nd, idwt_nd, band_threshold, apply_threshold, csr_encode,
-// csr_decode, sync_ghosts, global_mass, run.  Not routed: the per-patch
-// fv_step template (the drop-in's fv_step is per grid) and the reference's
+// csr_decode, sync_ghosts, global_mass, run, sweep (its runs through the
+// drop-in's run).  Not routed: the per-patch fv_step template (the drop-in's fv_step is per grid) and the reference's
 // non-path helpers (decompose, fill, assemble, lz_*, file formats).
 #pragma once
 
@@ -57,6 +57,7 @@
 #define sync_ghosts(...) ref_cpu_sync_ghosts(__VA_ARGS__)
 #define global_mass(...) ref_cpu_global_mass(__VA_ARGS__)
 #define run(...) ref_cpu_run(__VA_ARGS__)
+#define sweep(...) ref_cpu_sweep(__VA_ARGS__)
 
 #include "wavegrid/codec.hpp"
 #include "wavegrid/field.hpp"
@@ -75,6 +76,7 @@
 #undef sync_ghosts
 #undef global_mass
 #undef run
+#undef sweep
 
 #include "wavegrid_b200_reference.hpp"
 
@@ -87,5 +89,6 @@ using b200::dwt_nd;
 using b200::global_mass;
 using b200::idwt_nd;
 using b200::run;
+using b200::sweep;
 using b200::sync_ghosts;
 }  // namespace wavegrid
