@@ -344,7 +344,7 @@ inline std::vector<SweepEntry> sweep(const SweepConfig& sc) {
                 char file[128];
                 std::snprintf(file, sizeof file, "run_%s_L%d_c%g.csv", codec == Codec::lz ? "lz" : "csr", level, c);
                 rc.metrics_path = sc.out_dir.empty() ? std::string(file) : (fs::path(sc.out_dir) / file).string();
-                const RunResult r = run(rc);
+                const RunResult r = b200::run(rc);
                 SweepEntry e;
                 e.codec = codec;
                 e.level = level;

@@ -293,15 +293,27 @@ __host__ __device__ __forceinline__ double lbm_feq(int q, double rho, double cu,
 // BGK collide of the 9 pulled populations f (in place); returns the density.
 //   rho = sum_q f_q (sequential), j = (x, y) momentum sums, u = j * (1 / rho)
 //   f_q <- fma(omega, feq_q - f_q, f_q)          (= f - (f - feq) omega)
-__host__ __device__ __forceinline__ double lbm_collide(double (&f)[9], double omega) {
+// The moments of the collide: density (returned) and velocity.
+__host__ __device__ __forceinline__ double lbm_moments(const double (&f)[9], double& ux, double& uy) {
     const double rho = ((((((((f[0] + f[1]) + f[2]) + f[3]) + f[4]) + f[5]) + f[6]) + f[7]) + f[8]);
     const double jx = ((f[1] - f[2]) + (f[5] - f[6])) + (f[7] - f[8]);
     const double jy = ((f[3] - f[4]) + (f[5] - f[6])) + (f[8] - f[7]);
     const double inv = 1.0 / rho;
-    const double ux = jx * inv, uy = jy * inv;
+    ux = jx * inv;
+    uy = jy * inv;
+    return rho;
+}
+// The relaxation of one population toward its equilibrium.
+__host__ __device__ __forceinline__ double lbm_relax(int q, double fq, double rho, double ux, double uy, double usq,
+                                                     double omega) {
+    return fma(omega, lbm_feq(q, rho, lbm_cu(q, ux, uy), usq) - fq, fq);
+}
+__host__ __device__ __forceinline__ double lbm_collide(double (&f)[9], double omega) {
+    double ux, uy;
+    const double rho = lbm_moments(f, ux, uy);
     const double usq = lbm_usq(ux, uy);
 #pragma unroll
-    for (int q = 0; q < 9; ++q) f[q] = fma(omega, lbm_feq(q, rho, lbm_cu(q, ux, uy), usq) - f[q], f[q]);
+    for (int q = 0; q < 9; ++q) f[q] = lbm_relax(q, f[q], rho, ux, uy, usq, omega);
     return rho;
 }
 
