@@ -549,10 +549,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<N>::NT, 1
                 }
                 __syncthreads();
                 WG_PHASE_MARK(21);
-                // MODE_DECODE: the next patch's inputs (the staging area is free
-                // once D1 has run).  The step modes park the collide's moments
-                // there and prefetch after M2 (or after the raw store).
-                if (MODE == MODE_DECODE && t == CTL && !cur_redo && cur_p + npairs < p_end) {
+                // next patch's inputs: the staging area is free once D1 has run
+                // (the skip rule's re-derivation reads the global copies)
+                if (t == CTL && !cur_redo && cur_p + npairs < p_end) {
                     fence_proxy_async();
                     prefetch(cur_p + npairs, par ^ 1);
                 }
@@ -618,121 +617,57 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<N>::NT, 1
                 // D2 has read the ghosts: gather the next patch's (asynchronously,
                 // completed at the end of this patch)
                 if (cur_p + npairs < p_end) gather_ghosts(cur_p + npairs);
-                // C: BGK collide (lbm_collide, physics.cuh) in two halves, with
-                // DSMEM traffic as pure remote LOADS (B200: mixing remote loads
-                // and stores on one direction of the pair halves its throughput,
-                // profiles/r2_dsmem_duplex.txt):
-                //   C1  cells of this CTA's column half: the peer's 4 populations
-                //       loaded over DSMEM, the moments (rho, u) computed, the own
-                //       4 populations and population 0 relaxed locally, the
-                //       moments parked in shared memory (the staging area and
-                //       population 0's other half: both free until F1 / M2);
-                //   C2  cells of the peer's half: its parked moments loaded over
-                //       DSMEM, the own 4 populations relaxed locally.
-                // Same operations as lbm_collide per cell (bit-identical).  The
-                // mass of the scheme output (strict check) as w * rho per cell.
+                // C: BGK collide of this CTA's column half (lbm_collide, physics.cuh);
+                // the mass of the scheme output (strict check) as w * rho per
+                // cell (BGK conserves it; a tolerance-checked diagnostic)
                 {
                     const unsigned rank = cluster_rank(), peer = rank ^ 1u;
                     cg::cluster_group cluster = cg::this_cluster();
-                    const bool redo = cur_redo != 0;
-                    constexpr int H = H0, cells = N * H;
-                    constexpr int K = WG_LBM_CELLS;  // cells per iteration (independent chains)
-                    // moment planes of a rank's half (cell (i, jl), jl = j - lo):
-                    // rho and ux in the staging area, uy in population 0's other
-                    // column half (its last column past the two planes)
-                    double* const mrho = reinterpret_cast<double*>(stage);
-                    double* const mux = mrho + cells;
-                    double* const mxt = mux + cells;  // uy of the columns past population 0's other half
-                    auto uy_at = [&](double* base_bufs, double* base_xt, unsigned r, int i, int jl) -> double* {
-                        const int olo = r == 0 ? H0 : 0, ow = r == 0 ? N - H0 : H0;
-                        return jl < ow ? base_bufs + (size_t)i * N + olo + jl : base_xt + i;
-                    };
-                    {
-                        double* P[9];  // population pointers (the peer's 4 through DSMEM, read only)
+                    double* P[9];  // population pointers (the peer's populations through DSMEM)
 #pragma unroll
-                        for (int k = 0; k < 9; ++k) {
-                            const bool mine = k == 0 || pop_owner(k) == (int)rank;
-                            const int sl = pop_slot(k);
-                            P[k] = mine ? bufs + (size_t)sl * BUFD : cluster.map_shared_rank(bufs + (size_t)sl * BUFD, peer);
-                        }
+                    for (int k = 0; k < 9; ++k) {
+                        const bool mine = k == 0 || pop_owner(k) == (int)rank;
+                        const int sl = pop_slot(k);
+                        P[k] = mine ? bufs + (size_t)sl * BUFD : cluster.map_shared_rank(bufs + (size_t)sl * BUFD, peer);
+                    }
+                    const bool redo = cur_redo != 0;
+                    {
+                        // one code path for both ranks: H0 columns from lo (rank 1's
+                        // half is one column narrower: that column's cells are skipped)
+                        constexpr int H = H0, cells = N * H;
                         const int lo = half_lo();
+                        constexpr int K = WG_LBM_CELLS;  // cells per iteration (independent chains)
                         double mfv = 0.0;
                         for (int c0 = t; c0 < cells; c0 += K * NT) {
                             double f[K][9];
                             int o[K];
+                            double w[K];
 #pragma unroll
                             for (int u = 0; u < K; ++u) {
                                 const int c = c0 + u * NT;
                                 const int cc = c < cells ? c : c0;
                                 const int i = cc / H, jj = min(lo + (cc - i * H), N - 1);
                                 o[u] = i * N + jj;
+                                w[u] = ((i == 0 || i == N - 1) ? 0.5 : 1.0) * ((jj == 0 || jj == N - 1) ? 0.5 : 1.0);
 #pragma unroll
                                 for (int k = 0; k < 9; ++k) f[u][k] = P[k][o[u]];
                             }
 #pragma unroll
                             for (int u = 0; u < K; ++u) {
+                                const double rho = lbm_collide(f[u], a.omega);
                                 const int c = c0 + u * NT;
-                                double ux, uy;
-                                const double rho = lbm_moments(f[u], ux, uy);
-                                const double usq = lbm_usq(ux, uy);
-                                const int i = c / H, jl = c - i * H;
-                                if (c < cells && lo + jl < N) {
+                                if (c < cells && lo + (c % H) < N) {
 #pragma unroll
-                                    for (int k = 0; k < 9; ++k)
-                                        if (k == 0 || pop_owner(k) == (int)rank)
-                                            P[k][o[u]] = lbm_relax(k, f[u][k], rho, ux, uy, usq, a.omega);
-                                    mrho[c] = rho;
-                                    mux[c] = ux;
-                                    *uy_at(bufs, mxt, rank, i, jl) = uy;
-                                    const int jj = lo + jl;
-                                    mfv += (((i == 0 || i == N - 1) ? 0.5 : 1.0) * ((jj == 0 || jj == N - 1) ? 0.5 : 1.0)) * rho;
+                                    for (int k = 0; k < 9; ++k) P[k][o[u]] = f[u][k];
+                                    mfv += w[u] * rho;
                                 }
                             }
                         }
                         if (!redo) acc_f[t] += mfv;
                     }
-                    WG_PHASE_MARK(24);
-                    cluster_sync_cta();  // both halves' moments parked
-                    {
-                        double* P[4];  // the own populations
-#pragma unroll
-                        for (int s2 = 0; s2 < 4; ++s2) P[s2] = bufs + (size_t)(1 + s2) * BUFD;
-                        const double* prho = cluster.map_shared_rank(mrho, peer);
-                        const double* pux = cluster.map_shared_rank(mux, peer);
-                        double* const pbufs = cluster.map_shared_rank(bufs, peer);
-                        double* const pxt = cluster.map_shared_rank(mxt, peer);
-                        const int plo = rank == 0 ? H0 : 0, pn = rank == 0 ? N - H0 : H0;  // the peer's half
-                        for (int c0 = t; c0 < cells; c0 += K * NT) {
-                            double m[K][3], f[K][4];
-                            int o[K];
-#pragma unroll
-                            for (int u = 0; u < K; ++u) {
-                                const int c = c0 + u * NT;
-                                const int cc = c < cells ? c : c0;
-                                const int i = cc / H, jl = min(cc - i * H, pn - 1);
-                                o[u] = i * N + plo + jl;
-                                const int pc = i * H + jl;
-                                m[u][0] = prho[pc];
-                                m[u][1] = pux[pc];
-                                m[u][2] = *uy_at(pbufs, pxt, peer, i, jl);
-#pragma unroll
-                                for (int s2 = 0; s2 < 4; ++s2) f[u][s2] = P[s2][o[u]];
-                            }
-#pragma unroll
-                            for (int u = 0; u < K; ++u) {
-                                const int c = c0 + u * NT;
-                                const double usq = lbm_usq(m[u][1], m[u][2]);
-                                if (c < cells && c - (c / H) * H < pn) {
-#pragma unroll
-                                    for (int s2 = 0; s2 < 4; ++s2)
-                                        P[s2][o[u]] = lbm_relax(pair_pop((int)rank, 1 + s2), f[u][s2], m[u][0], m[u][1],
-                                                                m[u][2], usq, a.omega);
-                                }
-                            }
-                        }
-                    }
                 }
-                __syncthreads();  // the own populations relaxed on both halves
+                WG_PHASE_MARK(24);
+                cluster_sync_cta();  // the peer's populations are written back
                 WG_PHASE_MARK(25);
             }
             if (cur_redo || !a.compress) {  // the collided state, to be stored raw
@@ -903,13 +838,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<N>::NT, 1
                 slot_off[0] = mail_off0;
                 slot_ok[0] = mail_ok0;
             }
-            // next patch's inputs into the staging area: both CTAs are past C2
-            // (the peer's reads of the parked moments); the skip rule's
-            // re-derivation prefetches after its raw store instead
-            if (MODE != MODE_INIT && t == CTL && !skip_patch && cur_p + npairs < p_end) {
-                fence_proxy_async();
-                prefetch(cur_p + npairs, (cur_it & 1) ^ 1);
-            }
             __syncthreads();
             if (!skip_patch) {
                 // W: CSR blocks (csr_encode, codec.hpp:37-60) from the parked
@@ -1048,10 +976,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<N>::NT, 1
             if (t == CTL && rank == 1) {
                 slot_off[0] = mail_off0;
                 slot_ok[0] = mail_ok0;
-            }
-            if (MODE != MODE_INIT && t == CTL && cur_p + npairs < p_end) {  // past C2 on both CTAs
-                fence_proxy_async();
-                prefetch(cur_p + npairs, (cur_it & 1) ^ 1);
             }
             __syncthreads();
             double mass = 0.0;
