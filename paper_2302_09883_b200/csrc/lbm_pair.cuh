@@ -197,6 +197,33 @@ __device__ __forceinline__ void store_streamed(double* dst, const double (&v)[N]
     if (cx == -1) dst[(N - 1) * S] = ghost;
 }
 
+// Output position p of the inverse line transform (idwt_line_reg<N, L, L>:
+// every detail +0.0) of a line whose corner-layout positions 0..NS-1 hold
+// the samples srow[] (interleaved positions k 2^L).  Only the chain of
+// predicts that leads to p is evaluated: at each level the interval
+// [a, a + 2h] around p is halved, its midpoint being lift_pred_inv(0, va, vb)
+// exactly as in the full inverse, so the value is bit-identical.
+template <int N, int L>
+__device__ __forceinline__ double idwt_samples_at(const double* srow, int p) {
+    constexpr int S = 1 << L;
+    int a = (p / S) * S;
+    if (a == p) return srow[a / S];
+    double va = srow[a / S], vb = srow[a / S + 1];
+#pragma unroll
+    for (int h = S / 2; h >= 1; h /= 2) {
+        const int mid = a + h;
+        const double vm = lift_pred_inv(0.0, va, vb);
+        if (p == mid) return vm;
+        if (p < mid) {
+            vb = vm;
+        } else {
+            a = mid;
+            va = vm;
+        }
+    }
+    return va;  // not reached: p is a midpoint at some level
+}
+
 template <int N>
 struct PairLayout {
     static constexpr int H0 = (N + 1) / 2;        // rank 0's half of population 0 (columns / rows)
@@ -283,6 +310,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<N>::NT, 1
     __shared__ __align__(8) unsigned long long mbar;
     __shared__ SlotIn slot_in[2][5];
     __shared__ Bits128 rmask[5];               // non-empty coefficient rows per slot
+    // samples-only decode (the common well-compressed block: every stored
+    // coefficient among the NS x NS coarsest samples): the samples per slot,
+    // and per slot whether the block needs the general row decode instead
+    constexpr int NS = ((N - 1) >> L) + 1;
+    constexpr bool kSampFast = L >= 1 && NS <= 5;
+    __shared__ double samp[5][kSampFast ? NS * NS : 1];
+    __shared__ int slot_gen[5];
     __shared__ unsigned long long mail_tot[5];  // peer's per-slot (zeroed << 32 | nnz) totals
     __shared__ unsigned long long mail_off0;    // population 0 block offset (rank 0 -> rank 1)
     __shared__ int mail_ok0;
@@ -450,7 +484,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<N>::NT, 1
     if (t >= CTL && t < CTL + 5) {
         rmask[t - CTL] = Bits128{0ull, 0ull};
         slot_top[t - CTL] = -1;
+        slot_gen[t - CTL] = kSampFast ? 0 : 1;
     }
+    if constexpr (kSampFast)
+        for (int k = t - CTL; k >= 0 && k < 5 * NS * NS; k += 32) (&samp[0][0])[k] = 0.0;
     __syncthreads();
     for (;;) {
         if (cur_p >= p_end) break;
@@ -540,14 +577,35 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<N>::NT, 1
                             store_streamed<N, 1>(rowp, x, (MODE == MODE_DECODE) ? 0 : cy, 0.0);
                         });
                     };
-                    if (jb.on) {  // one call site (instruction cache): own slots one row, population 0 strided
-                        double* Bs = bufs + (size_t)jb.s * BUFD;
-                        const int step = jb.s > 0 ? N : half_n();
-                        for (int r = jb.s > 0 ? jb.li : t - 4 * N; r < N; r += step)
-                            decode_row(Bs, slot_in[par][jb.s], r, jb.cy);
+                    // D1a: the rows of a samples-only block only scatter their
+                    // samples (D2 interpolates them per column); any other stored
+                    // row marks its block for the general row decode (D1b)
+                    auto scan_row = [&](int sl, const SlotIn& d, int r) {
+                        if (d.kind != IN_CSR) return;
+                        const double* vv = redo ? d.gv : d.v;
+                        const uint32_t* cc = redo ? d.gcol : d.col;
+                        const uint32_t* ro = redo ? d.gro : d.ro;
+                        const uint32_t k0 = ro[r], k1 = ro[r + 1];
+                        if (k0 == k1) return;
+                        if (!kSampFast || r >= NS || cc[k1 - 1] >= (uint32_t)NS) {
+                            slot_gen[sl] = 1;
+                            return;
+                        }
+                        for (uint32_t k = k0; k < k1; ++k) samp[sl][r * NS + cc[k]] = vv[k];
+                    };
+                    const int step = jb.s > 0 ? N : half_n();
+                    if (jb.on)  // own slots one row, population 0 strided
+                        for (int r = jb.s > 0 ? jb.li : t - 4 * N; r < N; r += step) scan_row(jb.s, slot_in[par][jb.s], r);
+                    __syncthreads();
+                    if ((slot_gen[0] | slot_gen[1] | slot_gen[2] | slot_gen[3] | slot_gen[4]) != 0) {  // uniform
+                        if (jb.on && slot_gen[jb.s]) {  // D1b: one call site (instruction cache)
+                            double* Bs = bufs + (size_t)jb.s * BUFD;
+                            for (int r = jb.s > 0 ? jb.li : t - 4 * N; r < N; r += step)
+                                decode_row(Bs, slot_in[par][jb.s], r, jb.cy);
+                        }
+                        __syncthreads();
                     }
                 }
-                __syncthreads();
                 WG_PHASE_MARK(21);
                 // next patch's inputs: the staging area is free once D1 has run
                 // (the skip rule's re-derivation reads the global copies)
@@ -592,6 +650,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<N>::NT, 1
                                                            : __longlong_as_double((long long)(((unsigned long long)d.raw_ld << 32) | d.nnz));
 #pragma unroll
                         for (int i = 0; i < N; ++i) v[i] = c;
+                        emit(v);
+                    } else if (kSampFast && !slot_gen[jb.s]) {
+                        // samples-only block: the D1 row values at this column
+                        // straight from the samples (idwt_samples_at), then the
+                        // column inverse — bit-identical to D1 + the masked path
+                        const double* sp = samp[jb.s];
+#pragma unroll
+                        for (int rr = 0; rr < N; ++rr) {
+                            const int cp = corner_pos<N, L>(rr);
+                            v[rr] = cp < NS ? idwt_samples_at<N, L>(sp + cp * NS, jc) : 0.0;
+                        }
+                        idwt_line_reg<N, L, L>(v);
                         emit(v);
                     } else {
                         const Bits128 m = rmask[jb.s];
@@ -1036,7 +1106,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<N>::NT, 1
         if (t >= CTL && t < CTL + 5) {
             rmask[t - CTL] = Bits128{0ull, 0ull};
             slot_top[t - CTL] = -1;
+            slot_gen[t - CTL] = kSampFast ? 0 : 1;
         }
+        if constexpr (kSampFast)
+            for (int k = t - CTL; k >= 0 && k < 5 * NS * NS; k += 32) (&samp[0][0])[k] = 0.0;
         __syncthreads();
     }
     cluster_sync_all();  // no DSMEM access of an exited peer
