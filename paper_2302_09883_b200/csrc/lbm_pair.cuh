@@ -198,30 +198,37 @@ __device__ __forceinline__ void store_streamed(double* dst, const double (&v)[N]
 }
 
 // Output position p of the inverse line transform (idwt_line_reg<N, L, L>:
-// every detail +0.0) of a line whose corner-layout positions 0..NS-1 hold
-// the samples srow[] (interleaved positions k 2^L).  Only the chain of
-// predicts that leads to p is evaluated: at each level the interval
-// [a, a + 2h] around p is halved, its midpoint being lift_pred_inv(0, va, vb)
-// exactly as in the full inverse, so the value is bit-identical.
-template <int N, int L>
-__device__ __forceinline__ double idwt_samples_at(const double* srow, int p) {
+// every detail +0.0) of NS lines whose corner-layout positions 0..NS-1 hold
+// the samples srow[l * NS + k] (interleaved positions k 2^L), all lines at
+// once.  Only the chain of predicts that leads to p is evaluated: at each
+// level the interval [a, a + 2h] around p is halved, its midpoint being
+// lift_pred_inv(0, va, vb) exactly as in the full inverse, so the values are
+// bit-identical.  Branch-free (selects): the lanes of a warp hold different p.
+template <int N, int L, int NS>
+__device__ __forceinline__ void idwt_samples_at(const double* srow, int p, double (&out)[NS]) {
     constexpr int S = 1 << L;
-    int a = (p / S) * S;
-    if (a == p) return srow[a / S];
-    double va = srow[a / S], vb = srow[a / S + 1];
+    const int k = min(p / S, NS - 2);  // the coarse interval [k S, (k + 1) S] holding p
+    int a = k * S;
+    double va[NS], vb[NS];
+#pragma unroll
+    for (int l = 0; l < NS; ++l) {
+        va[l] = srow[l * NS + k];
+        vb[l] = srow[l * NS + k + 1];
+        out[l] = p == a ? va[l] : vb[l];  // p on a sample (the right end: p == (k + 1) S)
+    }
 #pragma unroll
     for (int h = S / 2; h >= 1; h /= 2) {
         const int mid = a + h;
-        const double vm = lift_pred_inv(0.0, va, vb);
-        if (p == mid) return vm;
-        if (p < mid) {
-            vb = vm;
-        } else {
-            a = mid;
-            va = vm;
+        const bool hit = p == mid, right = p > mid;
+#pragma unroll
+        for (int l = 0; l < NS; ++l) {
+            const double vm = lift_pred_inv(0.0, va[l], vb[l]);
+            out[l] = hit ? vm : out[l];
+            va[l] = right ? vm : va[l];
+            vb[l] = right ? vb[l] : vm;
         }
+        a = right ? mid : a;
     }
-    return va;  // not reached: p is a midpoint at some level
 }
 
 template <int N>
@@ -314,7 +321,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<N>::NT, 1
     // coefficient among the NS x NS coarsest samples): the samples per slot,
     // and per slot whether the block needs the general row decode instead
     constexpr int NS = ((N - 1) >> L) + 1;
-    constexpr bool kSampFast = L >= 1 && NS <= 5;
+    constexpr bool kSampFast = L >= 1 && NS >= 2 && NS <= 5;
     __shared__ double samp[5][kSampFast ? NS * NS : 1];
     __shared__ int slot_gen[5];
     __shared__ unsigned long long mail_tot[5];  // peer's per-slot (zeroed << 32 | nnz) totals
@@ -655,11 +662,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<N>::NT, 1
                         // samples-only block: the D1 row values at this column
                         // straight from the samples (idwt_samples_at), then the
                         // column inverse — bit-identical to D1 + the masked path
-                        const double* sp = samp[jb.s];
+                        double yr[NS];
+                        idwt_samples_at<N, L, NS>(samp[jb.s], jc, yr);
 #pragma unroll
                         for (int rr = 0; rr < N; ++rr) {
                             const int cp = corner_pos<N, L>(rr);
-                            v[rr] = cp < NS ? idwt_samples_at<N, L>(sp + cp * NS, jc) : 0.0;
+                            v[rr] = cp < NS ? yr[cp < NS ? cp : 0] : 0.0;
                         }
                         idwt_line_reg<N, L, L>(v);
                         emit(v);
