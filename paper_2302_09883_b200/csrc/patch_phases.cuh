@@ -116,6 +116,12 @@ struct StepArgs {
     const double* raw_in;
     uint32_t p_begin, p_end;
     int chunk_first, chunk_last;
+    // SWE: patches handed out dynamically (work: the launch's patch counter,
+    // reset by the last CTA) and the masses kept per patch ([npatch][2]:
+    // reconstruction, scheme output), summed by the last CTA in patch order
+    // — the step's masses do not depend on which CTA took which patch
+    unsigned* work;
+    double* patch_mass;
 };
 
 // MODE_STEP_LZ: a step that also stages the thresholded coefficient arrays
@@ -692,6 +698,14 @@ __device__ __forceinline__ void finalize_step(const StepArgs& a, const StepParti
         mf += __ldcg(&pp->mass_fv);
         l2 += __ldcg(&pp->l2);
     }
+    if (a.patch_mass) {  // per-patch masses, fixed order (dynamic patch scheduling)
+        m = 0.0;
+        mf = 0.0;
+        for (unsigned p = lane; p < a.g.npatch; p += 32) {
+            m += __ldcg(a.patch_mass + 2 * (size_t)p);
+            mf += __ldcg(a.patch_mass + 2 * (size_t)p + 1);
+        }
+    }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         cb += __shfl_xor_sync(0xffffffffu, cb, o);
@@ -728,6 +742,7 @@ __device__ __forceinline__ void finalize_step(const StepArgs& a, const StepParti
         *mfv_out = mf;
         *a.done = 0;
         *a.bump_next = 0;
+        if (a.work) *a.work = 0;
     }
 }
 

@@ -418,6 +418,8 @@ struct Session {
     unsigned grid = 0;                   // launch grid of the step kernels
     unsigned long long* bump = nullptr;  // [2]
     unsigned* err = nullptr;
+    unsigned* work = nullptr;       // SWE: dynamic patch counter
+    double* patch_mass = nullptr;   // SWE: per-patch masses [npatch][2]
     wg_metrics_row* rows = nullptr;
     double* mass_fv = nullptr;
     uint64_t row_cap = 0;
@@ -491,6 +493,10 @@ struct Session {
         cudaFree(peer_flags);
         peer_flags = nullptr;
         cudaFree(done);
+        cudaFree(work);
+        work = nullptr;
+        cudaFree(patch_mass);
+        patch_mass = nullptr;
         cudaFree(scratch);
         scratch = nullptr;
         cudaFree(bump);
@@ -666,6 +672,9 @@ struct Session {
         if (is_swe()) {
             swe = dalloc<unsigned long long>(5);
             WG_CUDA(cudaMemsetAsync(swe, 0, 5 * sizeof(unsigned long long), stream));
+            work = dalloc<unsigned>(1);
+            WG_CUDA(cudaMemsetAsync(work, 0, sizeof(unsigned), stream));
+            patch_mass = dalloc<double>(2 * (uint64_t)sg.npatch);
         }
         phase = dalloc<unsigned long long>(32);
         WG_CUDA(cudaMemsetAsync(phase, 0, 32 * sizeof(unsigned long long), stream));
@@ -869,6 +878,8 @@ struct Session {
         a.err = err;
         a.partials = partials;
         a.done = done;
+        a.work = work;
+        a.patch_mass = patch_mass;
         a.scratch = scratch;
         a.g = sg;
         a.compress = cfg.no_compression ? 0 : 1;

@@ -97,10 +97,21 @@ __global__ void __launch_bounds__(SweLayout<N>::NT, WG_SWE_MIN_BLOCKS) k_swe_ste
     const double r = clk.dt / a.dx;  // solver.hpp:212
 
     StepPartial part{0, 0, 0, 0.0, 0.0, 0.0};
-    double macc = 0.0, mfacc = 0.0, vmax = 0.0;
-    if (t == 0) cs.cur = cs.end = 0;
+    double vmax = 0.0;
+    // patches are handed out dynamically (the dam break's patches differ in
+    // cost by far: flat constant blocks against the front's Riemann solves),
+    // the next index fetched while the current patch is decoded
+    __shared__ uint32_t p_next;
+    __shared__ double red_m[NT / 32], red_f[NT / 32];
+    if (t == 0) {
+        cs.cur = cs.end = 0;
+        p_next = atomicAdd(a.work, 1u);
+    }
+    __syncthreads();
     WG_PHASE_MARK(-1);
-    for (uint32_t p = blockIdx.x; p < g.npatch; p += gridDim.x) {
+    for (;;) {
+        const uint32_t p = p_next;
+        if (p >= g.npatch) break;  // uniform
         const PatchPos pp = patch_pos(p, g);
         // ---- decode h, hu, hv + ghost ring --------------------------------
         bool raw_in = false;
@@ -108,7 +119,8 @@ __global__ void __launch_bounds__(SweLayout<N>::NT, WG_SWE_MIN_BLOCKS) k_swe_ste
             raw_in = decode_row<N, L>(T, li, a.dir_in[(size_t)p * 3 + s], a.store_in);
             fill_ghosts<N>(T, li, a.ein, pp, s, g);
         }
-        __syncthreads();
+        __syncthreads();  // every thread has read p
+        if (t == 0) p_next = atomicAdd(a.work, 1u);
         WG_PHASE_MARK(0);
         if (lane_ok && !raw_in) {
             double v[N];
@@ -148,7 +160,6 @@ __global__ void __launch_bounds__(SweLayout<N>::NT, WG_SWE_MIN_BLOCKS) k_swe_ste
             const double wgt = ((i == 0 || i == N - 1) ? 0.5 : 1.0) * ((j == 0 || j == N - 1) ? 0.5 : 1.0);
             mfv += wgt * out[0];  // global_mass(grid, 0): h only (pipeline.hpp:274)
         }
-        mfacc += mfv;
         __syncthreads();
         WG_PHASE_MARK(2);
 
@@ -286,10 +297,27 @@ __global__ void __launch_bounds__(SweLayout<N>::NT, WG_SWE_MIN_BLOCKS) k_swe_ste
             __syncthreads();
             WG_PHASE_MARK(9);
         }
-        macc += m;
+        // the patch's masses (fixed order: warp trees, then warps in order)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            m += __shfl_xor_sync(0xffffffffu, m, o);
+            mfv += __shfl_xor_sync(0xffffffffu, mfv, o);
+        }
+        if ((t & 31) == 0) {
+            red_m[t >> 5] = m;
+            red_f[t >> 5] = mfv;
+        }
+        __syncthreads();
+        if (t == 0) {
+            double sm = 0.0, sf = 0.0;
+            for (int w = 0; w < NT / 32; ++w) {
+                sm += red_m[w];
+                sf += red_f[w];
+            }
+            a.patch_mass[2 * (size_t)p] = sm;
+            a.patch_mass[2 * (size_t)p + 1] = sf;
+        }
     }
-    part.mass = macc;
-    part.mass_fv = mfacc;
     if (t != 0) part.comp_bytes = part.nnz = part.zeroed = 0;
     const StepPartial tot = cta_reduce_partial<NT>(part);
     // CTA max of the wave speed (exact: order-independent)
