@@ -104,7 +104,8 @@ def cpu_model() -> str:
 
 def run_config(w: dict, steps: int) -> api.RunConfig:
     cfg = api.RunConfig(scheme=w["scheme"], nx=w["nx"], splits=tuple(w["splits"]), levels=w["levels"],
-                        spec=api.ThresholdSpec(w["mode"], w["c"]), compute_l2=False, lbm_steps=steps)
+                        spec=api.ThresholdSpec(w["mode"], w["c"]), lbm_steps=steps,
+                        compute_l2=w["scheme"] == "transport")  # run() computes l2 every step (pipeline.hpp:275-276)
     if w["scheme"] == "transport":
         cfg.t_end = steps * cfg.cfl * (1.0 / (w["nx"] - 1)) / max(cfg.alpha, cfg.beta)
     elif w["scheme"] == "swe":
@@ -441,8 +442,9 @@ def bench_b200(args, w: dict):
         "compute_ceiling": compute_ceiling(lib, w, value / world),  # per GPU
         # one fused kernel launch per step; Codec::lz adds the LZ-size pass
         # (k_lz_sizes, which also writes the step's row); the peer halo mode
-        # adds its device-side wait and signal
-        "gpu_launches": args.steps * ((2 if w.get("codec") == "lz" else 1) + (2 if sess.peer else 0)),
+        # adds its device-side wait and signal; transport adds the l2 pass
+        "gpu_launches": args.steps * ((2 if w.get("codec") == "lz" else 1) + (2 if sess.peer else 0)
+                                      + (1 if cfg.compute_l2 and w["scheme"] == "transport" else 0)),
         "clocks": clocks.summary(),
         "device_bytes": info.device_bytes,
         "device_mem_used_bytes": mem_used,

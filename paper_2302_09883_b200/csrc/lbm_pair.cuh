@@ -234,22 +234,34 @@ __device__ __forceinline__ void idwt_samples_at(const double* srow, int p, doubl
 template <int N>
 struct PairLayout {
     static constexpr int H0 = (N + 1) / 2;        // rank 0's half of population 0 (columns / rows)
-    static constexpr int JOBS = 4 * N + H0;       // line jobs of rank 0 (rank 1: one fewer)
+    // population 0's line jobs start at a warp boundary (P0): with BUFD below,
+    // no warp's line accesses conflict in shared-memory banks
+    static constexpr int P0 = ((4 * N + 31) / 32) * 32;
+    static constexpr int JOBS = P0 + H0;          // line jobs of rank 0 (rank 1: one fewer)
     // the line jobs' warps + one control warp (prefetch, allocation, mailbox,
     // the serial column-edge inverses) — free in registers: 9-12 warps all
     // get 168 registers per thread (3 warps per SM sub-partition)
     static constexpr int NT = ((JOBS + 31) / 32) * 32 + 32;
     static constexpr int CTL = NT - 32;  // first thread of the control warp
     static constexpr int NN = N * N;
-    static constexpr int BUFD = (NN + 1) & ~1;    // doubles per population buffer (16-byte multiple)
+    // doubles per population buffer: N^2 = 1 (mod 16) for N = 2^k + 1, so a
+    // warp whose lanes straddle two buffers (the last columns / rows of one
+    // population, the first of the next) spreads over the banks without a
+    // conflict (2 BUFD = 2 (mod 32) words: the next buffer's lanes start
+    // exactly where the previous one's end, modulo the 32 banks)
+    static constexpr int BUFD = NN;
+    static_assert(NN % 16 == 1, "bank-conflict-free buffer stride");
     static constexpr int NBUF = 5;                // slot 0: population 0 replica, slots 1..4: own populations
     static constexpr size_t kSmemMax = 232448;    // 227 KB per CTA (sm_100)
     static constexpr size_t kStatic = 8192;       // static shared memory of the kernel (bound, checked at load)
     // + the scan array, the column-edge partials of the 4 own populations and
     // the per-thread mass accumulators
+    // (+ one pad double so that the staging area after them is 16-byte
+    // aligned: the bulk copies land there)
+    static constexpr int PAD = (NBUF * BUFD + 3 * NT + 4 * N) & 1;
     static constexpr size_t fixed_bytes() {
         return sizeof(double) * (size_t)NBUF * BUFD + 8ull * NT + sizeof(double) * 4 * (size_t)N +
-               sizeof(double) * 2 * (size_t)NT;
+               sizeof(double) * 2 * (size_t)NT + sizeof(double) * PAD;
     }
     static constexpr size_t stage_bytes() {
         const size_t room = kSmemMax - kStatic - fixed_bytes();
@@ -312,7 +324,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<N>::NT, 1
     double* side = reinterpret_cast<double*>(inc + NT);  // [4][N] column-edge partials Y[r][1 or N-2]
     double* acc_m = side + 4 * N;                // per-thread mass of the reconstruction
     double* acc_f = acc_m + NT;                  // per-thread mass of the collided state
-    unsigned char* stage = reinterpret_cast<unsigned char*>(acc_f + NT);
+    unsigned char* stage = reinterpret_cast<unsigned char*>(acc_f + NT + Lay::PAD);
 
     __shared__ __align__(8) unsigned long long mbar;
     __shared__ SlotIn slot_in[2][5];
@@ -361,8 +373,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<N>::NT, 1
             jb.s = 1 + t / N;
             jb.li = t - (jb.s - 1) * N;
             jb.on = true;
-        } else if (t < 4 * N + H) {
-            jb.li = lo + (t - 4 * N);
+        } else if (t >= Lay::P0 && t < Lay::P0 + H) {
+            jb.li = lo + (t - Lay::P0);
             jb.on = true;
         }
         jb.q = pair_pop((int)rank, jb.s);
@@ -370,7 +382,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<N>::NT, 1
         jb.cy = lbm_cy(jb.q);
         return jb;
     };
-    auto jb_on_d2 = [&]() { return t < 4 * N + (cluster_rank() == 0 ? H0 : N - H0); };
+    auto jb_on_d2 = [&]() { return t < 4 * N || (t >= Lay::P0 && t < Lay::P0 + (cluster_rank() == 0 ? H0 : N - H0)); };
     auto half_lo = [&]() { return cluster_rank() == 0 ? 0 : H0; };
     auto half_n = [&]() { return cluster_rank() == 0 ? H0 : N - H0; };
     auto peer_of = [&]() { return cluster_rank() ^ 1u; };
@@ -602,12 +614,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<N>::NT, 1
                     };
                     const int step = jb.s > 0 ? N : half_n();
                     if (jb.on)  // own slots one row, population 0 strided
-                        for (int r = jb.s > 0 ? jb.li : t - 4 * N; r < N; r += step) scan_row(jb.s, slot_in[par][jb.s], r);
+                        for (int r = jb.s > 0 ? jb.li : t - Lay::P0; r < N; r += step) scan_row(jb.s, slot_in[par][jb.s], r);
                     __syncthreads();
                     if ((slot_gen[0] | slot_gen[1] | slot_gen[2] | slot_gen[3] | slot_gen[4]) != 0) {  // uniform
                         if (jb.on && slot_gen[jb.s]) {  // D1b: one call site (instruction cache)
                             double* Bs = bufs + (size_t)jb.s * BUFD;
-                            for (int r = jb.s > 0 ? jb.li : t - 4 * N; r < N; r += step)
+                            for (int r = jb.s > 0 ? jb.li : t - Lay::P0; r < N; r += step)
                                 decode_row(Bs, slot_in[par][jb.s], r, jb.cy);
                         }
                         __syncthreads();
@@ -857,7 +869,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<N>::NT, 1
             cta_inclusive_scan<NT>(cnt, inc);
             if (t >= CTL && t < CTL + 5) {
                 const int u = t - CTL;
-                const int first = u == 0 ? 4 * N : (u - 1) * N;
+                const int first = u == 0 ? Lay::P0 : (u - 1) * N;
                 const int n = u == 0 ? half_n() : N;
                 const unsigned long long before = first == 0 ? 0ull : inc[first - 1];
                 slot_tot[u] = inc[first + n - 1] - before;
@@ -930,7 +942,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<N>::NT, 1
                 uint32_t k = 0;
                 if (jb.on) {
                     const int s = jb.s;
-                    const int first = s == 0 ? 4 * N : (s - 1) * N;
+                    const int first = s == 0 ? Lay::P0 : (s - 1) * N;
                     const unsigned long long before = first == 0 ? 0ull : inc[first - 1];
                     k = (uint32_t)((inc[t] - before) & 0xffffffffull) - nz + slot_k0[s];
                     if (slot_ok[s]) {  // row offsets: u32 from 0 (csr_encode)

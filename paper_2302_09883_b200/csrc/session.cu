@@ -679,6 +679,10 @@ struct Session {
         phase = dalloc<unsigned long long>(32);
         WG_CUDA(cudaMemsetAsync(phase, 0, 32 * sizeof(unsigned long long), stream));
         grow_rows(1024);
+        // D2Q9: the row-chunk staging of the streamed first step and the
+        // chunked download, allocated up front (<= 1 GB) so that no allocation
+        // happens between a session's steps and its readback
+        if (ks.cluster > 1) ensure_row_stage();
         if (cfg.codec == 2 && !cfg.no_compression) {  // Codec::lz metrics (the store itself stays CSR)
             if (!ks.main_lz) raise(WG_INVALID_ARGUMENT, "Codec::lz metrics: not available for this kernel variant");
             const uint64_t nb = (uint64_t)sg.npatch * sg.m;
