@@ -74,6 +74,25 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned pari
         "r"(parity)
         : "memory");
 }
+// arrive (release, cluster scope) on the barrier at the offset of `bar` in
+// CTA `peer`'s shared memory: the arriving thread's earlier stores (DSMEM
+// included) happen before the waiter's acquire
+__device__ __forceinline__ void mbar_arrive_remote(unsigned long long* bar, unsigned peer) {
+    uint32_t b;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(b) : "r"(smem_u32(bar)), "r"(peer));
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(b) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_acq_cluster(unsigned long long* bar, unsigned parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WG_MBAR_WAITC_%=:\n"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WG_MBAR_WAITC_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
 // global -> this CTA's shared memory, completion counted on bar (bytes and
 // both addresses 16-byte aligned)
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
@@ -327,6 +346,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<N>::NT, 1
     unsigned char* stage = reinterpret_cast<unsigned char*>(acc_f + NT + Lay::PAD);
 
     __shared__ __align__(8) unsigned long long mbar;
+    __shared__ __align__(8) unsigned long long mbm;  // rank 1: population 0's block offset delivered
+    __shared__ __align__(16) DirEntry dnext[5];  // the next patch's directory entries (dir_ahead)
     __shared__ SlotIn slot_in[2][5];
     __shared__ Bits128 rmask[5];               // non-empty coefficient rows per slot
     // samples-only decode (the common well-compressed block: every stored
@@ -388,12 +409,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<N>::NT, 1
     auto peer_of = [&]() { return cluster_rank() ^ 1u; };
 
     // ---- input prefetch of patch p into descriptor set `par` (thread 0) ----
-    auto prefetch = [&](uint32_t p, int par) {
+    // (`early`: the patch's directory entries were copied into dnext by
+    // dir_ahead at the start of the current patch, so no global-load latency
+    // lands on the control thread here)
+    auto prefetch = [&](uint32_t p, int par, bool early = false) {
         const int rank = (int)cluster_rank();
         DirEntry e[5];
+        if (early) cp_async_wait_all();
 #pragma unroll
         for (int sl = 0; sl < 5; ++sl)  // independent loads in flight together
-            e[sl] = (MODE != MODE_INIT && !a.raw_in) ? a.dir_in[(size_t)p * 9 + pair_pop(rank, sl)]
+            e[sl] = (MODE != MODE_INIT && !a.raw_in) ? (early ? dnext[sl] : a.dir_in[(size_t)p * 9 + pair_pop(rank, sl)])
                                                       : DirEntry{0, 0u, DIR_DEAD};
         unsigned used = 0;
         unsigned char* src[5];
@@ -446,6 +471,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<N>::NT, 1
             if (nb[sl]) bulk_g2s(const_cast<double*>(slot_in[par][sl].v), src[sl], nb[sl], &mbar);
     };
 
+    // The next patch's directory entries into dnext by cp.async (control
+    // thread, at the start of a patch): consumed by prefetch(.., early) after D1.
+    auto dir_ahead = [&](uint32_t p) {
+        const int rank = (int)cluster_rank();
+#pragma unroll
+        for (int sl = 0; sl < 5; ++sl) {
+            const DirEntry* src = a.dir_in + (size_t)p * 9 + pair_pop(rank, sl);
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(smem_u32(&dnext[sl])), "l"(src) : "memory");
+        }
+    };
+
     // The ghost values of the own populations of patch p (sync_ghosts,
     // patchgrid.hpp:131-201), gathered by all threads from the neighbours'
     // edge lines (the previous step's output): per output column j of D2 the
@@ -479,6 +515,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<N>::NT, 1
     for (int k = t; k < N; k += NT) ilv[k] = (uint8_t)interleaved_of<N, L>(k);
     if (t == CTL) {
         mbar_init(&mbar, 1);
+        mbar_init(&mbm, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         cs.cur = cs.end = 0;
         part = a.chunk_first ? StepPartial{0, 0, 0, 0.0, 0.0, 0.0} : a.partials[blockIdx.x];
@@ -492,7 +529,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<N>::NT, 1
     __syncthreads();
     WG_PHASE_MARK(-1);
 
-    unsigned phase = 0;
+    unsigned phase = 0, mbm_phase = 0;
     if (t == CTL) {
         cur_p = a.p_begin + pair;
         cur_it = 0;
@@ -516,6 +553,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<N>::NT, 1
         WG_PHASE_MARK(12);
         mbar_wait(&mbar, phase);
         phase ^= 1u;
+        if (MODE != MODE_INIT && t == CTL && !a.raw_in && cur_p + npairs < p_end) dir_ahead(cur_p + npairs);
         WG_PHASE_MARK(13);
         acc_m[t] = 0.0;
         acc_f[t] = 0.0;
@@ -630,7 +668,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<N>::NT, 1
                 // (the skip rule's re-derivation reads the global copies)
                 if (t == CTL && !cur_redo && cur_p + npairs < p_end) {
                     fence_proxy_async();
-                    prefetch(cur_p + npairs, par ^ 1);
+                    prefetch(cur_p + npairs, par ^ 1, !a.raw_in);
                 }
                 // D2: decode columns, ghosts, pull streaming along dim 0 (a
                 // register shift), or the MODE_DECODE output.  Thread j owns
@@ -916,15 +954,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<N>::NT, 1
                     if (rank == 0) {
                         *cluster.map_shared_rank(&mail_off0, peer_of()) = slot_off[0];
                         *cluster.map_shared_rank(&mail_ok0, peer_of()) = slot_ok[0];
+                        mbar_arrive_remote(&mbm, peer_of());  // release: the two stores above first
                     } else {  // population 0: rank 0's rows come first in the block
                         slot_nnz[0] = (uint32_t)(slot_tot[0] & 0xffffffffull) + (uint32_t)(mail_tot[0] & 0xffffffffull);
                         slot_k0[0] = (uint32_t)(mail_tot[0] & 0xffffffffull);
                     }
                 }
             }
-            cluster_sync_cta();  // M2: population 0's block offset delivered
+            // M2: population 0's block offset, rank 0 -> rank 1 point to point
+            // (a remote mbarrier arrival, no cluster barrier: rank 0 moves on)
             WG_PHASE_MARK(29);
             if (t == CTL && cluster_rank() == 1 && !skip_patch) {
+                mbar_wait_acq_cluster(&mbm, mbm_phase);
+                mbm_phase ^= 1u;
                 slot_off[0] = mail_off0;
                 slot_ok[0] = mail_ok0;
             }
