@@ -530,6 +530,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<N>::NT, 1
     WG_PHASE_MARK(-1);
 
     unsigned phase = 0, mbm_phase = 0;
+    double tot_m = 0.0, tot_f = 0.0;  // this thread's mass contributions (reconstruction, scheme output)
     if (t == CTL) {
         cur_p = a.p_begin + pair;
         cur_it = 0;
@@ -1132,29 +1133,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<N>::NT, 1
             }
         }
         cp_async_wait_all();  // the next patch's ghosts (issued after D2)
-        // per-patch sums (fixed association: warps in order)
+        // per-thread mass sums over this CTA's patches (a static sequence:
+        // reduced once at the end, in a fixed order)
         if (MODE != MODE_DECODE) {
-            __syncthreads();
-            double mm = acc_m[t], mf = acc_f[t];
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                mm += __shfl_xor_sync(0xffffffffu, mm, o);
-                mf += __shfl_xor_sync(0xffffffffu, mf, o);
-            }
-            if ((t & 31) == 0) {
-                red_m[t >> 5] = mm;
-                red_f[t >> 5] = mf;
-            }
-            __syncthreads();
-            if (t == CTL) {
-                double sm = 0.0, sf = 0.0;
-                for (int w = 0; w < NT / 32; ++w) {
-                    sm += red_m[w];
-                    sf += red_f[w];
-                }
-                part.mass += sm;
-                part.mass_fv += sf;
-            }
+            tot_m += acc_m[t];
+            tot_f += acc_f[t];
         }
         __syncthreads();  // buffers and descriptors free for the next patch
         WG_PHASE_MARK(31);
@@ -1177,6 +1160,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<N>::NT, 1
     cluster_sync_all();  // no DSMEM access of an exited peer
     if (MODE == MODE_DECODE) return;
     __syncthreads();
+    {  // the CTA's mass sums (fixed association: lanes, then warps in order)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            tot_m += __shfl_xor_sync(0xffffffffu, tot_m, o);
+            tot_f += __shfl_xor_sync(0xffffffffu, tot_f, o);
+        }
+        if ((t & 31) == 0) {
+            red_m[t >> 5] = tot_m;
+            red_f[t >> 5] = tot_f;
+        }
+        __syncthreads();
+        if (t == CTL) {
+            double sm = 0.0, sf = 0.0;
+            for (int w = 0; w < NT / 32; ++w) {
+                sm += red_m[w];
+                sf += red_f[w];
+            }
+            part.mass += sm;
+            part.mass_fv += sf;
+        }
+        __syncthreads();
+    }
     finalize_step(a, part);
 }
 
