@@ -62,6 +62,12 @@ WORKLOADS = {
     # initial state is generated and compressed on the device instead.
     "lbm_c4": dict(scheme="lbm", components=9, nx=16385, splits=(256, 256), levels=4, c=1e-3, mode="capped",
                    budget=8 << 30, streamed=True, scaling="strong"),
+    # C4 / C2 at threshold 1e-5 (SURVEY §8d's sweep end): detail coefficients
+    # survive (ratio ~52), the general decode path runs
+    "lbm_c4_t1e5": dict(scheme="lbm", components=9, nx=16385, splits=(256, 256), levels=4, c=1e-5, mode="capped",
+                        budget=8 << 30, streamed=True, scaling="strong"),
+    "lbm_c2_t1e5": dict(scheme="lbm", components=9, nx=1025, splits=(16, 16), levels=4, c=1e-5, mode="capped",
+                        scaling="weak"),
     # C4 with the device-generated initial state (the N > 1 path on one GPU)
     "lbm_c4_devinit": dict(scheme="lbm", components=9, nx=16385, splits=(256, 256), levels=4, c=1e-3,
                            mode="capped", budget=8 << 30, device_init=True, scaling="strong"),

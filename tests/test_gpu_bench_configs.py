@@ -137,3 +137,13 @@ def test_step_host_equals_upload(product):
     b, rb = go(False)
     assert ra == rb and len(ra) == 5
     assert np.array_equal(bits(a), bits(b))
+
+
+@pytest.mark.parametrize("c", [1e-12, 1e-7])
+def test_c2_grid_tiny_threshold(product, oracle, c):
+    """The C2 grid at thresholds that zero almost nothing: every patch's
+    blocks are nearly dense CSR (up to 1.5x the raw block), or raw by the
+    skip rule — the default store pools (sized for the dense-CSR worst case)
+    never overflow, and the run equals the reference's bit for bit."""
+    cfg = lbm_cfg(C2["nx"], C2["splits"], C2["levels"], c, 3)
+    compare_runs(api.run(cfg, lib=product), api.run(cfg, lib=oracle))

@@ -294,3 +294,32 @@ def test_peer_halos_c5_geometry(product):
         single.close()
         for s in multi:
             s.close()
+
+
+def test_shards_transport_l2_sums(product):
+    """compute_l2 on (run()'s default): every shard reports its share of the
+    l2_error sum of the global grid (l2_scale per shard, solver.hpp:302-304);
+    the shares add up to the one-shard value (distributed.reduce_rows sums
+    them across ranks)."""
+    cfg = _cfg("transport", 257, (8, 8), 4, 1e-3)
+    cfg.compute_l2 = True
+    g0 = api.initial_state(cfg, lib=product)
+    single = LocalShards(product, cfg, 1)
+    multi = LocalShards(product, cfg, 3)
+    try:
+        single.upload(g0)
+        multi.upload(g0)
+        dt = cfg.cfl / (cfg.nx - 1) / 0.9
+        for _ in range(4):
+            for sh in (single, multi):
+                for s in sh.sessions:
+                    product.check(product.wg_session_step(s.handle, dt))
+                sh.exchange()
+        r1, rn = single.rows()[0], multi.rows()
+        for k in range(4):
+            total = sum(p[k]["l2"] for p in rn)
+            assert r1[k]["l2"] > 0.0
+            assert abs(total - r1[k]["l2"]) <= 1e-12 * r1[k]["l2"], (k, total, r1[k]["l2"])
+    finally:
+        single.close()
+        multi.close()
