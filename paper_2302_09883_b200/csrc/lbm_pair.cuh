@@ -368,10 +368,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<N>::NT, 1
     __shared__ int slot_top[5];                 // highest row holding a kept coefficient (-1: none)
     __shared__ ChunkState cs;
     __shared__ int skip_patch;
-    __shared__ PatchPos ppos;
     __shared__ StepPartial part;                // this CTA's step sums (thread 0)
+    __shared__ PatchPos ppos;
     __shared__ uint32_t cur_p;                  // the patch in flight (state lives in shared
-    __shared__ int cur_it, cur_redo, cur_raw;   // memory: short register live ranges)
+    __shared__ int cur_it, cur_redo;            // memory: short register live ranges)
     __shared__ double red_m[NT / 32], red_f[NT / 32];
     __shared__ double gh_row[4][N];             // ghost value streamed in along dim 0, per output column
     __shared__ double gh_col[4][N];             // ghost column streamed in along dim 1
@@ -536,7 +536,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<N>::NT, 1
         cur_it = 0;
         ppos = patch_pos(cur_p, g);
         cur_redo = 0;
-        cur_raw = 0;
     }
     if (t >= CTL && t < CTL + 5) {
         rmask[t - CTL] = Bits128{0ull, 0ull};
@@ -558,6 +557,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<N>::NT, 1
         WG_PHASE_MARK(13);
         acc_m[t] = 0.0;
         acc_f[t] = 0.0;
+        bool raw_now = false;  // this patch is stored raw (skip rule / no compression): uniform
         const int par = cur_it & 1;
         // produce the post-collide state (D1, D2, C); pass 1 re-derives the
         // state of a skip-rule patch after the transform overwrote it
@@ -799,8 +799,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<N>::NT, 1
                 cluster_sync_cta();  // the peer's populations are written back
                 WG_PHASE_MARK(25);
             }
-            if (cur_redo || !a.compress) {  // the collided state, to be stored raw
-                if (t == CTL) cur_raw = 1;
+            if (cur_redo || !a.compress) {  // the collided state, to be stored raw (uniform)
+                raw_now = true;
                 break;
             }
 
@@ -905,7 +905,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<N>::NT, 1
             }
             WG_PHASE_MARK(27);
             // S: CTA scan of the counts in job order, per-slot totals, mailbox
-            cta_inclusive_scan<NT>(cnt, inc);
+            cta_inclusive_scan<NT>(cnt, inc, true);  // the previous patch's scan is barriers behind
             if (t >= CTL && t < CTL + 5) {
                 const int u = t - CTL;
                 const int first = u == 0 ? Lay::P0 : (u - 1) * N;
@@ -1087,8 +1087,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<N>::NT, 1
             if (t == CTL) cur_redo = 1;  // skip rule: the buffers hold the transform, re-derive the state
             __syncthreads();
         }
-        __syncthreads();  // cur_raw visible to every thread
-        if (MODE != MODE_DECODE && cur_raw) {
+        if (MODE != MODE_DECODE && raw_now) {
             // skip rule / no compression: the collided state itself, stored raw
             const unsigned rank = cluster_rank();
             if (t == CTL) {
@@ -1105,11 +1104,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<N>::NT, 1
                     *cluster.map_shared_rank(&mail_ok0, peer_of()) = slot_ok[0];
                 }
             }
-            cluster_sync_all();
+            cluster_sync_all();  // (also: every thread has read cur_redo of this patch)
             if (t == CTL && rank == 1) {
                 slot_off[0] = mail_off0;
                 slot_ok[0] = mail_ok0;
             }
+            if (t == CTL) cur_redo = 0;  // read again only after the next patch's barriers
             __syncthreads();
             double mass = 0.0;
             const int lo = half_lo(), H = half_n();
@@ -1145,8 +1145,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<N>::NT, 1
             cur_p += npairs;
             ++cur_it;
             ppos = patch_pos(cur_p, g);
-            cur_redo = 0;
-            cur_raw = 0;
         }
         if (t >= CTL && t < CTL + 5) {
             rmask[t - CTL] = Bits128{0ull, 0ull};

@@ -496,7 +496,8 @@ __device__ __forceinline__ double col_mass(int j, const double (&v)[N]) {
 // Inclusive scan of one u64 per thread over the CTA (warp shuffles + one
 // shared pass); result written to inc[threadIdx.x].  Contains barriers.
 template <int NT>
-__device__ __forceinline__ void cta_inclusive_scan(unsigned long long x, unsigned long long* inc) {
+__device__ __forceinline__ void cta_inclusive_scan(unsigned long long x, unsigned long long* inc,
+                                                   bool after_barrier = false) {
     __shared__ unsigned long long wtot[NT / 32];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
 #pragma unroll
@@ -504,7 +505,9 @@ __device__ __forceinline__ void cta_inclusive_scan(unsigned long long x, unsigne
         const unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
         if (lane >= o) x += y;
     }
-    __syncthreads();  // wtot may still be read by a previous scan
+    // wtot may still be read by a previous scan (after_barrier: the caller
+    // knows a CTA barrier separates the two)
+    if (!after_barrier) __syncthreads();
     if (lane == 31) wtot[w] = x;
     __syncthreads();
     unsigned long long before = 0;
