@@ -110,6 +110,22 @@ wg_status wg_csr_decode(const double* v, const uint32_t* col, uint64_t nnz,
                         const uint32_t* row, uint64_t row_len, uint32_t rows,
                         uint32_t cols, double* dense);
 
+/* ---- Codec::lz (codec.hpp:81-244) --------------------------------------
+ * lz_encode(data[n], chunk) (codec.hpp:223-235): chunk k covers bytes
+ * [k chunk, min((k + 1) chunk, n)); its lz_encode_chunk payload
+ * (codec.hpp:127-175) is written at out + the sum of the previous payload
+ * lengths, its length to enc_len[k] (room for ceil(n / chunk) entries);
+ * *out_len = the total.  out == NULL: lengths only.  chunk == 0:
+ * WG_INVALID_ARGUMENT (as lz_encode); cap < total: WG_OUT_OF_RANGE. */
+wg_status wg_lz_encode(const uint8_t* data, uint64_t n, uint64_t chunk, uint8_t* out,
+                       uint64_t cap, uint64_t* enc_len, uint64_t* out_len);
+/* lz_decode (codec.hpp:237-244): chunk k's payload (enc_len[k] bytes, the
+ * chunks back to back in payload) decoded to its raw length
+ * min(chunk, n - k chunk) into out[n]; lz_decode_chunk's checks
+ * (codec.hpp:177-220) -> WG_CORRUPT_STREAM. */
+wg_status wg_lz_decode(const uint8_t* payload, const uint64_t* enc_len, uint64_t chunk,
+                       uint8_t* out, uint64_t n);
+
 /* ---- patch grid (patchgrid.hpp) ----------------------------------------- */
 
 typedef struct wg_grid_desc { /* PatchGrid, patchgrid.hpp:38-55 */

@@ -14,12 +14,14 @@
 //   dwt_nd          wavelet.hpp:175-198     idwt_nd        wavelet.hpp:200-223
 //   apply_threshold threshold.hpp:51-86     band_threshold threshold.hpp:31-47
 //   csr_encode      codec.hpp:37-60         csr_decode     codec.hpp:62-79
+//   lz_encode       codec.hpp:223-235       lz_decode      codec.hpp:237-244
 //   sync_ghosts     patchgrid.hpp:131-201   global_mass    patchgrid.hpp:244-266
 //   fv_step (every patch of a grid)         solver.hpp:207-231
 //   run             pipeline.hpp:129-305    (+ Session: the device-resident loop)
 #pragma once
 
 #include <cstdint>
+#include <algorithm>
 #include <cstdio>
 #include <cstring>
 #include <exception>
@@ -114,6 +116,44 @@ inline std::vector<double> csr_decode(const CsrBlock& b) {
     check(wg_csr_decode(b.v.data(), b.col.data(), b.v.size(), b.row.data(), b.row.size(), b.rows, b.cols,
                         dense.data()));
     return dense;
+}
+
+// lz_encode / lz_decode (codec.hpp:223-244) through wg_lz_encode /
+// wg_lz_decode: same LzStream, same bytes, same exceptions.
+inline LzStream lz_encode(std::span<const std::uint8_t> data, std::size_t chunk_size) {
+    const uint64_t n = data.size();
+    const uint64_t nc = chunk_size ? (n + chunk_size - 1) / chunk_size : 0;
+    std::vector<uint64_t> lens(nc ? nc : 1);
+    uint64_t tot = 0;
+    check(wg_lz_encode(data.data(), n, chunk_size, nullptr, 0, lens.data(), &tot));
+    std::vector<std::uint8_t> bytes(tot ? tot : 1);
+    check(wg_lz_encode(data.data(), n, chunk_size, bytes.data(), tot, lens.data(), &tot));
+    LzStream s;
+    s.chunk_size = chunk_size;
+    uint64_t at = 0;
+    for (uint64_t k = 0; k < nc; ++k) {
+        LzChunk c;
+        c.raw_len = static_cast<std::uint32_t>(std::min<uint64_t>(chunk_size, n - k * chunk_size));
+        c.payload.assign(bytes.begin() + (std::ptrdiff_t)at, bytes.begin() + (std::ptrdiff_t)(at + lens[k]));
+        at += lens[k];
+        s.chunks.push_back(std::move(c));
+    }
+    return s;
+}
+
+inline std::vector<std::uint8_t> lz_decode(const LzStream& s) {
+    std::vector<std::uint8_t> out;
+    for (const LzChunk& c : s.chunks) {  // every chunk with its own raw length
+        if (c.raw_len == 0) {
+            if (!c.payload.empty()) throw corrupt_stream_error("lz_decode: trailing bytes");
+            continue;
+        }
+        std::vector<std::uint8_t> d(c.raw_len);
+        const uint64_t len = c.payload.size();
+        check(wg_lz_decode(c.payload.data(), &len, c.raw_len, d.data(), c.raw_len));
+        out.insert(out.end(), d.begin(), d.end());
+    }
+    return out;
 }
 
 // ---- patch grids: PatchGrid <-> the ABI's flat grid buffer ------------------

@@ -566,6 +566,43 @@ wg_status wg_run_initial_state(const wg_run_config* c, double* out) {
     });
 }
 
+// lz_encode / lz_decode of the reference (codec.hpp:223-244)
+wg_status wg_lz_encode(const uint8_t* data, uint64_t n, uint64_t chunk, uint8_t* out, uint64_t cap,
+                       uint64_t* enc_len, uint64_t* out_len) {
+    return guard([&] {
+        const LzStream st = lz_encode(std::span<const std::uint8_t>(data, n), chunk);
+        uint64_t tot = 0;
+        for (std::size_t k = 0; k < st.chunks.size(); ++k) {
+            if (enc_len) enc_len[k] = st.chunks[k].payload.size();
+            if (out) {
+                if (tot + st.chunks[k].payload.size() > cap) throw std::out_of_range("lz_encode: output buffer too small");
+                std::memcpy(out + tot, st.chunks[k].payload.data(), st.chunks[k].payload.size());
+            }
+            tot += st.chunks[k].payload.size();
+        }
+        if (out_len) *out_len = tot;
+    });
+}
+
+wg_status wg_lz_decode(const uint8_t* payload, const uint64_t* enc_len, uint64_t chunk, uint8_t* out, uint64_t n) {
+    return guard([&] {
+        if (chunk == 0) throw std::invalid_argument("lz_decode: chunk_size must be > 0");
+        LzStream st;
+        st.chunk_size = chunk;
+        uint64_t p = 0, k = 0;
+        for (uint64_t off = 0; off < n; off += chunk, ++k) {
+            LzChunk c;
+            c.raw_len = static_cast<std::uint32_t>(std::min<uint64_t>(chunk, n - off));
+            c.payload.assign(payload + p, payload + p + enc_len[k]);
+            p += enc_len[k];
+            st.chunks.push_back(std::move(c));
+        }
+        const std::vector<std::uint8_t> d = lz_decode(st);
+        if (d.size() != n) throw corrupt_stream_error("lz_decode: size mismatch");
+        std::memcpy(out, d.data(), n);
+    });
+}
+
 wg_status wg_run_hooked(const wg_run_config* c, wg_metrics_row* rows, uint64_t max_rows,
                         uint64_t* nrows, double* final_grid, wg_run_summary* summary, wg_step_hook hook,
                         void* user) {

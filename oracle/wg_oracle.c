@@ -881,14 +881,41 @@ static double now_s(void) {
 /* The per-patch compression cycle of run(), pipeline.hpp:217-257:
  * extract_logical -> dwt_nd -> apply_threshold -> encode/decode (CSR) ->
  * nnz count -> skip rule -> idwt_nd -> insert_logical. */
-/* lz_encode_chunk (codec.hpp:127-175): the payload length of the greedy
- * LZ parse of one chunk (13-bit hash of 4 bytes, minimum match 4, offsets
- * <= 65535, literal/match lengths extended with 255-bytes). */
-static uint64_t lz_chunk_payload(const unsigned char* in, uint64_t n) {
+/* lz_encode_chunk (codec.hpp:127-175): the greedy LZ parse of one chunk
+ * (13-bit hash of 4 bytes, minimum match 4, offsets <= 65535, literal/match
+ * lengths extended with 255-bytes); returns the payload length and writes
+ * the payload to out when out != NULL. */
+static uint64_t lz_put_len(unsigned char* out, uint64_t o, uint64_t len) { /* lz_put_length, codec.hpp:113-119 */
+    while (len >= 255) {
+        if (out) out[o] = 255;
+        ++o;
+        len -= 255;
+    }
+    if (out) out[o] = (unsigned char)len;
+    return o + 1;
+}
+static uint64_t lz_put_seq(unsigned char* out, uint64_t o, const unsigned char* in, uint64_t anchor, uint64_t lit,
+                           int64_t ml, uint64_t offset) {
+    const unsigned ln = lit < 15 ? (unsigned)lit : 15u;
+    const unsigned mn = ml < 0 ? 0u : (ml < 15 ? (unsigned)ml : 15u);
+    if (out) out[o] = (unsigned char)((ln << 4) | mn);
+    ++o;
+    if (ln == 15) o = lz_put_len(out, o, lit - 15);
+    if (out) memcpy(out + o, in + anchor, lit);
+    o += lit;
+    if (ml < 0) return o;
+    if (out) {
+        out[o] = (unsigned char)(offset & 0xff);
+        out[o + 1] = (unsigned char)(offset >> 8);
+    }
+    o += 2;
+    if (mn == 15) o = lz_put_len(out, o, (uint64_t)ml - 15);
+    return o;
+}
+static uint64_t lz_chunk_encode(const unsigned char* in, uint64_t n, unsigned char* out) {
     static int64_t table[1u << 13];
     for (uint32_t k = 0; k < (1u << 13); ++k) table[k] = -1;
-    uint64_t anchor = 0, pos = 0, out = 0;
-#define LZ_EXT(len) ((len) / 255 + 1)
+    uint64_t anchor = 0, pos = 0, o = 0;
     while (n >= 4 && pos + 4 <= n) {
         uint32_t v;
         memcpy(&v, in + pos, 4);
@@ -898,20 +925,88 @@ static uint64_t lz_chunk_payload(const unsigned char* in, uint64_t n) {
         if (cand >= 0 && pos - (uint64_t)cand <= 65535 && memcmp(in + cand, in + pos, 4) == 0) {
             uint64_t len = 4;
             while (pos + len < n && in[cand + len] == in[pos + len]) ++len;
-            const uint64_t lit = pos - anchor, ml = len - 4;
-            out += 1 + (lit >= 15 ? LZ_EXT(lit - 15) : 0) + lit + 2 + (ml >= 15 ? LZ_EXT(ml - 15) : 0);
+            o = lz_put_seq(out, o, in, anchor, pos - anchor, (int64_t)(len - 4), pos - (uint64_t)cand);
             pos += len;
             anchor = pos;
             continue;
         }
         ++pos;
     }
-    if (anchor < n) {
-        const uint64_t lit = n - anchor;
-        out += 1 + (lit >= 15 ? LZ_EXT(lit - 15) : 0) + lit;
+    if (anchor < n) o = lz_put_seq(out, o, in, anchor, n - anchor, -1, 0);
+    return o;
+}
+static uint64_t lz_chunk_payload(const unsigned char* in, uint64_t n) { return lz_chunk_encode(in, n, NULL); }
+
+/* lz_decode_chunk (codec.hpp:177-220): 0 or the reason (1 truncated,
+ * 2 raw_len overrun, 3 bad match offset, 4 trailing bytes). */
+static int lz_get_len(const unsigned char* in, uint64_t in_len, uint64_t* p, uint64_t base, uint64_t* len) {
+    *len = base;
+    if (base == 15) {
+        unsigned b;
+        do {
+            if (*p + 1 > in_len) return 1;
+            b = in[(*p)++];
+            *len += b;
+        } while (b == 255);
     }
-#undef LZ_EXT
-    return out;
+    return 0;
+}
+static int lz_chunk_decode(const unsigned char* in, uint64_t in_len, uint64_t raw_len, unsigned char* out) {
+    uint64_t p = 0, o = 0;
+    while (o < raw_len) {
+        if (p + 1 > in_len) return 1;
+        const unsigned token = in[p++];
+        uint64_t lit, ml;
+        if (lz_get_len(in, in_len, &p, token >> 4, &lit)) return 1;
+        if (p + lit > in_len) return 1;
+        if (o + lit > raw_len) return 2;
+        memcpy(out + o, in + p, lit);
+        p += lit;
+        o += lit;
+        if (o == raw_len) break;
+        if (p + 2 > in_len) return 1;
+        const uint64_t offset = (uint64_t)in[p] | ((uint64_t)in[p + 1] << 8);
+        p += 2;
+        if (lz_get_len(in, in_len, &p, token & 0x0f, &ml)) return 1;
+        ml += 4;
+        if (offset == 0 || offset > o) return 3;
+        if (o + ml > raw_len) return 2;
+        for (uint64_t i = 0; i < ml; ++i) out[o + i] = out[o - offset + i];
+        o += ml;
+    }
+    return p != in_len ? 4 : 0;
+}
+
+wg_status wg_lz_encode(const uint8_t* data, uint64_t n, uint64_t chunk, uint8_t* out, uint64_t cap,
+                       uint64_t* enc_len, uint64_t* out_len) {
+    if (chunk == 0) return fail(WG_INVALID_ARGUMENT, "lz_encode: chunk_size must be > 0");
+    uint64_t tot = 0, k = 0;
+    for (uint64_t off = 0; off < n; off += chunk, ++k) { /* lz_encode, codec.hpp:223-235 */
+        const uint64_t len = n - off < chunk ? n - off : chunk;
+        const uint64_t m = lz_chunk_payload(data + off, len);
+        if (enc_len) enc_len[k] = m;
+        if (out) {
+            if (tot + m > cap) return fail(WG_OUT_OF_RANGE, "lz_encode: output buffer too small");
+            lz_chunk_encode(data + off, len, out + tot);
+        }
+        tot += m;
+    }
+    if (out_len) *out_len = tot;
+    return WG_OK;
+}
+
+wg_status wg_lz_decode(const uint8_t* payload, const uint64_t* enc_len, uint64_t chunk, uint8_t* out, uint64_t n) {
+    static const char* why[] = {"", "lz_decode: truncated chunk", "lz_decode: raw_len overrun",
+                                "lz_decode: bad match offset", "lz_decode: trailing bytes"};
+    if (chunk == 0) return fail(WG_INVALID_ARGUMENT, "lz_decode: chunk_size must be > 0");
+    uint64_t p = 0, k = 0;
+    for (uint64_t off = 0; off < n; off += chunk, ++k) { /* lz_decode, codec.hpp:237-244 */
+        const uint64_t len = n - off < chunk ? n - off : chunk;
+        const int e = lz_chunk_decode(payload + p, enc_len[k], len, out + off);
+        if (e) return fail(WG_CORRUPT_STREAM, why[e]);
+        p += enc_len[k];
+    }
+    return WG_OK;
 }
 
 /* LzStream::byte_size of lz_encode(bytes, chunk) (codec.hpp:99-105, 223-235). */

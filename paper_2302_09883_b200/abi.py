@@ -209,6 +209,8 @@ _PROTOS = {
     "wg_global_mass": (i32, [P(GridDesc), dp, u32, dp]),
     "wg_fv_step": (i32, [P(GridDesc), dp, dp, i32, f64, f64, f64, f64, f64]),
     "wg_lbm_step": (i32, [P(GridDesc), dp, dp, f64]),
+    "wg_lz_encode": (i32, [C.c_void_p, u64, u64, C.c_void_p, u64, P(u64), P(u64)]),
+    "wg_lz_decode": (i32, [C.c_void_p, P(u64), u64, C.c_void_p, u64]),
     "wg_run_config_default": (None, [P(RunConfigC)]),
     "wg_run_step_count": (i32, [P(RunConfigC), P(u64)]),
     "wg_run_grid_doubles": (i32, [P(RunConfigC), P(u64)]),

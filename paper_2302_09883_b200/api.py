@@ -266,6 +266,33 @@ def csr_decode(b: CsrBlock, lib=None) -> np.ndarray:
     return out
 
 
+def lz_encode(data, chunk_size: int, lib=None) -> tuple[bytes, list]:
+    """lz_encode (codec.hpp:223-235): (payloads back to back, per-chunk
+    payload lengths) of `data` (bytes-like) in chunks of chunk_size bytes."""
+    L = _lib(lib)
+    buf = np.frombuffer(bytes(data), dtype=np.uint8)
+    n = buf.size
+    nc = (n + chunk_size - 1) // chunk_size if chunk_size else 0
+    lens = (abi.u64 * max(nc, 1))()
+    tot = abi.u64()
+    src = buf.ctypes.data if n else None
+    L.check(L.wg_lz_encode(src, n, chunk_size, None, 0, lens, C.byref(tot)))
+    out = np.empty(max(tot.value, 1), dtype=np.uint8)
+    L.check(L.wg_lz_encode(src, n, chunk_size, out.ctypes.data, tot.value, lens, C.byref(tot)))
+    return out[: tot.value].tobytes(), [lens[k] for k in range(nc)]
+
+
+def lz_decode(payload: bytes, enc_len, chunk_size: int, n: int, lib=None) -> bytes:
+    """lz_decode (codec.hpp:237-244) of lz_encode's output back to n bytes;
+    CorruptStreamError like lz_decode_chunk (codec.hpp:177-220)."""
+    L = _lib(lib)
+    pl = np.frombuffer(bytes(payload) + b"\0", dtype=np.uint8)
+    lens = (abi.u64 * max(len(enc_len), 1))(*enc_len)
+    out = np.empty(max(n, 1), dtype=np.uint8)
+    L.check(L.wg_lz_decode(pl.ctypes.data, lens, chunk_size, out.ctypes.data, n))
+    return out[:n].tobytes()
+
+
 # ---- patchgrid.hpp ---------------------------------------------------------------
 
 

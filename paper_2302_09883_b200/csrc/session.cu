@@ -18,6 +18,7 @@
 #include "common.cuh"
 #include "host_model.h"
 #include "kernel_table.h"
+#include "lz.cuh"
 #include "patch_phases.cuh"
 
 namespace wg {
@@ -169,107 +170,8 @@ __global__ void k_swe_vmax(const double* grid, uint32_t N, uint64_t npatch, doub
 }
 
 // ---- Codec::lz metrics (codec.hpp:81-244): the byte size of lz_encode of
-// every block's coefficient array, computed exactly like lz_encode_chunk's
-// greedy parse (13-bit hash table, 4-byte minimum match, offsets < 65536,
-// the match extension compares 8 bytes at a time but stops at the same
-// first differing byte) without materialising the stream. ------------------
-__device__ __forceinline__ uint64_t lz_load8(const unsigned char* p) {
-    const uintptr_t a = reinterpret_cast<uintptr_t>(p);
-    const uint64_t* w = reinterpret_cast<const uint64_t*>(a & ~uintptr_t(7));
-    const unsigned sh = (unsigned)(a & 7) * 8;
-    const uint64_t lo = __ldg(w);
-    return sh ? (lo >> sh) | (__ldg(w + 1) << (64 - sh)) : lo;  // the buffer has 8 B of tail padding
-}
-
-// One warp per chunk: the parse itself is sequential (every lane follows it
-// in lock-step), the table is cleared and every match is extended 256 bytes
-// at a time by the 32 lanes (ballot: the first differing byte).
-__device__ uint32_t lz_chunk_size_warp(const unsigned char* in, uint32_t n, unsigned short* table) {
-    const int lane = threadIdx.x & 31;
-    // chunk positions are < 65536 - 3, so 16-bit entries with 0xFFFF as "empty"
-    for (int k = lane; k < 8192 / 8; k += 32) reinterpret_cast<uint4*>(table)[k] = make_uint4(~0u, ~0u, ~0u, ~0u);
-    __syncwarp();
-    uint32_t anchor = 0, pos = 0, out = 0;
-    auto ext = [](uint32_t len) { return len / 255 + 1; };  // lz_put_length bytes
-    // 32 candidate positions per iteration, one per lane: each lane sees the
-    // table as the sequential parse would after inserting the positions of
-    // the lower lanes (the latest lower lane with the same hash, else the
-    // table), the lowest lane with a match ends the window, and only the
-    // positions up to it are inserted (latest position per hash).
-    while (n >= 4 && pos + 4 <= n) {
-        const uint32_t w = pos + lane;
-        const bool act = w + 4 <= n;
-        const uint32_t v = act ? (uint32_t)lz_load8(in + w) : 0u;
-        const uint32_t h = (v * 2654435761u) >> 19;
-        const unsigned actm = __ballot_sync(0xffffffffu, act);
-        const unsigned peers = __match_any_sync(0xffffffffu, act ? h : 0xFFFFFFFFu) & actm;
-        const unsigned lower = peers & ((1u << lane) - 1u);
-        const unsigned short t = act && !lower ? table[h] : (unsigned short)0xFFFFu;
-        const int cand = !act ? -1 : lower ? (int)(pos + 31 - __clz(lower)) : (t == 0xFFFFu ? -1 : (int)t);
-        const bool hit = act && cand >= 0 && w - (uint32_t)cand <= 65535u && (uint32_t)lz_load8(in + cand) == v;
-        const unsigned hits = __ballot_sync(0xffffffffu, hit);
-        const int first = hits ? __ffs(hits) - 1 : 31;
-        const unsigned upto = (first == 31) ? actm : (actm & ((2u << first) - 1u));
-        // insert the processed positions: per hash the latest one wins
-        const unsigned later = peers & upto & ~((2u << lane) - 1u);
-        __syncwarp();
-        if (((upto >> lane) & 1u) && !later) table[h] = (unsigned short)w;
-        __syncwarp();
-        if (!hits) {
-            pos += __popc(actm);  // all literals
-            continue;
-        }
-        const uint32_t mpos = pos + first;
-        const int mc = __shfl_sync(0xffffffffu, cand, first);
-        uint32_t len = 4;
-        for (;;) {
-            if (mpos + len + 1024 <= n) {  // 1 KiB per round: 4 independent word pairs per lane in flight
-                uint64_t d[4];
-#pragma unroll
-                for (int u = 0; u < 4; ++u)
-                    d[u] = lz_load8(in + mc + len + 256 * u + 8 * lane) ^ lz_load8(in + mpos + len + 256 * u + 8 * lane);
-                bool stop = false;
-#pragma unroll
-                for (int u = 0; u < 4 && !stop; ++u) {
-                    const unsigned m = __ballot_sync(0xffffffffu, d[u] != 0);
-                    if (!m) {
-                        len += 256;
-                        continue;
-                    }
-                    const int f = __ffs(m) - 1;
-                    const uint64_t df = __shfl_sync(0xffffffffu, d[u], f);
-                    len += 8 * f + (uint32_t)(__ffsll((long long)df) - 1) / 8;
-                    stop = true;
-                }
-                if (stop) break;
-                continue;
-            }
-            if (mpos + len + 256 <= n) {
-                const uint64_t d = lz_load8(in + mc + len + 8 * lane) ^ lz_load8(in + mpos + len + 8 * lane);
-                const unsigned m = __ballot_sync(0xffffffffu, d != 0);
-                if (!m) {
-                    len += 256;
-                    continue;
-                }
-                const int f = __ffs(m) - 1;
-                const uint64_t df = __shfl_sync(0xffffffffu, d, f);
-                len += 8 * f + (uint32_t)(__ffsll((long long)df) - 1) / 8;
-                break;
-            }
-            while (mpos + len < n && in[mc + len] == in[mpos + len]) ++len;  // the tail (< 256 B)
-            break;
-        }
-        const uint32_t lit = mpos - anchor, ml = len - 4;
-        out += 1 + (lit >= 15 ? ext(lit - 15) : 0) + lit + 2 + (ml >= 15 ? ext(ml - 15) : 0);
-        pos = mpos + len;
-        anchor = pos;
-    }
-    if (anchor < n) {  // the terminal literal-only sequence
-        const uint32_t lit = n - anchor;
-        out += 1 + (lit >= 15 ? ext(lit - 15) : 0) + lit;
-    }
-    return out;
-}
+// every block's coefficient array — the warp parse of lz.cuh without
+// emitting the bytes. ------------------------------------------------------
 
 // The step's LZ row: the sizes are summed by atomics (integers: any order
 // gives the same sum) and the last warp writes compressed_bytes and ratio
@@ -308,7 +210,7 @@ __global__ void __launch_bounds__(32 * kLzWarps) k_lz_sizes(const double* dense,
         // table positions whatever the configured size
         for (uint32_t off = 0; off < bytes; off += chunk) {
             const uint32_t len = min(chunk, bytes - off);
-            sum += 8 + lz_chunk_size_warp(in + off, len, table);
+            sum += 8 + lz_chunk_warp<unsigned short>(in + off, len, table, nullptr);
         }
     }
     if ((threadIdx.x & 31) != 0) return;

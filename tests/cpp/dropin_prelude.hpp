@@ -15,8 +15,8 @@
 // the sm_100a product on the GPU box, the C oracle on CPU.
 //
 // Routed: dwt_nd, idwt_nd, band_threshold, apply_threshold, csr_encode,
-// csr_decode, sync_ghosts, global_mass, run, sweep (its runs through the
-// drop-in's run).  Not routed: the per-patch fv_step template (the drop-in's fv_step is per grid) and the reference's
+// csr_decode, lz_encode, lz_decode, sync_ghosts, global_mass, run, sweep
+// (its runs through the drop-in's run).  Not routed: the per-patch fv_step template (the drop-in's fv_step is per grid) and the reference's
 // non-path helpers (decompose, fill, assemble, lz_*, file formats).
 #pragma once
 
@@ -58,6 +58,8 @@
 #define global_mass(...) ref_cpu_global_mass(__VA_ARGS__)
 #define run(...) ref_cpu_run(__VA_ARGS__)
 #define sweep(...) ref_cpu_sweep(__VA_ARGS__)
+#define lz_encode(...) ref_cpu_lz_encode(__VA_ARGS__)
+#define lz_decode(...) ref_cpu_lz_decode(__VA_ARGS__)
 
 #include "wavegrid/codec.hpp"
 #include "wavegrid/field.hpp"
@@ -77,6 +79,8 @@
 #undef global_mass
 #undef run
 #undef sweep
+#undef lz_encode
+#undef lz_decode
 
 #include "wavegrid_b200_reference.hpp"
 
@@ -88,6 +92,8 @@ using b200::csr_encode;
 using b200::dwt_nd;
 using b200::global_mass;
 using b200::idwt_nd;
+using b200::lz_decode;
+using b200::lz_encode;
 using b200::run;
 using b200::sweep;
 using b200::sync_ghosts;

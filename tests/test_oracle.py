@@ -265,3 +265,28 @@ def test_lz_metrics_vs_reference(oracle, reference, scheme):
                         spec=api.ThresholdSpec("capped", 1e-3), codec="lz", compute_l2=False, **kw)
     a, b = api.run(cfg, lib=oracle), api.run(cfg, lib=reference)
     assert [(r["compressed_bytes"], r["ratio"]) for r in a.rows] == [(r["compressed_bytes"], r["ratio"]) for r in b.rows]
+
+
+# ---- Codec::lz bytes (codec.hpp:81-244): the C restatement's lz_encode /
+# lz_decode against the reference compiled unchanged, byte for byte ----------
+
+def test_lz_codec_matches_reference(oracle, reference):
+    from .lz_cases import CHUNKS, corruptions, lz_inputs
+
+    for name, data in lz_inputs().items():
+        for chunk in CHUNKS:
+            if chunk < 64 and len(data) > 5000:
+                continue
+            got = api.lz_encode(data, chunk, lib=oracle)
+            want = api.lz_encode(data, chunk, lib=reference)
+            assert got == want, (name, chunk)
+            assert api.lz_decode(got[0], got[1], chunk, len(data), lib=oracle) == data, (name, chunk)
+    data = lz_inputs()["smooth_f64"][:4000]
+    pl, lens = api.lz_encode(data, 1 << 16, lib=reference)
+    for name, p2, l2 in corruptions(pl, lens):
+        for lib in (oracle, reference):
+            with pytest.raises(abi.CorruptStreamError):
+                api.lz_decode(p2, l2, 1 << 16, len(data), lib=lib)
+    for lib in (oracle, reference):
+        with pytest.raises(abi.InvalidArgument):
+            api.lz_encode(b"abc", 0, lib=lib)
