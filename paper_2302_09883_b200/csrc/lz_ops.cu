@@ -3,6 +3,7 @@
 // chunk (lz.cuh).  Encoding runs the parse twice: lengths first (a host
 // prefix sum places the chunks), then the payload bytes at their offsets —
 // byte-identical to the reference (tests/test_gpu_lz_codec.py).
+#include <cstring>
 #include <vector>
 
 #include "common.cuh"
@@ -35,6 +36,43 @@ __global__ void __launch_bounds__(32) k_lz_decode(const unsigned char* in, const
 }
 
 }  // namespace
+
+// lz_encode of a device buffer (n bytes + >= 16 B of tail padding) in chunks
+// of `chunk` bytes: the per-chunk payload lengths and the payloads back to
+// back, on the host (session checkpoints, wg_lz_encode).
+void lz_encode_device(const unsigned char* d_in, uint64_t n, uint64_t chunk, std::vector<uint64_t>& len,
+                      std::vector<unsigned char>* payload) {
+    const uint64_t nc = (n + chunk - 1) / chunk;
+    len.assign(nc, 0);
+    if (payload) payload->clear();
+    if (nc == 0) return;
+    if (nc > 0x7FFFFFFFull || chunk > 0xFFFFFFFFull) raise(WG_INVALID_ARGUMENT, "lz_encode: sizes out of range");
+    DevBuf<uint64_t> d_len(nc);
+    const bool small = chunk <= 65535;
+    const size_t smem = small ? 8192 * sizeof(uint16_t) : 8192 * sizeof(uint32_t);
+    auto launch = [&](const uint64_t* off, unsigned char* dst) {
+        if (small) k_lz_encode<uint16_t><<<(unsigned)nc, 32, smem>>>(d_in, n, chunk, off, dst, d_len.p);
+        else k_lz_encode<uint32_t><<<(unsigned)nc, 32, smem>>>(d_in, n, chunk, off, dst, d_len.p);
+        WG_LAUNCH_CHECK("lz encode");
+        WG_CUDA(cudaDeviceSynchronize());
+    };
+    launch(nullptr, nullptr);  // payload lengths
+    d_len.download(len.data());
+    if (!payload) return;
+    std::vector<uint64_t> off(nc);
+    uint64_t tot = 0;
+    for (uint64_t c = 0; c < nc; ++c) {
+        off[c] = tot;
+        tot += len[c];
+    }
+    DevBuf<uint64_t> d_off(nc);
+    d_off.upload(off.data());
+    DevBuf<unsigned char> d_out(tot + 1);
+    launch(d_off.p, d_out.p);  // the payload bytes
+    payload->resize(tot);
+    if (tot) WG_CUDA(cudaMemcpy(payload->data(), d_out.p, tot, cudaMemcpyDeviceToHost));
+}
+
 }  // namespace wg
 
 using namespace wg;
@@ -45,41 +83,23 @@ wg_status wg_lz_encode(const uint8_t* data, uint64_t n, uint64_t chunk, uint8_t*
                        uint64_t* enc_len, uint64_t* out_len) {
     return guard([&] {
         if (chunk == 0) raise(WG_INVALID_ARGUMENT, "lz_encode: chunk_size must be > 0");
-        if (chunk > 0xFFFFFFFFull) raise(WG_INVALID_ARGUMENT, "lz_encode: chunk_size above 4 GiB");
-        const uint64_t nc = (n + chunk - 1) / chunk;
         if (out_len) *out_len = 0;
-        if (nc == 0) return;
-        if (nc > 0x7FFFFFFFull) raise(WG_INVALID_ARGUMENT, "lz_encode: too many chunks");
+        if (n == 0) return;
         DevBuf<unsigned char> d_in(n + 16);  // tail padding for the 8-byte word loads
         WG_CUDA(cudaMemcpy(d_in.p, data, n, cudaMemcpyHostToDevice));
         WG_CUDA(cudaMemset(d_in.p + n, 0, 16));
-        DevBuf<uint64_t> d_len(nc);
-        const bool small = chunk <= 65535;
-        const size_t smem = small ? 8192 * sizeof(uint16_t) : 8192 * sizeof(uint32_t);
-        auto launch = [&](const uint64_t* off, unsigned char* dst) {
-            if (small) k_lz_encode<uint16_t><<<(unsigned)nc, 32, smem>>>(d_in.p, n, chunk, off, dst, d_len.p);
-            else k_lz_encode<uint32_t><<<(unsigned)nc, 32, smem>>>(d_in.p, n, chunk, off, dst, d_len.p);
-            WG_LAUNCH_CHECK("lz encode");
-            WG_CUDA(cudaDeviceSynchronize());
-        };
-        launch(nullptr, nullptr);  // payload lengths
-        std::vector<uint64_t> len(nc), off(nc);
-        d_len.download(len.data());
+        std::vector<uint64_t> len;
+        std::vector<unsigned char> pl;
+        lz_encode_device(d_in.p, n, chunk, len, out ? &pl : nullptr);
         uint64_t tot = 0;
-        for (uint64_t c = 0; c < nc; ++c) {
-            off[c] = tot;
+        for (size_t c = 0; c < len.size(); ++c) {
+            if (enc_len) enc_len[c] = len[c];
             tot += len[c];
         }
-        if (enc_len)
-            for (uint64_t c = 0; c < nc; ++c) enc_len[c] = len[c];
         if (out_len) *out_len = tot;
         if (!out) return;
         if (tot > cap) raise(WG_OUT_OF_RANGE, "lz_encode: output buffer too small");
-        DevBuf<uint64_t> d_off(nc);
-        d_off.upload(off.data());
-        DevBuf<unsigned char> d_out(tot + 1);
-        launch(d_off.p, d_out.p);  // the payload bytes
-        WG_CUDA(cudaMemcpy(out, d_out.p, tot, cudaMemcpyDeviceToHost));
+        std::memcpy(out, pl.data(), tot);
     });
 }
 

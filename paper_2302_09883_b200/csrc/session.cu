@@ -24,6 +24,8 @@
 namespace wg {
 
 void direction_speeds(double alpha, double beta, double* smax, double* smin);  // ops.cu
+void lz_encode_device(const unsigned char* d_in, uint64_t n, uint64_t chunk, std::vector<uint64_t>& len,
+                      std::vector<unsigned char>* payload);  // lz_ops.cu
 
 namespace {
 
@@ -228,6 +230,22 @@ __global__ void __launch_bounds__(32 * kLzWarps) k_lz_sizes(const double* dense,
 }
 
 __global__ void k_set_u64(unsigned long long* p, unsigned long long v) { *p = v; }
+
+// Checkpoint: the raw blocks of a batch gathered back to back (block k from
+// pool offset src[k], or the constant with the bits cst[k] when src[k] is
+// ~0), for the device LZ encoder.
+__global__ void k_gather_raw(const unsigned char* pool, const uint64_t* src, const unsigned long long* cst,
+                             uint64_t rawb, unsigned char* dst) {
+    const uint64_t k = blockIdx.x;
+    unsigned char* d = dst + k * rawb;
+    if (src[k] == ~0ull) {
+        const double c = __longlong_as_double((long long)cst[k]);
+        for (uint64_t i = threadIdx.x; i < rawb / 8; i += blockDim.x) reinterpret_cast<double*>(d)[i] = c;
+    } else {
+        const double* s = reinterpret_cast<const double*>(pool + src[k]);
+        for (uint64_t i = threadIdx.x; i < rawb / 8; i += blockDim.x) reinterpret_cast<double*>(d)[i] = s[i];
+    }
+}
 
 // ---- peer halo mode (multi-GPU): the step kernels store the halo lines into
 // the ring neighbours' halo slots themselves (EdgeSet::peer_lo/peer_hi); a
@@ -1150,6 +1168,49 @@ struct Session {
         auto put64 = [&](uint64_t v) { put(&v, 8); };
         put(&h, sizeof h);
         const uint64_t nn = (uint64_t)N * N, rawb = nn * 8;
+        // lz_encode of every raw block (one 64 KiB chunk each: a block is
+        // smaller) by the device encoder (lz.cuh), in batches of <= 512 MB
+        // taken in record order: the file's raw records are the reference's
+        // own lz_encode output of the block bytes (codec.hpp:223-235)
+        std::vector<uint64_t> raw_src;
+        std::vector<unsigned long long> raw_cst;
+        for (uint64_t p = 0; p < sg.npatch; ++p) {
+            const DirEntry* e = &hd[p * sg.m];
+            bool raw = false;
+            for (uint32_t q = 0; q < sg.m; ++q) raw = raw || (e[q].flags & DIR_RAW);
+            if (!raw) continue;
+            for (uint32_t q = 0; q < sg.m; ++q) {
+                const bool cst = (e[q].flags & DIR_CONST) != 0;
+                raw_src.push_back(cst ? ~0ull : e[q].off);
+                raw_cst.push_back(cst ? (unsigned long long)e[q].off : 0ull);
+            }
+        }
+        const uint64_t batch = std::max<uint64_t>(1, (512ull << 20) / rawb);
+        uint64_t raw_next = 0, batch_first = 0;
+        std::vector<uint64_t> enc_len;
+        std::vector<unsigned char> enc_pl;
+        std::vector<uint64_t> enc_off;
+        auto raw_payload = [&](const unsigned char** pl, uint64_t* len) {
+            if (raw_next == batch_first + enc_len.size()) {  // encode the next batch
+                batch_first = raw_next;
+                const uint64_t nb = std::min<uint64_t>(batch, raw_src.size() - batch_first);
+                DevBuf<uint64_t> d_src(nb);
+                DevBuf<unsigned long long> d_cst(nb);
+                d_src.upload(raw_src.data() + batch_first);
+                d_cst.upload(raw_cst.data() + batch_first);
+                DevBuf<unsigned char> d_raw(nb * rawb + 16);
+                WG_CUDA(cudaMemset(d_raw.p + nb * rawb, 0, 16));
+                k_gather_raw<<<(unsigned)nb, 256, 0, stream>>>(store[cur], d_src.p, d_cst.p, rawb, d_raw.p);
+                WG_LAUNCH_CHECK("checkpoint gather");
+                WG_CUDA(cudaStreamSynchronize(stream));
+                lz_encode_device(d_raw.p, nb * rawb, rawb, enc_len, &enc_pl);
+                enc_off.assign(nb, 0);
+                for (uint64_t k = 1; k < nb; ++k) enc_off[k] = enc_off[k - 1] + enc_len[k - 1];
+            }
+            const uint64_t k = raw_next++ - batch_first;
+            *pl = enc_pl.data() + enc_off[k];
+            *len = enc_len[k];
+        };
         for (uint64_t p = 0; p < sg.npatch; ++p) {
             const DirEntry* e = &hd[p * sg.m];
             bool raw = false;
@@ -1169,35 +1230,17 @@ struct Session {
                 const bool cst = (e[q].flags & DIR_CONST) != 0;
                 if (!cst && e[q].off + (raw ? rawb : 12ull * e[q].nnz + 4ull * (N + 1)) > used)
                     raise(WG_CORRUPT_STREAM, "checkpoint: directory entry outside the pool");
-                std::vector<double> cbuf;  // a constant block, materialised (the file holds raw records)
-                if (cst) {
-                    double c;
-                    std::memcpy(&c, &e[q].off, 8);
-                    cbuf.assign(nn, c);
-                }
-                const unsigned char* b = cst ? reinterpret_cast<const unsigned char*>(cbuf.data()) : pool.data() + e[q].off;
+                const unsigned char* b = pool.data() + (cst ? 0 : e[q].off);  // CSR blocks only (raw: encoded above)
                 if (raw) {
                     if (!(e[q].flags & DIR_RAW)) raise(WG_LOGIC, "checkpoint: mixed raw/CSR patch");
-                    const uint64_t chunk = 64 * 1024, nch = (rawb + chunk - 1) / chunk;
-                    put64(chunk);
-                    put64(nch);
-                    for (uint64_t c = 0; c < nch; ++c) {
-                        const uint64_t len = std::min(chunk, rawb - c * chunk);
-                        std::vector<unsigned char> pl;  // literal-only sequence
-                        pl.push_back(len >= 15 ? 0xF0 : (unsigned char)(len << 4));
-                        if (len >= 15) {
-                            uint64_t r = len - 15;
-                            while (r >= 255) {
-                                pl.push_back(255);
-                                r -= 255;
-                            }
-                            pl.push_back((unsigned char)r);
-                        }
-                        pl.insert(pl.end(), b + c * chunk, b + c * chunk + len);
-                        put32((uint32_t)len);
-                        put32((uint32_t)pl.size());
-                        put(pl.data(), pl.size());
-                    }
+                    const unsigned char* pl = nullptr;
+                    uint64_t pl_len = 0;
+                    raw_payload(&pl, &pl_len);
+                    put64(64 * 1024);  // LzStream: chunk_size, one chunk (rawb < 64 KiB)
+                    put64(1);
+                    put32((uint32_t)rawb);
+                    put32((uint32_t)pl_len);
+                    put(pl, pl_len);
                 } else {
                     const uint32_t nz = e[q].nnz;
                     put32(N);

@@ -103,9 +103,10 @@ def test_resume_is_bit_identical(product, oracle, tmp_path, scheme):
         b.close()
 
 
-def test_raw_patches_round_trip(product, tmp_path):
-    """c = 0: every patch is stored raw (skip rule) -> Codec::lz records
-    with literal-only chunks; -0.0 and every other bit pattern survive."""
+def test_raw_patches_round_trip(product, reference, tmp_path):
+    """c = 0: every patch is stored raw (skip rule) -> Codec::lz records whose
+    payloads are the reference's own lz_encode of the block bytes (the device
+    encoder, csrc/lz.cuh); -0.0 and every other bit pattern survive."""
     cfg = _cfg("swe")
     cfg.spec = api.ThresholdSpec("constant", 0.0)
     g0 = api.initial_state(cfg, lib=product)
@@ -117,6 +118,17 @@ def test_raw_patches_round_trip(product, tmp_path):
         product.check(product.wg_session_save(a.h, str(ck).encode()))
         _, recs = api.read_checkpoint(ck)
         assert {r.codec for r in recs} == {2} and all(r.levels == 0 for r in recs)
+        state = a.state()
+        n = recs[0].dims[0]
+        tc = (n + 2) ** 2
+        for p in (0, 5, len(recs) - 1):
+            for q in range(recs[p].components):
+                blk = state[(p * recs[p].components + q) * tc: (p * recs[p].components + q + 1) * tc].reshape(n + 2, n + 2)
+                raw = np.ascontiguousarray(blk[1:-1, 1:-1]).tobytes()
+                payload, lens = api.lz_encode(raw, 64 * 1024, lib=reference)
+                chunk, chunks = recs[p].lz[q]
+                assert chunk == 64 * 1024 and [c[0] for c in chunks] == [len(raw)]
+                assert [len(c[1]) for c in chunks] == lens and chunks[0][1] == payload, (p, q)
         product.check(product.wg_session_load(b.h, str(ck).encode()))
         assert np.array_equal(bits(b.state()), bits(a.state()))
         a.steps(2)
