@@ -58,6 +58,8 @@ def exchange_halos(send_lo, send_hi, recv_lo, recv_hi, rank: int, world: int, di
         dist.P2POp(dist.irecv, recv_lo, above),
         dist.P2POp(dist.irecv, recv_hi, below),
     ]
+    # NCCL: wait() orders the session stream after the transfer (a device-side
+    # dependency, no host wait); gloo (tests on one GPU) completes on the host
     for req in dist.batch_isend_irecv(ops):
         req.wait()
     if staged:
