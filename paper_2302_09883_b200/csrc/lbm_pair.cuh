@@ -999,17 +999,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<N>::NT, 1
                 {
                     const int lane = t & 31;
                     unsigned todo = __ballot_sync(0xffffffffu, jb.on && nz != 0 && slot_ok[jb.s]);
+                    // rows whose kept coefficients are all samples: only the
+                    // first 32 corner columns can hold them (NS <= 32)
+                    const unsigned sonly = __ballot_sync(0xffffffffu, samp_only);
                     while (todo) {
                         const int src = __ffs(todo) - 1;
                         todo &= todo - 1;
                         const int s_ = __shfl_sync(0xffffffffu, jb.s, src), r_ = __shfl_sync(0xffffffffu, jb.li, src);
                         uint32_t k_ = __shfl_sync(0xffffffffu, k, src);
+                        const int cols = ((sonly >> src) & 1u) && ((N - 1) >> L) < 32 ? 32 : N;  // uniform
                         const double* row = bufs + (size_t)s_ * BUFD + (size_t)r_ * N;  // interleaved order
                         unsigned char* const blk = a.store_out + slot_off[s_];
                         double* vo = reinterpret_cast<double*>(blk);
                         uint32_t* co = reinterpret_cast<uint32_t*>(blk + 8ull * slot_nnz[s_]);
 #pragma unroll
                         for (int base = 0; base < N; base += 32) {
+                            if (base >= cols) break;
                             const int pc = base + lane;  // corner-layout column
                             const double xv = pc < N ? row[ilv[pc < N ? pc : 0]] : 0.0;
                             const unsigned m = __ballot_sync(0xffffffffu, xv != 0.0);
