@@ -147,3 +147,63 @@ def test_c2_grid_tiny_threshold(product, oracle, c):
     never overflow, and the run equals the reference's bit for bit."""
     cfg = lbm_cfg(C2["nx"], C2["splits"], C2["levels"], c, 3)
     compare_runs(api.run(cfg, lib=product), api.run(cfg, lib=oracle))
+
+
+def test_c4_full_size_streamed_equals_uploaded(product):
+    """C4 at its full size (16384^2, 256 x 256 patches of 65^2, L = 4, capped
+    1e-3) with the host initial state: the bench path (store budget 8 GiB,
+    the raw state streamed into step 1, wg_session_step_host) against the
+    plain path (no budget: the raw state uploaded into the store first) —
+    two different code paths, the same result: every metrics row equal
+    (nnz, zeroed, bytes; mass to 1e-13), the stored CSR blocks of sampled
+    patches (all 9 populations) bitwise equal; and the size-independent
+    properties: mass conserved to round-off, every block at the L = 4 floor
+    (25 samples: 564 bytes)."""
+    cfg = lbm_cfg(16385, (256, 256), 4, 1e-3, 4)
+    g0 = api.initial_state(cfg, lib=product).data.reshape(-1)
+    steps = 4
+    samples = [0, 255, 256 * 128 + 77, 65535 - 256, 65535]
+
+    def block(s, p, q):
+        nnz, raw = abi.u64(), abi.i32()
+        product.check(product.wg_session_patch_csr(s, p, q, None, None, None, C.byref(nnz), C.byref(raw)))
+        v = np.empty(max(nnz.value, 1))
+        col = np.empty(max(nnz.value, 1), np.uint32)
+        row = np.empty(66, np.uint32)
+        product.check(product.wg_session_patch_csr(
+            s, p, q, abi.dptr(v), col.ctypes.data_as(C.POINTER(abi.u32)),
+            row.ctypes.data_as(C.POINTER(abi.u32)), C.byref(nnz), C.byref(raw)))
+        return raw.value, bits(v[: nnz.value]).tobytes(), col[: nnz.value].tobytes(), row.tobytes()
+
+    def go(budget):
+        cfg.store_budget_bytes = budget
+        s = _session(product, cfg)
+        try:
+            if budget:
+                product.check(product.wg_session_step_host(s, abi.dptr(g0), 1.0))
+            else:
+                product.check(product.wg_session_upload(s, abi.dptr(g0)))
+                product.check(product.wg_session_step(s, 1.0))
+            for _ in range(steps - 1):
+                product.check(product.wg_session_step(s, 1.0))
+            rows = (abi.MetricsRowC * steps)()
+            n = abi.u64()
+            product.check(product.wg_session_metrics(s, rows, steps, C.byref(n)))
+            r = [(x.step, x.nnz, x.zeroed, x.compressed_bytes, x.dense_bytes, x.global_mass) for x in rows[: n.value]]
+            blocks = {(p, q): block(s, p, q) for p in samples for q in range(9)}
+            return r, blocks
+        finally:
+            product.wg_session_destroy(s)
+
+    ra, ba = go(8 << 30)
+    rb, bb = go(0)
+    assert len(ra) == steps and [x[:5] for x in ra] == [x[:5] for x in rb]
+    # masses: the streamed step 1 sums its patch-row chunks' partials in
+    # another (fixed) order than one launch does
+    assert all(abs(x[5] - y[5]) <= 1e-13 * abs(y[5]) for x, y in zip(ra, rb))
+    assert ba == bb
+    npatch = 256 * 256
+    m0 = ra[0][5]
+    for step, nnz, zeroed, cb, db, mass in ra:
+        assert nnz == npatch * 9 * 25 and cb == npatch * 9 * 564 and db == npatch * 9 * 65 * 65 * 8
+        assert abs(mass - m0) <= 1e-12 * abs(m0)

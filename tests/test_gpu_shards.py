@@ -323,3 +323,53 @@ def test_shards_transport_l2_sums(product):
     finally:
         single.close()
         multi.close()
+
+
+def test_c5_full_size_two_shards_equal_one(product):
+    """C5 at its full size (65536^2: 1024 x 1024 patches of 65^2, L = 4,
+    capped 1e-3, store budget 24 GiB per shard, device-generated initial
+    state): the grid as 2 patch-row shards with the halo ring exchanged
+    between steps equals the one-shard run — every metrics row (the shards'
+    integer counts summed exactly, masses to round-off), the stored blocks of
+    sampled patches on both sides of both shard boundaries bitwise; mass
+    conserved and every block at the L = 4 floor."""
+    cfg = _cfg("lbm", 65537, (1024, 1024), 4, 1e-3)
+    cfg.store_budget_bytes = 24 << 30
+    steps, n, P1 = 3, 65, 1024
+    single = LocalShards(product, cfg, 1)
+    try:
+        for s in single.sessions:
+            product.check(product.wg_session_init_device(s.handle))
+        single.exchange()
+        for _ in range(steps):
+            single.step()
+        single.stream.synchronize()
+        r1 = single.rows()[0]
+        picks = [(row, col) for row in (0, 511, 512, 1023) for col in (0, 700)]
+        want = {(row, col, q): _block(product, single.sessions[0], row * P1 + col, q, n)
+                for row, col in picks for q in range(9)}
+    finally:
+        single.close()
+    multi = LocalShards(product, cfg, 2)
+    try:
+        for s in multi.sessions:
+            product.check(product.wg_session_init_device(s.handle))
+        multi.exchange()
+        for _ in range(steps):
+            multi.step()
+        multi.stream.synchronize()
+        rn = multi.rows()
+        for k in range(steps):
+            for key in ("dense_bytes", "compressed_bytes", "nnz", "zeroed"):
+                assert r1[k][key] == sum(p[k][key] for p in rn), key
+            m = sum(p[k]["global_mass"] for p in rn)
+            assert abs(m - r1[k]["global_mass"]) <= 1e-12 * abs(r1[k]["global_mass"])
+            assert r1[k]["compressed_bytes"] == 1024 * 1024 * 9 * 564
+            assert abs(r1[k]["global_mass"] - r1[0]["global_mass"]) <= 1e-12 * abs(r1[0]["global_mass"])
+        for row, col in picks:
+            sh = 0 if row < 512 else 1
+            for q in range(9):
+                got = _block(product, multi.sessions[sh], (row - 512 * sh) * P1 + col, q, n)
+                assert got == want[(row, col, q)], (row, col, q)
+    finally:
+        multi.close()
