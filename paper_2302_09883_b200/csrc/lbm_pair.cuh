@@ -3,18 +3,22 @@
 //
 // A 65^2 x 9 fp64 patch is 304 KB: more than one SM's shared memory, less
 // than two.  The pair splits it by population: rank 0 owns populations
-// 1..4, rank 1 owns 5..8, and both hold a replica of the rest population 0
-// (no streaming, no edges).  Every CTA therefore has 4 x 65 + 33 (or 32)
-// line jobs per pass — one per thread (10 warps) — and every phase except
-// the collide is CTA-local:
+// {1, 3, 5, 6}, rank 1 {2, 4, 7, 8}, and both hold a replica of the rest
+// population 0 (no streaming, no edges).  Every CTA therefore has 4 x 65 +
+// 33 (or 32) line jobs per pass — one per thread, population 0's from the
+// next warp boundary (12 warps with the control warp) — and every phase
+// except the collide is CTA-local:
 //
 //   D0  wait for the patch's CSR blocks (cp.async.bulk into shared memory,
 //       issued while the previous patch was being processed; mbarrier)
-//   D1  decode rows: CSR scatter + inverse transform along dim 1 of the
-//       non-empty coefficient rows only (a row that decodes to nothing is
-//       never touched: the column pass reads it as +0.0 through a row mask)
-//   D2  decode columns: inverse transform along dim 0 from the masked rows
-//       (zero-detail levels skipped bit-exactly, lifting.cuh), ghost values
+//   D1  decode rows: a block whose stored coefficients are all among the
+//       NS x NS coarsest samples (the common case) only scatters them;
+//       otherwise CSR scatter + inverse transform along dim 1 of the
+//       non-empty coefficient rows (a row that decodes to nothing is never
+//       touched: the column pass reads it as +0.0 through a row mask)
+//   D2  decode columns: inverse transform along dim 0 (samples-only blocks:
+//       each column's row values by the predict chains, idwt_samples_at;
+//       zero-detail levels skipped bit-exactly, lifting.cuh), ghost values
 //       from the neighbours' edge lines, pull streaming as a register shift
 //       -> the streamed population field in shared memory
 //   C   BGK collide of this CTA's column half of the patch: 9 populations per
