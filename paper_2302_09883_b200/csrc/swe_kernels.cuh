@@ -51,6 +51,37 @@ struct SweLayout {
 #define WG_SWE_MIN_BLOCKS 2  // 2 CTAs per SM (spills in the lifting phases, +44% C3)
 #endif
 
+// A still-water patch: its three input blocks are constant directory entries
+// (h, +0.0, +0.0) and so are those of its four face neighbours (whose edge
+// lines, the ghost values, are then these constants too).  Every face then
+// carries the same Riemann problem with u* = 0 exactly, the ±x (±y) momentum
+// fluxes cancel exactly and the mass fluxes are 0: the FV output equals the
+// input bit for bit, its transform has the 5/3 samples h and zero details
+// (nothing zeroed: the skip rule stores it raw, i.e. constant entries
+// again).  Only patch rows whose neighbours live in this shard qualify.
+template <int N, int L>
+__device__ __forceinline__ bool swe_still_water(const StepArgs& a, uint32_t p, const PatchPos& pp,
+                                                const ShardGeom& g) {
+    if (g.world > 1 && (pp.ar == 0 || pp.ar == (int)g.R - 1)) return false;
+    const DirEntry* d = a.dir_in;
+    const DirEntry e0 = d[(size_t)p * 3], e1 = d[(size_t)p * 3 + 1], e2 = d[(size_t)p * 3 + 2];
+    if (!(e0.flags & DIR_CONST) || !(e1.flags & DIR_CONST) || !(e2.flags & DIR_CONST) || e1.off || e2.off)
+        return false;
+    const double h = __longlong_as_double((long long)e0.off);
+    if (!(h > 0.0) || h < a.thr[0]) return false;  // the samples are kept (band 0 x 0)
+    const uint32_t up = (uint32_t)((pp.ar + (int)g.R - 1) % (int)g.R) * g.P1 + pp.b;
+    const uint32_t dn = (uint32_t)((pp.ar + 1) % (int)g.R) * g.P1 + pp.b;
+    const uint32_t nb[4] = {up, dn, (uint32_t)pp.ar * g.P1 + pp.bl, (uint32_t)pp.ar * g.P1 + pp.br};
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+            const DirEntry e = d[(size_t)nb[k] * 3 + q];
+            if (!(e.flags & DIR_CONST) || e.off != (q == 0 ? e0.off : 0ull)) return false;
+        }
+    return true;
+}
+
 template <int N, int L, int MODE>
 __global__ void __launch_bounds__(SweLayout<N>::NT, WG_SWE_MIN_BLOCKS) k_swe_step(const __grid_constant__ StepArgs a) {
     using Lay = SweLayout<N>;
@@ -113,6 +144,40 @@ __global__ void __launch_bounds__(SweLayout<N>::NT, WG_SWE_MIN_BLOCKS) k_swe_ste
         const uint32_t p = p_next;
         if (p >= g.npatch) break;  // uniform
         const PatchPos pp = patch_pos(p, g);
+        double m = 0.0, mfv = 0.0;  // the patch's masses (reconstruction, scheme output)
+        // still water (swe_still_water, every thread evaluates it: uniform):
+        // the cycle's outputs written directly — the same entries, edge
+        // lines, counts, masses and wave speed, with the same operations
+        if (MODE == MODE_STEP && a.compress && a.thr_any && swe_still_water<N, L>(a, p, pp, g)) {
+            __syncthreads();  // every thread has read p
+            const DirEntry e0 = a.dir_in[(size_t)p * 3];
+            const double h = __longlong_as_double((long long)e0.off);
+            if (t == 0) {
+                p_next = atomicAdd(a.work, 1u);
+#pragma unroll
+                for (int sl = 0; sl < 3; ++sl)
+                    a.dir_out[(size_t)p * 3 + sl] = DirEntry{sl == 0 ? e0.off : 0ull, 0u, DIR_RAW | DIR_CONST};
+                constexpr uint64_t kept = (uint64_t)(((N - 1) >> L) + 1) * (uint64_t)(((N - 1) >> L) + 1);
+                part.comp_bytes += 12ull * kept + 3ull * 4ull * (N + 1);  // CSR sizes of (h, 0, 0)
+                part.nnz += kept;
+            }
+            if (lane_ok) {
+                double v[N];
+#pragma unroll
+                for (int i = 0; i < N; ++i) v[i] = s == 0 ? h : 0.0;
+                write_edges<N>(a.eout, pp, s, g, li, v);
+                if (s == 0) m = col_mass<N>(li, v);
+            }
+            for (int c = t; c < NN; c += NT) {
+                const int i = c / N, j = c - (c / N) * N;
+                mfv += (((i == 0 || i == N - 1) ? 0.5 : 1.0) * ((j == 0 || j == N - 1) ? 0.5 : 1.0)) * h;
+            }
+            if (t < NN) {
+                const double cc = sqrt(a.gravity * h);
+                const double u = fabs(0.0 / h);
+                vmax = fmax(vmax, fmax(u + cc, u + cc));
+            }
+        } else {
         // ---- decode h, hu, hv + ghost ring --------------------------------
         bool raw_in = false;
         if (lane_ok) {
@@ -134,7 +199,6 @@ __global__ void __launch_bounds__(SweLayout<N>::NT, WG_SWE_MIN_BLOCKS) k_swe_ste
         const double* T1 = tiles + TILE;
         const double* T2 = tiles + 2 * TILE;
         const int di[4] = {1, -1, 0, 0}, dj[4] = {0, 0, 1, -1};  // +x, -x, +y, -y
-        double mfv = 0.0;
         for (int c = t; c < NN; c += NT) {
             const int i = c / N, j = c - (c / N) * N;
             const int o = (i + 1) * TP + j + 1;
@@ -163,7 +227,6 @@ __global__ void __launch_bounds__(SweLayout<N>::NT, WG_SWE_MIN_BLOCKS) k_swe_ste
         __syncthreads();
         WG_PHASE_MARK(2);
 
-        double m = 0.0;
         bool store_raw = !a.compress;
         if (a.compress) {
             if (t == 0) {
@@ -297,6 +360,7 @@ __global__ void __launch_bounds__(SweLayout<N>::NT, WG_SWE_MIN_BLOCKS) k_swe_ste
             __syncthreads();
             WG_PHASE_MARK(9);
         }
+        }  // general path
         // the patch's masses (fixed order: warp trees, then warps in order)
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
